@@ -16,7 +16,8 @@ LR record (exactly 70 bytes, fixed-width CSV, zero-padded digits):
 
 CM record (one '\\n'-terminated CSV line, 13 columns, Google task_events order):
   ts,missing,jobId,taskIndex,machineId,eventType,user,category,priority,cpu,ram,disk,constraint
-  valid iff: exactly 13 comma-separated fields; ts = 1..9 digits; missing is
+  valid iff: the line (without '\\n') is at most 255 bytes and was
+  '\\n'-terminated; exactly 13 comma-separated fields; ts = 1..9 digits; missing is
   empty; jobId = 1..19 digits; eventType = 1 digit; category = 1 digit;
   cpu = D.DDDDDD (one digit, '.', six digits).  Other fields are free text
   without ',' or '\\n'.
@@ -36,6 +37,7 @@ LR_FIELDS = {
     "lane": (28, 29), "dir": (30, 31), "seg": (32, 35),
 }
 DIGITS = b"0123456789"
+CM_MAX_LINE = 255          # bytes before the '\n' (reading R1: longer lines are malformed)
 
 
 @dataclass(frozen=True)
@@ -100,6 +102,8 @@ def _digits(s: bytes, lo: int, hi: int) -> bool:
 
 def parse_cm_record(line: bytes):
     """Decode one CM line (without its '\\n'); return CMRecord or None if invalid."""
+    if len(line) > CM_MAX_LINE:
+        return None
     f = line.split(b",")
     if len(f) != 13:
         return None
@@ -119,13 +123,15 @@ def parse_cm_record(line: bytes):
                     cat=int(f[7].decode()), cpu_m=cpu_m)
 
 
-def frame_cm(data: bytes) -> list[bytes]:
-    """Newline framing: the records are the '\\n'-terminated lines of the dataset."""
-    if data and data[-1] != ord("\n"):
-        raise ValueError("CM dataset does not end with a newline")
+def frame_cm(data: bytes) -> tuple[list[bytes], int]:
+    """Newline framing: the records are the '\\n'-terminated lines of the dataset.
+
+    Returns (lines, n_unterminated): bytes after the last '\\n' form one
+    unterminated (hence malformed) record.
+    """
     lines = data.split(b"\n")
-    assert lines[-1] == b""
-    return lines[:-1]
+    tail = lines.pop()
+    return lines, (1 if tail else 0)
 
 
 def parse_dataset(family: str, data: bytes, num_xways: int = 10):
@@ -139,7 +145,9 @@ def parse_dataset(family: str, data: bytes, num_xways: int = 10):
             else:
                 out.append(r)
     elif family == "CM":
-        for line in frame_cm(data):
+        lines, unterminated = frame_cm(data)
+        bad += unterminated
+        for line in lines:
             r = parse_cm_record(line)
             if r is None:
                 bad += 1

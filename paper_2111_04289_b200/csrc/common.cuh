@@ -1,0 +1,219 @@
+// Device helpers shared by the LMStream kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.h"
+
+namespace lms {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// ---- mbarrier + 1-D bulk copy (TMA engine, UBLKCP) -------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAIT;\n}" ::"r"(smem_addr(b)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared, bytes % 16 == 0, both addresses 16-byte aligned; completes on mbarrier b.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
+// ---- arithmetic ----------------------------------------------------------------------
+// pane = ts / S exactly for ts < 2^32, S <= 2^31 (magic = ceil(2^64 / S), S > 1).
+__device__ __forceinline__ uint32_t pane_of(uint32_t ts, uint32_t S, unsigned long long magic) {
+  return S == 1 ? ts : (uint32_t)__umul64hi((unsigned long long)ts, magic);
+}
+
+__device__ __forceinline__ long long floor_div(long long a, long long b) {
+  long long q = a / b;
+  if ((a % b != 0) && ((a < 0) != (b < 0))) q--;
+  return q;
+}
+
+__device__ __forceinline__ unsigned long long fmix64(unsigned long long k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdull;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33;
+  return k;
+}
+
+// Dictionary lookup-or-insert: key -> dense index < max_keys; kEmpty32 on overflow.
+__device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long key, DevState* st) {
+  unsigned long long h = fmix64(key) & d.cap_mask;
+  while (true) {
+    unsigned long long k = *(volatile unsigned long long*)&d.keys[h];
+    if (k == key || k == kEmpty64) {
+      if (k == kEmpty64) {
+        k = atomicCAS(&d.keys[h], kEmpty64, key);
+        if (k == kEmpty64) {   // we own the slot: allocate the index and publish it
+          uint32_t idx = atomicAdd(&st->n_keys, 1u);
+          if (idx >= d.max_keys) {
+            atomicExch(&st->key_overflow, 1u);
+            idx = kEmpty32 - 1;   // poison: entry exists but is unusable
+          } else {
+            d.key_by_idx[idx] = key;
+          }
+          __threadfence();
+          atomicExch(&d.vals[h], idx);
+          return idx >= d.max_keys ? kEmpty32 : idx;
+        }
+      }
+      if (k == key) {
+        uint32_t v;
+        while ((v = *(volatile uint32_t*)&d.vals[h]) == kEmpty32) { }
+        return v >= d.max_keys ? kEmpty32 : v;
+      }
+    }
+    h = (h + 1) & d.cap_mask;
+  }
+}
+
+// ---- pane table: pane index -> accumulator slot ------------------------------------------
+__device__ __forceinline__ uint32_t pane_hash(uint32_t p, uint32_t mask) { return (p * 0x9E3779B1u) & mask; }
+
+// Accumulator slot of pane p, allocating one on first sight; kFail32 if all P slots are live.
+// Called rarely (threads cache the last pane they resolved).
+__device__ __forceinline__ uint32_t claim_slot(const QueryDev& q, uint32_t p) {
+  uint32_t h = pane_hash(p, q.H_mask);
+  while (true) {
+    uint32_t k = *(volatile uint32_t*)&q.pane_key[h];
+    if (k == kEmpty32) {
+      k = atomicCAS(&q.pane_key[h], kEmpty32, p);
+      if (k == kEmpty32) {   // we inserted p: allocate a slot and publish it
+        const int top = atomicSub(&q.state->free_top, 1) - 1;
+        uint32_t s = kFail32;
+        if (top >= 0) {
+          s = q.free_stack[top];
+          q.slot_pane[s] = p;
+        } else {
+          atomicAdd(&q.state->free_top, 1);
+        }
+        __threadfence();
+        atomicExch(&q.pane_slot[h], s);
+        return s;
+      }
+    }
+    if (k == p) {
+      uint32_t s;
+      while ((s = *(volatile uint32_t*)&q.pane_slot[h]) == kEmpty32) { }
+      return s;
+    }
+    h = (h + 1) & q.H_mask;
+  }
+}
+
+// Lookup only (no concurrent inserts may run): slot of pane p or kEmpty32.
+__device__ __forceinline__ uint32_t find_slot(const QueryDev& q, long long p) {
+  if (p < 0 || p > 0xFFFFFFF0ll) return kEmpty32;
+  uint32_t h = pane_hash((uint32_t)p, q.H_mask);
+  while (true) {
+    const uint32_t k = q.pane_key[h];
+    if (k == kEmpty32) return kEmpty32;
+    if (k == (uint32_t)p) {
+      const uint32_t s = q.pane_slot[h];
+      return s == kFail32 ? kEmpty32 : s;
+    }
+    h = (h + 1) & q.H_mask;
+  }
+}
+
+// Single thread, no concurrent access: free every slot holding a pane <= upto, then rebuild
+// the pane hash table from the live slots (the table is tiny: H = pow2 >= 4P).
+__device__ __forceinline__ void evict_and_rebuild(const QueryDev& q, long long upto) {
+  for (uint32_t h = 0; h <= q.H_mask; h++) { q.pane_key[h] = kEmpty32; q.pane_slot[h] = kEmpty32; }
+  int top = 0;
+  for (uint32_t s = 0; s < q.P; s++) {
+    const uint32_t p = q.slot_pane[s];
+    if (p != kEmpty32 && (long long)p <= upto) q.slot_pane[s] = kEmpty32;
+    if (q.slot_pane[s] == kEmpty32) { q.free_stack[top++] = s; continue; }
+    uint32_t h = pane_hash(q.slot_pane[s], q.H_mask);
+    while (q.pane_key[h] != kEmpty32) h = (h + 1) & q.H_mask;
+    q.pane_key[h] = q.slot_pane[s];
+    q.pane_slot[h] = s;
+  }
+  q.state->free_top = top;
+}
+
+// Per-CTA pane slots (2, tags in smem: acc slot << 32 | pane).  Sets lslot = 0/1 (local table)
+// or 2 (not local: use the global accumulators directly) and gslot = accumulator slot / kFail32.
+__device__ __forceinline__ void local_slot(unsigned long long* slot_tag, const QueryDev& q, uint32_t p,
+                                           uint32_t& lslot, uint32_t& gslot) {
+  for (int sl = 0; sl < 2; sl++) {
+    unsigned long long tg = *(volatile unsigned long long*)&slot_tag[sl];
+    if (tg == kEmpty64) {
+      const unsigned long long want = ((unsigned long long)claim_slot(q, p) << 32) | p;
+      tg = atomicCAS(&slot_tag[sl], kEmpty64, want);
+      if (tg == kEmpty64) tg = want;
+    }
+    if ((uint32_t)tg == p) { lslot = sl; gslot = (uint32_t)(tg >> 32); return; }
+  }
+  lslot = 2;
+  gslot = claim_slot(q, p);
+}
+
+// ---- block reductions (blockDim multiple of 32, <= 1024) ----------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
+
+// Per-CTA counters flushed once per CTA (one atomic per counter per CTA).
+struct CtaCounters {
+  unsigned long long n, bad, late, overflow;
+  uint32_t ts_min, ts_max1;   // ts_max1 = max ts + 1 (0 = none)
+};
+
+__device__ __forceinline__ void flush_counters(CtaCounters c, DevState* st) {
+  __shared__ unsigned long long s_n[32], s_bad[32], s_late[32], s_ovf[32];
+  __shared__ uint32_t s_min[32], s_max[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  c.n = warp_sum(c.n); c.bad = warp_sum(c.bad); c.late = warp_sum(c.late); c.overflow = warp_sum(c.overflow);
+  c.ts_min = warp_min_u32(c.ts_min); c.ts_max1 = warp_max_u32(c.ts_max1);
+  if (lane == 0) { s_n[w] = c.n; s_bad[w] = c.bad; s_late[w] = c.late; s_ovf[w] = c.overflow;
+                   s_min[w] = c.ts_min; s_max[w] = c.ts_max1; }
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long n = lane < nw ? s_n[lane] : 0, bad = lane < nw ? s_bad[lane] : 0;
+    unsigned long long late = lane < nw ? s_late[lane] : 0, ovf = lane < nw ? s_ovf[lane] : 0;
+    uint32_t mn = lane < nw ? s_min[lane] : kEmpty32, mx = lane < nw ? s_max[lane] : 0;
+    n = warp_sum(n); bad = warp_sum(bad); late = warp_sum(late); ovf = warp_sum(ovf);
+    mn = warp_min_u32(mn); mx = warp_max_u32(mx);
+    if (lane == 0) {
+      if (n) atomicAdd(&st->n_records, n);
+      if (bad) atomicAdd(&st->bad, bad);
+      if (late) atomicAdd(&st->late, late);
+      if (ovf) atomicAdd(&st->overflow, ovf);
+      if (mn != kEmpty32) atomicMin(&st->ts_min, mn);
+      if (mx) atomicMax(&st->wm, (unsigned long long)mx);
+    }
+  }
+}
+
+}  // namespace lms

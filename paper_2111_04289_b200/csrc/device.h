@@ -1,0 +1,128 @@
+// Device-side data layout of the LMStream hot path and the kernel launchers.
+//
+// HBM layout per query (one GPU):
+//   input        : raw record bytes of the micro-batch (host-pushed block, 16 B aligned,
+//                  + borrowed device datasets), read once by the aggregate kernel
+//   pane table   : P accumulator slots; pane index floor(ts/S) -> slot through an open-
+//                  addressing table pane_key/pane_slot[H] (H >= 4P, rebuilt at eviction) and a
+//                  free-slot stack, so only the number of DISTINCT live panes is bounded (not
+//                  their span); a window instance k = [kS, kS+R) is panes k .. k+R/S-1 (R5, R19)
+//   accumulators : acc_sum[P][K], acc_cnt[P][K] (u64, exact integer sums: LR speed, CM
+//                  cpu*1e6), LR1: acc_cnt32[P][K]
+//   partials     : per aggregate-CTA smem tables written as u32 (LR2) / u64 (CM1)
+//                  part[C][2 slots][2][K], merged by the close kernel per key slice
+//   dictionary   : open-addressing jobId / vehicle -> dense index (CM2, LR1)
+//   rows         : result rows of the batch (lms_agg_row / lms_lr1_row)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lms {
+
+constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
+constexpr uint32_t kFail32 = 0xFFFFFFFEu;   // pane table full: the pane's records overflow
+constexpr unsigned long long kEmpty64 = ~0ull;
+constexpr int kMaxSegs = 16;
+constexpr int kLrRecBytes = 70;
+constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records
+constexpr int kLrTileBytes = kLrTileRecs * kLrRecBytes; // 35840 = 16 * 2240
+constexpr int kCmTile = 32768;                         // CM tile payload bytes
+constexpr int kCmHaloL = 16;
+constexpr int kCmHaloR = 256;                          // >= max line (255) + '\n'
+constexpr int kCmStage = kCmHaloL + kCmTile + kCmHaloR;
+constexpr int kCmMaxLine = 255;
+
+enum QueryKind : int32_t { kLR1S = 0, kLR1T = 1, kLR2S = 2, kCM1S = 3, kCM1T = 4, kCM2S = 5 };
+
+// Device-resident query state (one per query).
+struct DevState {
+  unsigned long long wm;        // live watermark: max kept ts + 1 (0 = none)
+  unsigned long long wm_prev;   // snapshot at batch start: late iff ts + 1 < wm_prev
+  long long next_k;             // first window instance not yet emitted
+  long long evict_upto;         // LR1: panes <= this are evicted by k_lr1_evict
+  unsigned int next_k_valid;
+  unsigned int ts_min;          // min kept ts of the current batch (0xFFFFFFFF = none)
+  unsigned long long n_records, bad, late, overflow, rows, windows_closed;
+  unsigned int row_overflow;
+  unsigned int close_ticket;
+  unsigned int n_keys;          // dictionary entries in use
+  unsigned int key_overflow;
+  unsigned int fifo_count[2];   // LR1 retained-row FIFO sizes
+  unsigned int fifo_cur;        // LR1: which FIFO holds the live rows
+  unsigned int fifo_overflow;
+  int free_top;                 // free accumulator slots on the stack
+};
+
+// Copied to the host after every batch.
+struct BatchReport {
+  unsigned long long n_records, bad, late, overflow, rows, windows_closed;
+  long long watermark;          // -1 if none
+  unsigned int n_keys, row_overflow, key_overflow, fifo_overflow;
+};
+
+struct Segment {
+  const uint8_t* ptr;
+  unsigned long long nbytes;
+};
+
+struct SegTable {
+  int n;
+  Segment s[kMaxSegs];
+  unsigned long long tile_prefix[kMaxSegs + 1];   // tiles before segment i
+};
+
+// Retained LR1 row (projection of the 7 output columns; vehicle via dictionary index).
+struct Lr1Retained {
+  uint32_t ts;
+  uint32_t vidx;
+  uint16_t speed, xway, seg;
+  uint8_t lane, dir;
+};
+
+struct Dict {
+  unsigned long long* keys;     // [cap], kEmpty64 = free
+  uint32_t* vals;               // [cap], kEmpty32 until published
+  unsigned long long* key_by_idx;  // [max_keys]
+  unsigned long long cap_mask;
+  uint32_t max_keys;
+};
+
+struct QueryDev {
+  int kind;
+  uint32_t S, R, ppw, P;        // slide, range (s), panes per window, ring slots
+  unsigned long long div_magic; // ceil(2^64 / S) for pane = ts / S (S > 1)
+  uint32_t num_xways;
+  uint32_t K;                   // key-space size of the accumulators
+  DevState* state;
+  BatchReport* report;
+  uint32_t* pane_key;           // [H] pane index or kEmpty32
+  uint32_t* pane_slot;          // [H] accumulator slot (kEmpty32 until published, kFail32)
+  uint32_t H_mask;              // H - 1
+  uint32_t* slot_pane;          // [P] pane held by accumulator slot s (kEmpty32 = free)
+  uint32_t* free_stack;         // [P]
+  unsigned long long* acc_sum;  // [P][K]
+  unsigned long long* acc_cnt;  // [P][K]
+  uint32_t* acc_cnt32;          // LR1 [P][K]
+  uint32_t* part32;             // LR2 [C][2][2][K]
+  unsigned long long* part64;   // CM1 [C][2][2][K]
+  unsigned long long* part_tag; // [C][2] (slot << 32 | pane), kEmpty64 = unused
+  uint32_t n_agg_ctas;          // C
+  Dict dict;
+  void* rows;                   // lms_agg_row[] / lms_lr1_row[]
+  unsigned long long row_cap;
+  Lr1Retained* fifo[2];
+  unsigned long long fifo_cap;
+};
+
+// Launchers (kernels_*.cu).  All asynchronous on `st`.
+int lr_agg_ctas(const QueryDev& q);
+int cm_agg_ctas(const QueryDev& q);
+size_t lr_agg_smem(const QueryDev& q);
+cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
+cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
+cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st);
+cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st);
+cudaError_t launch_state_init(const QueryDev& q, cudaStream_t st);
+int close_ctas(const QueryDev& q);
+
+}  // namespace lms

@@ -1,0 +1,357 @@
+// Window close / slide (all queries) and LR1 pane eviction.
+//
+// PAPER.md Table IV windows: "[range R slide S]", tumbling when SlideTime = 0
+// (Table I).  Emission rule and window alignment: DESIGN.md readings R5, R7, R19.
+// An instance k = [kS, kS+R) is the union of panes k .. k+R/S-1; a pane is evicted as soon
+// as the last instance containing it has been emitted (pane state carried between batches).
+//
+// One launch per micro-batch.  Every CTA owns a slice of the key space and, for that slice,
+//   1. merges the aggregate kernel's per-CTA partials into the pane accumulators (LR2),
+//   2. emits every instance k in [next_k, k_last] (k_last = floor((W-R)/S), flush:
+//      floor(W/S)): SUM/COUNT over its panes, AVG = SUM/COUNT in fp64, HAVING avg < 40.0
+//      (LR2), ORDER BY SUM(cpu) rank (CM1), one row per non-empty group,
+//   3. zeroes its slice of every pane <= k_last.
+// The slices are disjoint, so no grid barrier is needed; the last CTA (atomic ticket)
+// resets the ring tags, advances next_k / the watermark snapshot and writes the batch report.
+// LR1 instead probes the retained rows of each closing instance's newest slide against the
+// summed per-pane vehicle counts (bag multiplicity, reading R8) and compacts the FIFO.
+#include "../../include/lmstream.h"
+#include "common.cuh"
+
+namespace lms {
+namespace {
+
+constexpr int kCloseThreads = 256;
+
+struct CloseArgs {
+  QueryDev q;
+  int flush;
+};
+
+struct WinRange {
+  long long nk, k_last;
+  bool any;   // data was ever seen
+};
+
+__device__ __forceinline__ WinRange win_range(const QueryDev& q, int flush) {
+  const DevState* st = q.state;
+  WinRange w{0, -1, false};
+  const unsigned long long wm = st->wm;
+  if (wm == 0) return w;
+  w.any = true;
+  const long long W = (long long)wm - 1;
+  if (st->next_k_valid) w.nk = st->next_k;
+  else w.nk = floor_div((long long)st->ts_min - (long long)q.R, (long long)q.S) + 1;
+  w.k_last = flush ? floor_div(W, (long long)q.S) : floor_div(W - (long long)q.R, (long long)q.S);
+  return w;
+}
+
+// Resolve the accumulator slots of instance k's panes into smem (kEmpty32: pane never seen).
+__device__ __forceinline__ void window_slots(const QueryDev& q, long long k, uint32_t* slots) {
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < q.ppw; j += blockDim.x) slots[j] = find_slot(q, k + j);
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long row_slot(DevState* st, bool want) {
+  // warp-aggregated append to the result buffer
+  const uint32_t m = __ballot_sync(__activemask(), want);
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  const int leader = m ? __ffs(m) - 1 : 0;
+  if (m && (int)lane == leader) base = atomicAdd(&st->rows, (unsigned long long)__popc(m));
+  base = __shfl_sync(__activemask(), base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+__device__ void finish(const QueryDev& q, const WinRange& w, int flush) {
+  // last CTA: ring tags, state advance, report.
+  DevState* st = q.state;
+  const bool lr1 = (q.kind == kLR1S || q.kind == kLR1T);
+  if (w.any) {
+    const long long closed = w.k_last >= w.nk ? (w.k_last - w.nk + 1) : 0;
+    st->windows_closed += (unsigned long long)closed;
+    if (!lr1) evict_and_rebuild(q, w.k_last);   // LR1: k_lr1_evict frees the slots
+    st->evict_upto = w.k_last;
+    st->next_k = w.k_last + 1 > w.nk ? w.k_last + 1 : w.nk;
+    st->next_k_valid = 1;
+  }
+  if (q.kind == kLR2S)
+    for (uint32_t i = 0; i < 2 * q.n_agg_ctas; i++) q.part_tag[i] = kEmpty64;
+  if (lr1) {
+    st->fifo_count[st->fifo_cur] = 0;
+    st->fifo_cur ^= 1u;
+  }
+  st->wm_prev = st->wm;
+  BatchReport* r = q.report;
+  r->n_records = st->n_records; r->bad = st->bad; r->late = st->late; r->overflow = st->overflow;
+  r->rows = st->rows; r->windows_closed = st->windows_closed;
+  r->watermark = st->wm ? (long long)st->wm - 1 : -1;
+  r->n_keys = st->n_keys; r->row_overflow = st->row_overflow; r->key_overflow = st->key_overflow;
+  r->fifo_overflow = st->fifo_overflow;
+  st->n_records = st->bad = st->late = st->overflow = st->rows = st->windows_closed = 0;
+  st->row_overflow = 0;
+  st->fifo_overflow = 0;
+  st->key_overflow = 0;
+  st->ts_min = kEmpty32;
+  (void)flush;
+}
+
+__device__ __forceinline__ void ticket(const QueryDev& q, const WinRange& w, int flush) {
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t t = atomicAdd(&q.state->close_ticket, 1u);
+    last = (t == gridDim.x - 1);
+    if (last) {
+      __threadfence();
+      finish(q, w, flush);
+      q.state->close_ticket = 0;
+      __threadfence();
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) {
+  const QueryDev& q = a.q;
+  DevState* st = q.state;
+  const WinRange w = win_range(q, a.flush);
+  const uint32_t K = (q.kind == kCM2S) ? min(st->n_keys, q.K) : q.K;
+  const uint32_t k0 = (uint32_t)((unsigned long long)K * blockIdx.x / gridDim.x);
+  const uint32_t k1 = (uint32_t)((unsigned long long)K * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t P = q.P;
+  __shared__ uint32_t wslots[256];   // ppw <= 256
+
+  // 1. merge LR2 partials of this batch into the pane accumulators (my key slice)
+  if (q.kind == kLR2S) {
+    for (uint32_t c = 0; c < q.n_agg_ctas; c++) {
+      for (int sl = 0; sl < 2; sl++) {
+        const unsigned long long tg = q.part_tag[c * 2 + sl];
+        if (tg == kEmpty64) continue;
+        const size_t g = (size_t)(tg >> 32) * q.K;
+        uint32_t* part = q.part32 + ((size_t)c * 4 + sl * 2) * q.K;
+        for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+          const uint32_t cv = part[q.K + k];
+          if (cv) {
+            q.acc_sum[g + k] += part[k];
+            q.acc_cnt[g + k] += cv;
+            part[k] = 0;
+            part[q.K + k] = 0;
+          }
+        }
+      }
+    }
+  }
+
+  // 2. emit closing instances
+  if (w.any && w.k_last >= w.nk) {
+    lms_agg_row* rows = reinterpret_cast<lms_agg_row*>(q.rows);
+    for (long long k = w.nk; k <= w.k_last; k++) {
+      window_slots(q, k, wslots);
+      if (q.kind == kCM1S || q.kind == kCM1T) {
+        // single CTA (grid = 1); K <= 10 categories; ORDER BY SUM(cpu), ties by category (R9)
+        __shared__ unsigned long long s_sum[10], s_cnt[10];
+        if (threadIdx.x < 10) {
+          unsigned long long s = 0, c = 0;
+          for (uint32_t j = 0; j < q.ppw; j++) {
+            const uint32_t g = wslots[j];
+            if (g != kEmpty32) { s += q.acc_sum[(size_t)g * q.K + threadIdx.x];
+                                 c += q.acc_cnt[(size_t)g * q.K + threadIdx.x]; }
+          }
+          s_sum[threadIdx.x] = s;
+          s_cnt[threadIdx.x] = c;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          const uint32_t c = threadIdx.x;
+          const bool want = c < 10 && s_cnt[c] > 0;
+          uint32_t rank = 0;
+          if (want)
+            for (uint32_t j = 0; j < 10; j++)
+              if (s_cnt[j] > 0 && (s_sum[j] < s_sum[c] || (s_sum[j] == s_sum[c] && j < c))) rank++;
+          const unsigned long long pos = row_slot(st, want);
+          if (want) {
+            if (pos < q.row_cap) {
+              lms_agg_row r;
+              r.win_start_s = k * (long long)q.S;
+              r.win_end_s = r.win_start_s + (long long)q.R;
+              r.key = c; r.count = s_cnt[c]; r.sum_fixed = s_sum[c];
+              r.sum = (double)s_sum[c] / 1e6;
+              r.avg = r.sum / (double)s_cnt[c];
+              r.key_xway = r.key_dir = r.key_seg = 0;
+              r.rank = rank;
+              rows[pos] = r;
+            } else {
+              atomicExch(&st->row_overflow, 1u);
+            }
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      // LR2 / CM2: one thread per key of my slice
+      for (uint32_t kb = k0; kb < k1; kb += blockDim.x) {
+        const uint32_t key = kb + threadIdx.x;
+        unsigned long long s = 0, c = 0;
+        if (key < k1) {
+          for (uint32_t j = 0; j < q.ppw; j++) {
+            const uint32_t g = wslots[j];
+            if (g != kEmpty32) { s += q.acc_sum[(size_t)g * q.K + key];
+                                 c += q.acc_cnt[(size_t)g * q.K + key]; }
+          }
+        }
+        bool want = c > 0;
+        double sum, avg;
+        if (q.kind == kLR2S) {
+          sum = (double)s;                 // integer speed sum, exact below 2^53
+          avg = want ? sum / (double)c : 0.0;
+          want = want && (avg < 40.0);     // HAVING (avgSpeed < 40.0)
+        } else {
+          sum = (double)s / 1e6;           // SUM(cpu) from the exact fixed-point sum (R20)
+          avg = want ? sum / (double)c : 0.0;
+        }
+        const unsigned long long pos = row_slot(st, want);
+        if (want) {
+          if (pos < q.row_cap) {
+            lms_agg_row r;
+            r.win_start_s = k * (long long)q.S;
+            r.win_end_s = r.win_start_s + (long long)q.R;
+            r.count = c; r.sum_fixed = s; r.sum = sum; r.avg = avg; r.rank = 0;
+            if (q.kind == kLR2S) {
+              r.key = key; r.key_xway = key / 200u; r.key_dir = (key / 100u) % 2u; r.key_seg = key % 100u;
+            } else {
+              r.key = q.dict.key_by_idx[key]; r.key_xway = r.key_dir = r.key_seg = 0;
+            }
+            rows[pos] = r;
+          } else {
+            atomicExch(&st->row_overflow, 1u);
+          }
+        }
+      }
+    }
+  }
+
+  // 3. evict panes whose last instance has been emitted (my key slice)
+  if (w.any) {
+    const uint32_t kk0 = (q.kind == kCM1S || q.kind == kCM1T) ? 0 : k0;
+    const uint32_t kk1 = (q.kind == kCM1S || q.kind == kCM1T) ? q.K : k1;
+    __syncthreads();
+    for (uint32_t g = 0; g < P; g++) {
+      const uint32_t p = q.slot_pane[g];
+      if (p == kEmpty32 || (long long)p > w.k_last) continue;
+      for (uint32_t k = kk0 + threadIdx.x; k < kk1; k += blockDim.x) {
+        q.acc_sum[(size_t)g * q.K + k] = 0;
+        q.acc_cnt[(size_t)g * q.K + k] = 0;
+      }
+    }
+  }
+  ticket(q, w, a.flush);
+}
+
+// LR1: probe retained rows whose pane is the newest slide of a closing instance.
+__global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) {
+  const QueryDev& q = a.q;
+  DevState* st = q.state;
+  const WinRange w = win_range(q, a.flush);
+  const uint32_t cur = st->fifo_cur;
+  const uint32_t n = min((unsigned long long)st->fifo_count[cur], q.fifo_cap);
+  const Lr1Retained* src = q.fifo[cur];
+  Lr1Retained* dst = q.fifo[cur ^ 1u];
+  lms_lr1_row* rows = reinterpret_cast<lms_lr1_row*>(q.rows);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t iters = (n + stride - 1) / stride;
+  for (uint32_t it = 0; it < iters; it++) {
+    const uint32_t i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    bool emit = false, keep = false;
+    Lr1Retained r{};
+    long long k = 0;
+    uint32_t m = 0;
+    if (i < n) {
+      r = src[i];
+      const long long p = (long long)pane_of(r.ts, q.S, q.div_magic);
+      k = p - (long long)q.ppw + 1;              // instance whose newest slide is pane p
+      if (w.any && k <= w.k_last) {
+        emit = true;
+        for (long long j = k; j <= p; j++) {
+          const uint32_t g = find_slot(q, j);
+          if (g != kEmpty32) m += q.acc_cnt32[(size_t)g * q.K + r.vidx];
+        }
+      } else {
+        keep = true;
+      }
+    }
+    const unsigned long long pos = row_slot(st, emit);
+    if (emit) {
+      if (pos < q.row_cap) {
+        lms_lr1_row o;
+        o.win_start_s = k * (long long)q.S;
+        o.vehicle = q.dict.key_by_idx[r.vidx];
+        o.ts = r.ts; o.multiplicity = m; o.speed = r.speed; o.xway = r.xway; o.segment = r.seg;
+        o.lane = r.lane; o.dir = r.dir;
+        rows[pos] = o;
+      } else {
+        atomicExch(&st->row_overflow, 1u);
+      }
+    }
+    // compaction of the rows still needed into the other FIFO
+    const uint32_t km = __ballot_sync(0xffffffffu, keep);
+    uint32_t base = 0;
+    if ((threadIdx.x & 31) == 0 && km) base = atomicAdd(&st->fifo_count[cur ^ 1u], __popc(km));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) dst[base + __popc(km & ((1u << (threadIdx.x & 31)) - 1u))] = r;
+  }
+  ticket(q, w, a.flush);
+}
+
+// LR1: zero the vehicle counts of evicted panes, then (last CTA) free their ring slots.
+__global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
+  DevState* st = q.state;
+  const long long upto = st->evict_upto;
+  const uint32_t nk = min(st->n_keys, q.K);
+  for (uint32_t g = 0; g < q.P; g++) {
+    const uint32_t p = q.slot_pane[g];
+    if (p == kEmpty32 || (long long)p > upto) continue;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += gridDim.x * blockDim.x)
+      q.acc_cnt32[(size_t)g * q.K + k] = 0;
+  }
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&st->close_ticket, 1u) == gridDim.x - 1;
+    if (last) {
+      __threadfence();
+      evict_and_rebuild(q, upto);
+      st->close_ticket = 0;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace
+
+int close_ctas(const QueryDev& q) {
+  if (q.kind == kCM1S || q.kind == kCM1T) return 1;
+  static int nsm = -1;
+  if (nsm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+
+cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {
+  CloseArgs a{q, flush};
+  if (q.kind == kLR1S || q.kind == kLR1T) k_close_lr1<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+  else k_close_agg<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st) {
+  k_lr1_evict<<<close_ctas(q), kCloseThreads, 0, st>>>(q);
+  return cudaGetLastError();
+}
+
+}  // namespace lms

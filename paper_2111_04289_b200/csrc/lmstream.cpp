@@ -1,0 +1,757 @@
+// liblmstream: C ABI (include/lmstream.h) over the B200 micro-batch pipeline.
+//
+// Host responsibilities (§III): dataset ingest (Alg. 1 "newFiles"), admission
+// (Alg. 1 / Eq. 6, CG(dN), OS(tN)), device-preference labels (Alg. 2, Eq. 7-9, report-only:
+// execution is always the GPU path), Eq. 4 / Eq. 5 metrics, Eq. 10 online InfPT.  Device
+// work per micro-batch: one aggregate-pass launch per <= 16 input segments, one close
+// launch (+ LR1 evict), one 88 B report copy; rows are copied after completion.
+#include <cuda_runtime.h>
+
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/lmstream.h"
+#include "device.h"
+#include "host_control.h"
+
+using namespace lms;
+
+namespace {
+
+thread_local std::string g_err;
+
+lms_status fail(lms_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+#define CUDA_TRY(x)                                                                       \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) return fail(LMS_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+double now_host() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+struct Pending {
+  uint64_t id;
+  double ingest;
+  uint64_t nbytes;
+  const uint8_t* dptr;   // borrowed device buffer, or nullptr (host-pushed, in d_in)
+  double h2d_s;
+};
+
+bool table_iv(int kind, uint32_t& R, uint32_t& S) {
+  switch (kind) {   // Table IV
+    case kLR1S: R = 30; S = 5; return true;
+    case kLR1T: R = 30; S = 30; return true;
+    case kLR2S: R = 30; S = 10; return true;
+    case kCM1S: R = 60; S = 10; return true;
+    case kCM1T: R = 60; S = 60; return true;
+    case kCM2S: R = 60; S = 5; return true;
+    default: return false;
+  }
+}
+bool is_lr(int k) { return k == kLR1S || k == kLR1T || k == kLR2S; }
+bool is_tumbling(int k) { return k == kLR1T || k == kCM1T; }
+bool is_lr1(int k) { return k == kLR1S || k == kLR1T; }
+
+uint64_t next_pow2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+}  // namespace
+
+struct lms_query {
+  lms_config cfg{};
+  int kind = 0;
+  uint32_t R = 0, S = 0, ppw = 0, P = 0;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  QueryDev qd{};
+  std::vector<void*> dallocs;
+  uint8_t* d_in[2] = {nullptr, nullptr};
+  uint64_t in_cap = 0, in_used[2] = {0, 0};
+  int in_cur = 0;
+  BatchReport* h_report = nullptr;
+  std::vector<Pending> pending;
+  uint64_t next_ds_id = 0;
+  double last_ingest = -std::numeric_limits<double>::infinity();
+  // Eq. 4 / Eq. 5 / Eq. 10 history
+  std::vector<double> maxlat_hist;
+  double cum_bytes = 0, cum_proc = 0;
+  double next_trigger = 0;
+  double infpt = 150e3;
+  std::deque<std::array<double, 3>> reg_hist;
+  Dag dag;
+  // in-flight batch
+  bool in_flight = false;
+  int in_flight_buf = 0;
+  bool in_flight_flush = false;
+  cudaEvent_t ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
+  lms_batch_record cur{};
+  std::vector<lms_batch_record> records;
+  std::deque<lms_agg_row> agg_rows;
+  std::deque<lms_lr1_row> lr1_rows;
+  uint64_t launches = 0;
+  double last_batch_s = 0, last_agg_s = 0, last_close_s = 0;
+  lms_status last_completion = LMS_OK;
+
+  ~lms_query() {
+    cudaSetDevice(cfg.device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : dallocs) cudaFree(p);
+    if (h_report) cudaFreeHost(h_report);
+    for (cudaEvent_t e : {ev_start, ev_agg, ev_close, ev_end})
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+  }
+
+  template <typename T>
+  lms_status dalloc(T** p, size_t n_elems, int fill_byte) {
+    void* v = nullptr;
+    const size_t bytes = std::max<size_t>(n_elems * sizeof(T), 16);
+    cudaError_t e = cudaMalloc(&v, bytes);
+    if (e != cudaSuccess) return fail(LMS_ENOMEM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    dallocs.push_back(v);
+    e = cudaMemset(v, fill_byte, bytes);
+    if (e != cudaSuccess) return fail(LMS_ECUDA, cudaGetErrorString(e));
+    *p = static_cast<T*>(v);
+    return LMS_OK;
+  }
+};
+
+namespace {
+
+lms_status validate_config(const lms_config* c) {
+  if (!c) return fail(LMS_EINVAL, "null config");
+  if (c->struct_size != sizeof(lms_config)) return fail(LMS_EINVAL, "struct_size mismatch");
+  uint32_t R, S;
+  if (!table_iv(c->kind, R, S)) return fail(LMS_EINVAL, "unknown query kind");
+  if (c->mode < 0 || c->mode > 3) return fail(LMS_EINVAL, "unknown mode");
+  if (c->mode == LMS_MODE_TRIGGER && !(c->trigger_s > 0)) return fail(LMS_EINVAL, "trigger_s must be > 0");
+  if (c->mode == LMS_MODE_DEADLINE && !(c->deadline_s >= 0)) return fail(LMS_EINVAL, "deadline_s must be >= 0");
+  if (c->range_s < 0 || c->slide_s < 0) return fail(LMS_EINVAL, "negative window");
+  if (c->range_s != std::floor(c->range_s) || c->slide_s != std::floor(c->slide_s))
+    return fail(LMS_EINVAL, "window range/slide must be whole seconds");
+  if (c->num_cores < 1) return fail(LMS_EINVAL, "num_cores < 1");
+  if (c->num_xways < 1 || c->num_xways > 16) return fail(LMS_EINVAL, "num_xways must be 1..16");
+  if (!(c->inf_pt_bytes > 0) || !(c->base_trans_cost >= 0)) return fail(LMS_EINVAL, "bad cost constants");
+  if (c->max_batch_bytes == 0 || c->max_batch_bytes > (1ull << 40)) return fail(LMS_EINVAL, "max_batch_bytes");
+  if (c->max_keys == 0 || c->max_keys > (1ull << 30)) return fail(LMS_EINVAL, "max_keys");
+  if (c->max_result_rows == 0 || c->max_result_rows > (1ull << 32)) return fail(LMS_EINVAL, "max_result_rows");
+  return LMS_OK;
+}
+
+lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bool flush) {
+  // ---- batch composition: every pending dataset (Alg. 1 admits tmpMicroBatch whole)
+  lms_batch_record& r = q->cur;
+  r = lms_batch_record{};
+  r.index = q->records.size();
+  r.num_datasets = q->pending.size();
+  r.admit_time_s = now;
+  r.max_buff_s = 0;
+  double h2d = 0;
+  for (size_t j = 0; j < q->pending.size(); j++) {
+    const Pending& d = q->pending[j];
+    r.batch_bytes += d.nbytes;
+    r.max_buff_s = (j == 0) ? (now - d.ingest) : std::max(r.max_buff_s, now - d.ingest);   // Eq. 5 Buff
+    h2d += d.h2d_s;
+  }
+  r.h2d_s = h2d;
+  r.est_max_lat_s = est;
+  r.admit_reason = (uint32_t)reason;
+  r.inf_pt_bytes = q->infpt;
+  // ---- Alg. 2 labels (report-only)
+  {
+    const double t0 = now_host();
+    std::vector<uint8_t> dev;
+    const double part = (double)r.batch_bytes / (double)q->cfg.num_cores;
+    if (part > 0 && map_device(q->dag, part, q->infpt, q->cfg.base_trans_cost, dev)) {
+      for (size_t o = 0; o < dev.size(); o++) {
+        if (dev[o]) { r.n_gpu_ops++; r.plan_mask |= 1u << o; }
+        else r.n_cpu_ops++;
+      }
+    }
+    r.plan_overhead_s = now_host() - t0;
+  }
+  // ---- input segments
+  std::vector<Segment> segs;
+  const int buf = q->in_cur;
+  if (q->in_used[buf]) segs.push_back({q->d_in[buf], q->in_used[buf]});
+  for (const Pending& d : q->pending)
+    if (d.dptr) segs.push_back({d.dptr, d.nbytes});
+  q->pending.clear();
+  q->in_flight_buf = buf;
+  q->in_cur ^= 1;
+  q->in_used[q->in_cur] = 0;
+
+  const bool lr = is_lr(q->kind);
+  CUDA_TRY(cudaEventRecord(q->ev_start, q->stream));
+  for (size_t s0 = 0; s0 < segs.size(); s0 += kMaxSegs) {
+    SegTable t{};
+    t.n = (int)std::min<size_t>(kMaxSegs, segs.size() - s0);
+    t.tile_prefix[0] = 0;
+    for (int i = 0; i < t.n; i++) {
+      t.s[i] = segs[s0 + i];
+      const uint64_t tiles = lr ? ((t.s[i].nbytes / kLrRecBytes + kLrTileRecs - 1) / kLrTileRecs)
+                                : ((t.s[i].nbytes + kCmTile - 1) / kCmTile);
+      t.tile_prefix[i + 1] = t.tile_prefix[i] + tiles;
+    }
+    CUDA_TRY(lr ? launch_lr_agg(q->qd, t, q->stream) : launch_cm_agg(q->qd, t, q->stream));
+    q->launches++;
+  }
+  CUDA_TRY(cudaEventRecord(q->ev_agg, q->stream));
+  CUDA_TRY(launch_close(q->qd, flush ? 1 : 0, q->stream));
+  q->launches++;
+  if (is_lr1(q->kind)) {
+    CUDA_TRY(launch_lr1_evict(q->qd, q->stream));
+    q->launches++;
+  }
+  CUDA_TRY(cudaEventRecord(q->ev_close, q->stream));
+  CUDA_TRY(cudaMemcpyAsync(q->h_report, q->qd.report, sizeof(BatchReport), cudaMemcpyDeviceToHost, q->stream));
+  CUDA_TRY(cudaEventRecord(q->ev_end, q->stream));
+  q->in_flight = true;
+  q->in_flight_flush = flush;
+  return LMS_OK;
+}
+
+lms_status complete(lms_query* q) {
+  if (!q->in_flight) return LMS_OK;
+  CUDA_TRY(cudaEventSynchronize(q->ev_end));
+  q->in_flight = false;
+  lms_batch_record& r = q->cur;
+  const BatchReport rep = *q->h_report;
+  float ms_total = 0, ms_agg = 0, ms_close = 0, ms_end = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms_total, q->ev_start, q->ev_close));
+  CUDA_TRY(cudaEventElapsedTime(&ms_agg, q->ev_start, q->ev_agg));
+  CUDA_TRY(cudaEventElapsedTime(&ms_close, q->ev_agg, q->ev_close));
+  CUDA_TRY(cudaEventElapsedTime(&ms_end, q->ev_start, q->ev_end));
+  q->last_batch_s = ms_total * 1e-3;
+  q->last_agg_s = ms_agg * 1e-3;
+  q->last_close_s = ms_close * 1e-3;
+  // result rows -> host FIFO
+  const uint64_t nrows = std::min<uint64_t>(rep.rows, q->cfg.max_result_rows);
+  double d2h = 0;
+  if (nrows) {
+    const double t0 = now_host();
+    if (is_lr1(q->kind)) {
+      std::vector<lms_lr1_row> tmp(nrows);
+      CUDA_TRY(cudaMemcpy(tmp.data(), q->qd.rows, nrows * sizeof(lms_lr1_row), cudaMemcpyDeviceToHost));
+      q->lr1_rows.insert(q->lr1_rows.end(), tmp.begin(), tmp.end());
+    } else {
+      std::vector<lms_agg_row> tmp(nrows);
+      CUDA_TRY(cudaMemcpy(tmp.data(), q->qd.rows, nrows * sizeof(lms_agg_row), cudaMemcpyDeviceToHost));
+      q->agg_rows.insert(q->agg_rows.end(), tmp.begin(), tmp.end());
+    }
+    d2h = now_host() - t0;
+  }
+  q->in_used[q->in_flight_buf] = 0;
+  r.num_records = rep.n_records;
+  r.device_s = q->last_batch_s;
+  r.d2h_s = d2h;
+  r.proc_s = ms_end * 1e-3 + d2h;                            // Proc_i (reading R18)
+  r.max_lat_s = r.max_buff_s + r.proc_s;                     // Eq. 5
+  q->cum_bytes += (double)r.batch_bytes;                     // Eq. 4
+  q->cum_proc += r.proc_s;
+  r.avg_thput_Bps = q->cum_proc > 0 ? q->cum_bytes / q->cum_proc : 0;
+  r.windows_closed = rep.windows_closed;
+  r.rows_emitted = rep.rows;
+  r.late_records = rep.late;
+  r.bad_records = rep.bad;
+  r.overflow_records = rep.overflow;
+  r.watermark = rep.watermark;
+  if (r.num_datasets > 0) q->maxlat_hist.push_back(r.max_lat_s);
+  q->records.push_back(r);
+  // Eq. 10: online inflection point, optional
+  if ((q->cfg.flags & LMS_FLAG_ONLINE_INFPT) && r.num_datasets > 0) {
+    q->reg_hist.push_back({r.avg_thput_Bps, r.max_lat_s, r.inf_pt_bytes});
+    if (q->reg_hist.size() > 256) q->reg_hist.pop_front();
+    std::vector<double> th, la, ip;
+    double tmax = 0, lsum = 0;
+    for (auto& h : q->reg_hist) {
+      th.push_back(h[0]); la.push_back(h[1]); ip.push_back(h[2]);
+      tmax = std::max(tmax, h[0]);
+      lsum += h[1];
+    }
+    double b[3];
+    if (infpt_fit(th.data(), la.data(), ip.data(), th.size(), b)) {
+      const double tl = is_tumbling(q->kind) ? lsum / (double)q->reg_hist.size() : (double)q->S;
+      q->infpt = infpt_predict(b, tmax, tl);
+    }
+  }
+  lms_status st = LMS_OK;
+  if (rep.bad) st = fail(LMS_EFORMAT, "batch " + std::to_string(r.index) + ": " + std::to_string(rep.bad) +
+                                          " malformed records dropped");
+  if (rep.overflow || rep.row_overflow || rep.key_overflow || rep.fifo_overflow)
+    st = fail(LMS_EOVERFLOW, "batch " + std::to_string(r.index) + ": capacity exceeded (pane ring, keys, rows or FIFO)");
+  q->last_completion = st;
+  return st;
+}
+
+}  // namespace
+
+// =====================================================================================
+extern "C" {
+
+uint32_t lms_abi_version(void) { return LMS_ABI_VERSION; }
+const char* lms_last_error(void) { return g_err.c_str(); }
+
+lms_status lms_config_init(lms_config* c, int32_t kind) {
+  if (!c) return fail(LMS_EINVAL, "null config");
+  uint32_t R, S;
+  if (!table_iv(kind, R, S)) return fail(LMS_EINVAL, "unknown query kind");
+  *c = lms_config{};
+  c->struct_size = sizeof(lms_config);
+  c->kind = kind;
+  c->mode = LMS_MODE_LMSTREAM;
+  c->device = 0;
+  c->deadline_s = 0;
+  c->trigger_s = 10.0;              // Baseline trigger of the final paper
+  c->range_s = 0;
+  c->slide_s = 0;
+  c->num_cores = 12;                // executor size
+  c->num_xways = 10;
+  c->inf_pt_bytes = 150e3;
+  c->base_trans_cost = 0.1;
+  c->max_batch_bytes = is_lr1(kind) ? (256ull << 20) : (1536ull << 20);
+  c->max_keys = is_lr1(kind) ? (1ull << 20) : (1ull << 16);
+  c->max_result_rows = is_lr1(kind) ? (1ull << 22) : (1ull << 20);
+  c->pane_slots = 0;
+  c->flags = 0;
+  return LMS_OK;
+}
+
+lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
+  try {
+    if (!out) return fail(LMS_EINVAL, "null out");
+    *out = nullptr;
+    lms_status s = validate_config(cfg);
+    if (s) return s;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LMS_ECUDA, "no CUDA device");
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(LMS_EINVAL, "bad device ordinal");
+    CUDA_TRY(cudaSetDevice(cfg->device));
+    lms_query* q = new (std::nothrow) lms_query();
+    if (!q) return fail(LMS_ENOMEM, "host alloc");
+    q->cfg = *cfg;
+    q->kind = cfg->kind;
+    table_iv(q->kind, q->R, q->S);
+    if (cfg->range_s > 0) q->R = (uint32_t)cfg->range_s;
+    if (is_tumbling(q->kind)) q->S = q->R;                            // R19
+    else if (cfg->slide_s > 0) q->S = (uint32_t)cfg->slide_s;
+    if (q->S == 0 || q->S > q->R || q->R % q->S) { delete q; return fail(LMS_EINVAL, "window needs 0 < S <= R, S | R"); }
+    q->ppw = q->R / q->S;
+    q->P = cfg->pane_slots ? cfg->pane_slots : 2 * q->ppw + 64;
+    if (q->P < q->ppw + 1 || q->ppw > 256 || q->P > (1u << 16)) {
+      delete q;
+      return fail(LMS_EINVAL, "need R/S <= 256 and R/S + 1 <= pane_slots <= 65536");
+    }
+    q->infpt = cfg->inf_pt_bytes;
+    q->next_trigger = cfg->trigger_s;
+    q->dag = query_dag(q->kind);
+    auto bail = [&](lms_status st) { delete q; return st; };
+#define Q_TRY(x) do { lms_status st_ = (x); if (st_) return bail(st_); } while (0)
+#define QC_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return bail(fail(LMS_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_))); } while (0)
+    QC_TRY(cudaStreamCreateWithFlags(&q->stream, cudaStreamNonBlocking));
+    QC_TRY(cudaStreamCreateWithFlags(&q->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&q->ev_start, &q->ev_agg, &q->ev_close, &q->ev_end}) QC_TRY(cudaEventCreate(e));
+    QC_TRY(cudaHostAlloc((void**)&q->h_report, sizeof(BatchReport), cudaHostAllocDefault));
+    std::memset(q->h_report, 0, sizeof(BatchReport));
+
+    QueryDev& d = q->qd;
+    d.kind = q->kind;
+    d.S = q->S; d.R = q->R; d.ppw = q->ppw; d.P = q->P;
+    d.div_magic = q->S > 1 ? (~0ull / q->S) + 1 : 0;
+    d.num_xways = (uint32_t)cfg->num_xways;
+    switch (q->kind) {
+      case kLR2S: d.K = 200u * (uint32_t)cfg->num_xways; break;
+      case kCM1S: case kCM1T: d.K = 10; break;
+      default: d.K = (uint32_t)cfg->max_keys; break;
+    }
+    d.n_agg_ctas = (uint32_t)(is_lr(q->kind) ? lr_agg_ctas(d) : cm_agg_ctas(d));
+    Q_TRY(q->dalloc(&d.state, 1, 0));
+    Q_TRY(q->dalloc(&d.report, 1, 0));
+    {
+      const uint64_t H = next_pow2(4ull * q->P);
+      d.H_mask = (uint32_t)(H - 1);
+      Q_TRY(q->dalloc(&d.pane_key, H, 0xFF));
+      Q_TRY(q->dalloc(&d.pane_slot, H, 0xFF));
+      Q_TRY(q->dalloc(&d.slot_pane, q->P, 0xFF));
+      Q_TRY(q->dalloc(&d.free_stack, q->P, 0));
+      std::vector<uint32_t> fs(q->P);
+      for (uint32_t i = 0; i < q->P; i++) fs[i] = q->P - 1 - i;
+      QC_TRY(cudaMemcpy(d.free_stack, fs.data(), q->P * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    }
+    if (is_lr1(q->kind)) {
+      Q_TRY(q->dalloc(&d.acc_cnt32, (size_t)q->P * d.K, 0));
+    } else {
+      Q_TRY(q->dalloc(&d.acc_sum, (size_t)q->P * d.K, 0));
+      Q_TRY(q->dalloc(&d.acc_cnt, (size_t)q->P * d.K, 0));
+    }
+    if (q->kind == kLR2S) {
+      Q_TRY(q->dalloc(&d.part32, (size_t)d.n_agg_ctas * 4 * d.K, 0));
+      Q_TRY(q->dalloc(&d.part_tag, (size_t)d.n_agg_ctas * 2, 0xFF));
+    } else {
+      Q_TRY(q->dalloc(&d.part_tag, (size_t)d.n_agg_ctas * 2, 0xFF));
+    }
+    if (q->kind == kCM2S || is_lr1(q->kind)) {
+      const uint64_t cap = next_pow2(2 * cfg->max_keys);
+      d.dict.cap_mask = cap - 1;
+      d.dict.max_keys = (uint32_t)cfg->max_keys;
+      Q_TRY(q->dalloc(&d.dict.keys, cap, 0xFF));
+      Q_TRY(q->dalloc(&d.dict.vals, cap, 0xFF));
+      Q_TRY(q->dalloc(&d.dict.key_by_idx, cfg->max_keys, 0));
+    }
+    d.row_cap = cfg->max_result_rows;
+    if (is_lr1(q->kind)) {
+      lms_lr1_row* rows;
+      Q_TRY(q->dalloc(&rows, d.row_cap, 0));
+      d.rows = rows;
+      d.fifo_cap = 2 * (cfg->max_batch_bytes / kLrRecBytes) + 1024;
+      Q_TRY(q->dalloc(&d.fifo[0], d.fifo_cap, 0));
+      Q_TRY(q->dalloc(&d.fifo[1], d.fifo_cap, 0));
+    } else {
+      lms_agg_row* rows;
+      Q_TRY(q->dalloc(&rows, d.row_cap, 0));
+      d.rows = rows;
+    }
+    q->in_cap = cfg->max_batch_bytes;
+    for (int b = 0; b < 2; b++) Q_TRY(q->dalloc(&q->d_in[b], q->in_cap + 4096, 0));
+    DevState init{};
+    init.ts_min = kEmpty32;
+    init.free_top = (int)q->P;
+    QC_TRY(cudaMemcpy(d.state, &init, sizeof(init), cudaMemcpyHostToDevice));
+    QC_TRY(cudaDeviceSynchronize());
+#undef Q_TRY
+#undef QC_TRY
+    *out = q;
+    return LMS_OK;
+  } catch (const std::exception& e) {
+    return fail(LMS_EINTERNAL, e.what());
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "unknown exception");
+  }
+}
+
+lms_status lms_query_destroy(lms_query* q) {
+  try {
+    delete q;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in destroy");
+  }
+}
+
+static lms_status push_common(lms_query* q, uint64_t nbytes, double t) {
+  if (!q) return fail(LMS_EINVAL, "null query");
+  if (nbytes == 0) return fail(LMS_EINVAL, "empty dataset");
+  if (!(t >= q->last_ingest)) return fail(LMS_EINVAL, "ingest_time must be non-decreasing");
+  if (is_lr(q->kind) && nbytes % kLrRecBytes) return fail(LMS_EINVAL, "LR dataset is not whole 70 B records");
+  return LMS_OK;
+}
+
+lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, uint64_t* id) {
+  try {
+    lms_status s = push_common(q, nbytes, t);
+    if (s) return s;
+    if (!bytes) return fail(LMS_EINVAL, "null bytes");
+    if (!is_lr(q->kind) && static_cast<const uint8_t*>(bytes)[nbytes - 1] != '\n')
+      return fail(LMS_EINVAL, "CM dataset does not end with a newline");
+    const int b = q->in_cur;
+    if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    const double t0 = now_host();
+    CUDA_TRY(cudaMemcpyAsync(q->d_in[b] + q->in_used[b], bytes, nbytes, cudaMemcpyHostToDevice, q->copy_stream));
+    CUDA_TRY(cudaStreamSynchronize(q->copy_stream));
+    const double h2d = now_host() - t0;
+    q->in_used[b] += nbytes;
+    q->pending.push_back({q->next_ds_id, t, nbytes, nullptr, h2d});
+    q->last_ingest = t;
+    if (id) *id = q->next_ds_id;
+    q->next_ds_id++;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in push");
+  }
+}
+
+lms_status lms_push_device(lms_query* q, const void* dptr, uint64_t nbytes, double t, uint64_t* id) {
+  try {
+    lms_status s = push_common(q, nbytes, t);
+    if (s) return s;
+    if (!dptr || (reinterpret_cast<uintptr_t>(dptr) & 15u)) return fail(LMS_EINVAL, "device pointer must be 16 B aligned");
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, dptr) != cudaSuccess || at.type != cudaMemoryTypeDevice ||
+        at.device != q->cfg.device) {
+      cudaGetLastError();
+      return fail(LMS_EINVAL, "not device memory of the query's device");
+    }
+    q->pending.push_back({q->next_ds_id, t, nbytes, static_cast<const uint8_t*>(dptr), 0.0});
+    q->last_ingest = t;
+    if (id) *id = q->next_ds_id;
+    q->next_ds_id++;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in push_device");
+  }
+}
+
+lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    if (admitted) *admitted = 0;
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    lms_status cs = LMS_OK;
+    if (q->in_flight) {
+      cudaError_t e = cudaEventQuery(q->ev_end);
+      if (e == cudaErrorNotReady) return LMS_OK;    // one micro-batch in flight at a time
+      if (e != cudaSuccess) return fail(LMS_ECUDA, cudaGetErrorString(e));
+      cs = complete(q);
+    }
+    const Mode mode = (Mode)q->cfg.mode;
+    bool admit = false;
+    int32_t reason = kBuffer;
+    double est = std::nan("");
+    const double t0 = now_host();
+    if (mode == Mode::Trigger) {
+      if (now >= q->next_trigger) {                 // OS(tN): trigger instants N, 2N, ...
+        q->next_trigger = (std::floor(now / q->cfg.trigger_s) + 1.0) * q->cfg.trigger_s;
+        if (!q->pending.empty()) { admit = true; reason = kAdmitTrigger; }
+      }
+    } else if (mode == Mode::LMStream || mode == Mode::Deadline) {
+      const size_t n = q->pending.size();
+      std::vector<double> ing(n);
+      std::vector<uint64_t> by(n);
+      for (size_t j = 0; j < n; j++) { ing[j] = q->pending[j].ingest; by[j] = q->pending[j].nbytes; }
+      const double thp = q->cum_proc > 0 ? q->cum_bytes / q->cum_proc : 0.0;
+      const double slide = is_tumbling(q->kind) ? 0.0 : (double)q->S;   // SlideTime (Table I)
+      AdmitResult ar = admit_decision(mode, slide, q->cfg.deadline_s, now, ing.data(), by.data(), n, thp,
+                                      q->maxlat_hist.data(), q->maxlat_hist.size());
+      admit = ar.admit;
+      reason = ar.reason;
+      est = ar.est;
+    }
+    const double admit_overhead = now_host() - t0;
+    if (admit) {
+      lms_status s = launch_batch(q, now, reason, est, false);
+      if (s) return s;
+      q->cur.admit_overhead_s = admit_overhead;
+      if (admitted) *admitted = 1;
+      if (bidx) *bidx = q->cur.index;
+    }
+    return cs;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in poll");
+  }
+}
+
+lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    if (bidx) *bidx = UINT64_MAX;
+    if (q->in_flight) return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
+    if (q->pending.empty()) return LMS_OK;
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    lms_status s = launch_batch(q, now, kAdmitForced, std::nan(""), false);
+    if (s) return s;
+    if (bidx) *bidx = q->cur.index;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in force_batch");
+  }
+}
+
+lms_status lms_sync(lms_query* q) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    if (!q->in_flight) return LMS_OK;
+    return complete(q);
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in sync");
+  }
+}
+
+lms_status lms_flush(lms_query* q, double now) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    lms_status s1 = complete(q);
+    lms_status s = launch_batch(q, now, kAdmitFlush, std::nan(""), true);
+    if (s) return s;
+    lms_status s2 = complete(q);
+    return s2 ? s2 : s1;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in flush");
+  }
+}
+
+lms_status lms_read_agg(lms_query* q, lms_agg_row* rows, uint64_t cap, uint64_t* n, uint64_t* remaining) {
+  if (!q || (!rows && cap)) return fail(LMS_EINVAL, "null argument");
+  if (is_lr1(q->kind)) return fail(LMS_EINVAL, "LR1 queries emit lms_lr1_row (use lms_read_lr1)");
+  uint64_t k = 0;
+  while (k < cap && !q->agg_rows.empty()) { rows[k++] = q->agg_rows.front(); q->agg_rows.pop_front(); }
+  if (n) *n = k;
+  if (remaining) *remaining = q->agg_rows.size();
+  return LMS_OK;
+}
+
+lms_status lms_read_lr1(lms_query* q, lms_lr1_row* rows, uint64_t cap, uint64_t* n, uint64_t* remaining) {
+  if (!q || (!rows && cap)) return fail(LMS_EINVAL, "null argument");
+  if (!is_lr1(q->kind)) return fail(LMS_EINVAL, "not an LR1 query (use lms_read_agg)");
+  uint64_t k = 0;
+  while (k < cap && !q->lr1_rows.empty()) { rows[k++] = q->lr1_rows.front(); q->lr1_rows.pop_front(); }
+  if (n) *n = k;
+  if (remaining) *remaining = q->lr1_rows.size();
+  return LMS_OK;
+}
+
+lms_status lms_num_batches(lms_query* q, uint64_t* n) {
+  if (!q || !n) return fail(LMS_EINVAL, "null argument");
+  *n = q->records.size();
+  return LMS_OK;
+}
+
+lms_status lms_get_batch_record(lms_query* q, uint64_t i, lms_batch_record* out) {
+  if (!q || !out) return fail(LMS_EINVAL, "null argument");
+  if (i >= q->records.size()) return fail(LMS_EINVAL, "no such batch");
+  *out = q->records[i];
+  return LMS_OK;
+}
+
+lms_status lms_last_kernel_times(lms_query* q, double* batch_s, double* agg_s, double* close_s) {
+  if (!q) return fail(LMS_EINVAL, "null query");
+  if (batch_s) *batch_s = q->last_batch_s;
+  if (agg_s) *agg_s = q->last_agg_s;
+  if (close_s) *close_s = q->last_close_s;
+  return LMS_OK;
+}
+
+lms_status lms_kernel_launches(lms_query* q, uint64_t* n) {
+  if (!q || !n) return fail(LMS_EINVAL, "null argument");
+  *n = q->launches;
+  return LMS_OK;
+}
+
+// ------------------------------------------------------------------ pure functions
+lms_status lms_est_max_lat(const double* buff_s, const uint64_t* bytes, uint64_t n, double thp, double* out) {
+  if (!buff_s || !bytes || !out || n == 0) return fail(LMS_EINVAL, "empty micro-batch");
+  if (!(thp > 0)) return fail(LMS_EINVAL, "AvgThPut must be > 0");
+  *out = est_max_lat(buff_s, bytes, n, thp);
+  return LMS_OK;
+}
+
+lms_status lms_cpu_cost(double base, double part, double infpt, double* out) {
+  if (!out || !(base > 0) || !(part > 0) || !(infpt > 0)) return fail(LMS_EINVAL, "non-positive cost input");
+  *out = base * (part / infpt);   // Eq. 7
+  return LMS_OK;
+}
+lms_status lms_gpu_cost(double base, double part, double infpt, double* out) {
+  if (!out || !(base > 0) || !(part > 0) || !(infpt > 0)) return fail(LMS_EINVAL, "non-positive cost input");
+  *out = base * (infpt / part);   // Eq. 8
+  return LMS_OK;
+}
+lms_status lms_trans_cost(double btc, double part, double infpt, double* out) {
+  if (!out || !(btc >= 0) || !(part > 0) || !(infpt > 0)) return fail(LMS_EINVAL, "non-positive cost input");
+  *out = btc * (part / infpt);    // Eq. 9
+  return LMS_OK;
+}
+lms_status lms_base_cost(int32_t k, double* out) {
+  if (!out) return fail(LMS_EINVAL, "null out");
+  const double c = base_cost(k);
+  if (c < 0) return fail(LMS_EINVAL, "unknown operation kind");
+  *out = c;
+  return LMS_OK;
+}
+
+lms_status lms_map_device(const lms_dag* dag, double part, double infpt, double btc, uint8_t* dev_out) {
+  try {
+    if (!dag || !dev_out || !dag->op_kind || !dag->pred_off) return fail(LMS_EINVAL, "null argument");
+    if (!(part > 0) || !(infpt > 0) || !(btc >= 0)) return fail(LMS_EINVAL, "non-positive cost input");
+    Dag d;
+    for (uint32_t o = 0; o < dag->n; o++) {
+      if (base_cost(dag->op_kind[o]) < 0) return fail(LMS_EINVAL, "unknown operation kind");
+      d.kind.push_back(dag->op_kind[o]);
+      std::vector<int32_t> p;
+      for (int32_t j = dag->pred_off[o]; j < dag->pred_off[o + 1]; j++) p.push_back(dag->preds[j]);
+      d.preds.push_back(p);
+    }
+    std::vector<uint8_t> dev;
+    if (!map_device(d, part, infpt, btc, dev)) return fail(LMS_EPLAN, "DAG has a cycle or not exactly one root");
+    for (uint32_t o = 0; o < dag->n; o++) dev_out[o] = dev[o];
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in map_device");
+  }
+}
+
+lms_status lms_query_dag(int32_t kind, lms_dag* out) {
+  static thread_local std::vector<uint8_t> kinds[6];
+  static thread_local std::vector<int32_t> offs[6], preds[6];
+  uint32_t R, S;
+  if (!out || !table_iv(kind, R, S)) return fail(LMS_EINVAL, "unknown query kind");
+  const Dag d = query_dag(kind);
+  kinds[kind] = d.kind;
+  offs[kind].assign(1, 0);
+  preds[kind].clear();
+  for (auto& p : d.preds) {
+    preds[kind].insert(preds[kind].end(), p.begin(), p.end());
+    offs[kind].push_back((int32_t)preds[kind].size());
+  }
+  out->n = (uint32_t)d.kind.size();
+  out->op_kind = kinds[kind].data();
+  out->pred_off = offs[kind].data();
+  out->preds = preds[kind].data();
+  return LMS_OK;
+}
+
+lms_status lms_admit_decision(int32_t mode, double slide_s, double deadline_s, double now_s,
+                              const double* ingest_s, const uint64_t* bytes, uint64_t n, double thp,
+                              const double* maxlat_hist, uint64_t n_hist, int32_t* admit, double* est,
+                              int32_t* reason) {
+  if (!admit || !est || !reason || (n && (!ingest_s || !bytes)) || (n_hist && !maxlat_hist))
+    return fail(LMS_EINVAL, "null argument");
+  if (mode != LMS_MODE_LMSTREAM && mode != LMS_MODE_DEADLINE) return fail(LMS_EINVAL, "mode");
+  const AdmitResult r = admit_decision((Mode)mode, slide_s, deadline_s, now_s, ingest_s, bytes, n, thp,
+                                       maxlat_hist, n_hist);
+  *admit = r.admit ? 1 : 0;
+  *est = r.est;
+  *reason = r.reason;
+  return LMS_OK;
+}
+
+lms_status lms_infpt_fit(const double* th, const double* lat, const double* ip, uint64_t n, double* b0,
+                         double* b1, double* b2) {
+  if (!b0 || !b1 || !b2 || (n && (!th || !lat || !ip))) return fail(LMS_EINVAL, "null argument");
+  double b[3];
+  if (!infpt_fit(th, lat, ip, n, b)) return fail(LMS_EHISTORY, "insufficient or degenerate history");
+  *b0 = b[0]; *b1 = b[1]; *b2 = b[2];
+  return LMS_OK;
+}
+
+lms_status lms_infpt_predict(double b0, double b1, double b2, double th, double lat, double* out) {
+  if (!out) return fail(LMS_EINVAL, "null out");
+  const double b[3] = {b0, b1, b2};
+  *out = infpt_predict(b, th, lat);
+  return LMS_OK;
+}
+
+lms_status lms_percentile(const double* v, uint64_t n, double p, double* out) {
+  if (!v || !out || n == 0 || !(p > 0) || p > 100) return fail(LMS_EINVAL, "bad percentile input");
+  *out = percentile_nearest_rank(std::vector<double>(v, v + n), p);
+  return LMS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, element by element.
+
+Bar (BASELINE.json north_star): keys, counts, filter results bit-exact; LR2 SUM/AVG bit-exact
+(integer speed sums); CM SUM/AVG within 1e-9 relative; LR1 rows + multiplicities exact.
+Inputs: seeded lmsgen streams shaped like the paper's workloads, sized so the
+oracle finishes in seconds while spanning many tiles (LR tile = 512 records, CM tile = 32 KB)
+with ragged tails, plus malformed / late / multi-segment / empty edge cases.
+"""
+import random
+
+import pytest
+
+import lmsgen as g
+from tests.helpers import compare_run, oracle_rows, product_run
+
+pytestmark = pytest.mark.gpu
+
+
+def stream(family, traffic, seconds, seed=11, params=None, t0=0):
+    return [d for _, d in g.stream_datasets(family, traffic, seconds, seed=seed, params=params, t0=t0)]
+
+
+def split(secs, sizes):
+    out, i = [], 0
+    for s in sizes:
+        out.append(secs[i:i + s])
+        i += s
+    if i < len(secs):
+        out.append(secs[i:])
+    return out
+
+
+@pytest.mark.parametrize("qname,traffic,secs,bs", [
+    ("LR2S", "B(1.7)", 45, [3, 7, 1, 10, 4]),      # 1700 rec/s: 4 tiles per second, ragged tail
+    ("LR2S", "U(0.6)", 70, [10] * 7),
+    ("CM2S", "B(1.3)", 40, [5, 5, 1, 9, 2]),       # ~180 KB/s: 6 CM tiles per second
+    ("CM2S", "R(0.1,1)", 66, [5] * 13),
+    ("CM1S", "B(0.9)", 75, [10, 10, 3, 20]),
+    ("CM1T", "U(0.5)", 130, [30, 30, 60]),
+    ("LR1S", "B(0.4)", 40, [5, 5, 2, 8]),
+    ("LR1T", "B(0.3)", 65, [7, 11, 30]),
+])
+def test_parity_streams(qname, traffic, secs, bs):
+    fam = qname[:2]
+    params = g.LRParams(num_vehicles=300) if qname.startswith("LR1") else (
+        g.CMParams(num_jobs=200) if fam == "CM" else None)
+    data = stream(fam, traffic, secs, params=params)
+    batches = split(data, bs)
+    compare_run(qname, product_run(qname, batches), oracle_rows(qname, batches))
+
+
+def test_lr2_single_big_batch_many_tiles():
+    data = stream("LR", "B(12)", 3)                 # 36k records = 71 tiles in one batch
+    batches = [data]
+    compare_run("LR2S", product_run("LR2S", batches), oracle_rows("LR2S", batches))
+
+
+def test_cm2_single_big_batch_many_tiles():
+    data = stream("CM", "B(8)", 2)                  # 16k records ~ 2.2 MB = 67 tiles
+    batches = [data]
+    compare_run("CM2S", product_run("CM2S", batches), oracle_rows("CM2S", batches))
+
+
+def _corrupt(data: bytes, n: int, seed: int) -> bytes:
+    rng = random.Random(seed)
+    b = bytearray(data)
+    for _ in range(n):
+        i = rng.randrange(len(b))
+        b[i] = rng.choice(b"x,\n0.9 \x00\xff5")
+    return bytes(b)
+
+
+@pytest.mark.parametrize("qname", ["LR2S", "CM2S", "CM1S", "LR1S"])
+def test_malformed_records_counted_and_dropped(qname):
+    fam = qname[:2]
+    params = g.LRParams(num_vehicles=100) if qname.startswith("LR1") else None
+    data = stream(fam, "B(1)", 12, params=params)
+    data = [_corrupt(d, 40, i) for i, d in enumerate(data)]
+    if fam == "CM":
+        data = [d if d.endswith(b"\n") else d + b"\n" for d in data]
+        data[-1] = data[-1] + b"123,,456"            # unterminated tail record
+        data[-1] = data[-1] + b"\n"                   # pushes must end with '\n' (host-side rule)
+        data[3] = b"\n\n" + data[3]                   # empty lines
+        data[5] = data[5] + (b"9" * 300 + b"\n")      # over-long line
+    batches = split(data, [4, 4, 4])
+    prod = product_run(qname, batches)
+    compare_run(qname, prod, oracle_rows(qname, batches))
+    assert any(rec["bad_records"] > 0 for _, rec, _ in prod)
+
+
+def test_late_records():
+    lr = lambda ts, spd: g.lr_format(dict(type=0, time=ts, vid=1, spd=spd, xway=0, lane=0, dir=0, seg=3,
+                                          pos=0, qid=0, sinit=0, send=0, dow=0, tod=0, day=0))
+    b1 = [b"".join(lr(t, 20) for t in (10, 11, 12, 13))]
+    b2 = [b"".join(lr(t, 30) for t in (5, 12, 25, 13, 40))]     # 5 and 12 are late (W_prev = 13)
+    b3 = [b"".join(lr(t, 10) for t in (41, 44, 39))]            # 39 late (W_prev = 40)
+    batches = [b1, b2, b3]
+    compare_run("LR2S", product_run("LR2S", batches, range_s=4, slide_s=2),
+                oracle_rows("LR2S", batches, range_s=4, slide_s=2))
+
+
+def test_custom_windows_and_negative_instances():
+    data = stream("CM", "B(0.5)", 9)
+    batches = split(data, [2, 3, 4])
+    for R, S in ((4, 1), (6, 3), (5, 5), (1, 1)):
+        compare_run("CM2S", product_run("CM2S", batches, range_s=R, slide_s=S),
+                    oracle_rows("CM2S", batches, range_s=R, slide_s=S))
+
+
+def test_device_and_host_segments_mixed():
+    data = stream("CM", "B(1.1)", 20)
+    batches = split(data, [5, 5, 10])
+    devmask = [[i % 2 == 0 for i in range(len(b))] for b in batches]
+    compare_run("CM2S", product_run("CM2S", batches, device_batches=devmask), oracle_rows("CM2S", batches))
+    data = stream("LR", "B(1.3)", 20)
+    batches = split(data, [5, 5, 10])
+    devmask = [[i % 3 != 1 for i in range(len(b))] for b in batches]
+    compare_run("LR2S", product_run("LR2S", batches, device_batches=devmask), oracle_rows("LR2S", batches))
+
+
+def test_many_segments_more_than_16():
+    data = stream("LR", "B(0.2)", 40)
+    batches = [data[:37], data[37:]]
+    devmask = [[True] * len(b) for b in batches]
+    compare_run("LR2S", product_run("LR2S", batches, device_batches=devmask), oracle_rows("LR2S", batches))
+
+
+def test_empty_flush_and_tiny_batches():
+    compare_run("CM2S", product_run("CM2S", []), oracle_rows("CM2S", []))
+    one = [[g.cm_record(g.SEED, 3, 0)]]
+    compare_run("CM2S", product_run("CM2S", one), oracle_rows("CM2S", one))
+    one = [[g.lr_record(g.SEED, 3, 0)]]
+    compare_run("LR2S", product_run("LR2S", one), oracle_rows("LR2S", one))
+
+
+def test_xways_domain_and_high_key_space():
+    data = stream("LR", "B(2)", 31, params=g.LRParams(num_xways=16))
+    batches = split(data, [10, 10, 11])
+    compare_run("LR2S", product_run("LR2S", batches, num_xways=16), oracle_rows("LR2S", batches, num_xways=16))
+    # with the default domain (10 xways) records with xway >= 10 are malformed
+    compare_run("LR2S", product_run("LR2S", batches), oracle_rows("LR2S", batches))

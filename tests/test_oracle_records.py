@@ -79,7 +79,8 @@ def test_cm_cpu_equals_float_of_text():
 
 def test_framing():
     data = b"".join(g.cm_record(g.SEED, 0, i) for i in range(10))
-    lines = R.frame_cm(data)
+    lines, unterminated = R.frame_cm(data)
+    assert unterminated == 0
     assert len(lines) == 10 and all(not ln.endswith(b"\n") for ln in lines)
     recs, bad = R.parse_dataset("CM", data)
     assert len(recs) == 10 and bad == 0
@@ -88,3 +89,11 @@ def test_framing():
     assert len(recs) == 10 and bad == 0
     recs, bad = R.parse_dataset("CM", b"garbage\n" + g.cm_record(g.SEED, 0, 1) + b"\n")
     assert len(recs) == 1 and bad == 2
+
+
+def test_cm_line_length_limit_and_unterminated_tail():
+    base = b"1,,2,3,4,1,,0,0,0.000001,0,0,"
+    assert R.parse_cm_record(base + b"1" * (255 - len(base))) is not None
+    assert R.parse_cm_record(base + b"1" * (256 - len(base))) is None
+    recs, bad = R.parse_dataset("CM", g.cm_record(g.SEED, 0, 0) + b"1,,2,3,4,1,,0,0,0.000001,0,0,0")
+    assert len(recs) == 1 and bad == 1
