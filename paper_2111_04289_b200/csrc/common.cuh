@@ -110,6 +110,7 @@ __device__ __forceinline__ uint32_t claim_slot(const QueryDev& q, uint32_t p) {
           q.slot_pane[s] = p;
         } else {
           atomicAdd(&q.state->free_top, 1);
+          q.state->pane_fail = 1;
         }
         __threadfence();
         atomicExch(&q.pane_slot[h], s);
@@ -138,23 +139,6 @@ __device__ __forceinline__ uint32_t find_slot(const QueryDev& q, long long p) {
     }
     h = (h + 1) & q.H_mask;
   }
-}
-
-// Single thread, no concurrent access: free every slot holding a pane <= upto, then rebuild
-// the pane hash table from the live slots (the table is tiny: H = pow2 >= 4P).
-__device__ __forceinline__ void evict_and_rebuild(const QueryDev& q, long long upto) {
-  for (uint32_t h = 0; h <= q.H_mask; h++) { q.pane_key[h] = kEmpty32; q.pane_slot[h] = kEmpty32; }
-  int top = 0;
-  for (uint32_t s = 0; s < q.P; s++) {
-    const uint32_t p = q.slot_pane[s];
-    if (p != kEmpty32 && (long long)p <= upto) q.slot_pane[s] = kEmpty32;
-    if (q.slot_pane[s] == kEmpty32) { q.free_stack[top++] = s; continue; }
-    uint32_t h = pane_hash(q.slot_pane[s], q.H_mask);
-    while (q.pane_key[h] != kEmpty32) h = (h + 1) & q.H_mask;
-    q.pane_key[h] = q.slot_pane[s];
-    q.pane_slot[h] = s;
-  }
-  q.state->free_top = top;
 }
 
 // Per-CTA pane slots (2, tags in smem: acc slot << 32 | pane).  Sets lslot = 0/1 (local table)

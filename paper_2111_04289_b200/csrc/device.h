@@ -26,10 +26,11 @@ constexpr int kMaxSegs = 16;
 constexpr int kLrRecBytes = 70;
 constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records
 constexpr int kLrTileBytes = kLrTileRecs * kLrRecBytes; // 35840 = 16 * 2240
-constexpr int kCmTile = 32768;                         // CM tile payload bytes
+constexpr int kCmWin = 32768;                          // CM tile window: payload + right halo
 constexpr int kCmHaloL = 16;
 constexpr int kCmHaloR = 256;                          // >= max line (255) + '\n'
-constexpr int kCmStage = kCmHaloL + kCmTile + kCmHaloR;
+constexpr int kCmTile = kCmWin - kCmHaloR;             // CM tile payload bytes (32512)
+constexpr int kCmStage = kCmHaloL + kCmWin;
 constexpr int kCmMaxLine = 255;
 
 enum QueryKind : int32_t { kLR1S = 0, kLR1T = 1, kLR2S = 2, kCM1S = 3, kCM1T = 4, kCM2S = 5 };
@@ -51,6 +52,7 @@ struct DevState {
   unsigned int fifo_cur;        // LR1: which FIFO holds the live rows
   unsigned int fifo_overflow;
   int free_top;                 // free accumulator slots on the stack
+  unsigned int pane_fail;       // a pane found no free slot (table entry marked kFail32)
 };
 
 // Copied to the host after every batch.

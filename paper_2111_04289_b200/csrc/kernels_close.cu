@@ -6,15 +6,17 @@
 // as the last instance containing it has been emitted (pane state carried between batches).
 //
 // One launch per micro-batch.  Every CTA owns a slice of the key space and, for that slice,
-//   1. merges the aggregate kernel's per-CTA partials into the pane accumulators (LR2),
+//   1. merges the aggregate kernel's per-CTA partial tables into the pane accumulators (LR2):
+//      (partial, key) items spread over all threads, native u32 smem atomics,
 //   2. emits every instance k in [next_k, k_last] (k_last = floor((W-R)/S), flush:
 //      floor(W/S)): SUM/COUNT over its panes, AVG = SUM/COUNT in fp64, HAVING avg < 40.0
 //      (LR2), ORDER BY SUM(cpu) rank (CM1), one row per non-empty group,
 //   3. zeroes its slice of every pane <= k_last.
-// The slices are disjoint, so no grid barrier is needed; the last CTA (atomic ticket)
-// resets the ring tags, advances next_k / the watermark snapshot and writes the batch report.
-// LR1 instead probes the retained rows of each closing instance's newest slide against the
-// summed per-pane vehicle counts (bag multiplicity, reading R8) and compacts the FIFO.
+// The slices are disjoint, so no grid barrier is needed; the last CTA (atomic ticket) frees
+// the evicted pane slots, rebuilds the pane table, advances next_k / the watermark snapshot
+// and writes the batch report.  LR1 instead probes the retained rows of each closing
+// instance's newest slide against the summed per-pane vehicle counts (bag multiplicity,
+// reading R8), compacts the row FIFO, and a second small kernel frees the panes.
 #include "../../include/lmstream.h"
 #include "common.cuh"
 
@@ -22,6 +24,10 @@ namespace lms {
 namespace {
 
 constexpr int kCloseThreads = 256;
+constexpr int kMaxPartEntries = 1024;   // 2 * aggregate CTAs
+constexpr int kMaxG = 4;                // distinct pane slots merged in smem per batch
+constexpr int kMaxSlice = 64;           // keys per close CTA (LR2: 200 * xways / 148 <= 22)
+constexpr int kMaxH = 4096;             // pane table entries (P <= 1024)
 
 struct CloseArgs {
   QueryDev q;
@@ -55,61 +61,155 @@ __device__ __forceinline__ void window_slots(const QueryDev& q, long long k, uin
 
 __device__ __forceinline__ unsigned long long row_slot(DevState* st, bool want) {
   // warp-aggregated append to the result buffer
-  const uint32_t m = __ballot_sync(__activemask(), want);
+  const uint32_t act = __activemask();
+  const uint32_t m = __ballot_sync(act, want);
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long base = 0;
   const int leader = m ? __ffs(m) - 1 : 0;
   if (m && (int)lane == leader) base = atomicAdd(&st->rows, (unsigned long long)__popc(m));
-  base = __shfl_sync(__activemask(), base, leader);
+  base = __shfl_sync(act, base, leader);
   return base + __popc(m & ((1u << lane) - 1u));
 }
 
-__device__ void finish(const QueryDev& q, const WinRange& w, int flush) {
-  // last CTA: ring tags, state advance, report.
-  DevState* st = q.state;
-  const bool lr1 = (q.kind == kLR1S || q.kind == kLR1T);
-  if (w.any) {
-    const long long closed = w.k_last >= w.nk ? (w.k_last - w.nk + 1) : 0;
-    st->windows_closed += (unsigned long long)closed;
-    if (!lr1) evict_and_rebuild(q, w.k_last);   // LR1: k_lr1_evict frees the slots
-    st->evict_upto = w.k_last;
-    st->next_k = w.k_last + 1 > w.nk ? w.k_last + 1 : w.nk;
-    st->next_k_valid = 1;
+// Whole-CTA: free slots holding panes <= upto and rebuild the pane hash table (P <= 1024).
+__device__ void evict_rebuild_cta(const QueryDev& q, long long upto) {
+  __shared__ uint32_t s_pane[1024];
+  __shared__ uint32_t s_key[kMaxH];
+  __shared__ int s_need;
+  const uint32_t P = q.P, H = q.H_mask + 1;
+  if (threadIdx.x == 0) s_need = q.state->pane_fail ? 1 : 0;
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
+    uint32_t p = q.slot_pane[s];
+    if (p != kEmpty32 && (long long)p <= upto) { p = kEmpty32; q.slot_pane[s] = kEmpty32; s_need = 1; }
+    s_pane[s] = p;
   }
-  if (q.kind == kLR2S)
-    for (uint32_t i = 0; i < 2 * q.n_agg_ctas; i++) q.part_tag[i] = kEmpty64;
-  if (lr1) {
-    st->fifo_count[st->fifo_cur] = 0;
-    st->fifo_cur ^= 1u;
+  __syncthreads();
+  if (!s_need) return;
+  for (uint32_t h = threadIdx.x; h < H; h += blockDim.x) { s_key[h] = kEmpty32; q.pane_slot[h] = kEmpty32; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int top = 0;
+    for (uint32_t s = 0; s < P; s++) {
+      const uint32_t p = s_pane[s];
+      if (p == kEmpty32) { q.free_stack[top++] = s; continue; }
+      uint32_t h = pane_hash(p, q.H_mask);
+      while (s_key[h] != kEmpty32) h = (h + 1) & q.H_mask;
+      s_key[h] = p;
+      q.pane_slot[h] = s;
+    }
+    q.state->free_top = top;
+    q.state->pane_fail = 0;
   }
-  st->wm_prev = st->wm;
-  BatchReport* r = q.report;
-  r->n_records = st->n_records; r->bad = st->bad; r->late = st->late; r->overflow = st->overflow;
-  r->rows = st->rows; r->windows_closed = st->windows_closed;
-  r->watermark = st->wm ? (long long)st->wm - 1 : -1;
-  r->n_keys = st->n_keys; r->row_overflow = st->row_overflow; r->key_overflow = st->key_overflow;
-  r->fifo_overflow = st->fifo_overflow;
-  st->n_records = st->bad = st->late = st->overflow = st->rows = st->windows_closed = 0;
-  st->row_overflow = 0;
-  st->fifo_overflow = 0;
-  st->key_overflow = 0;
-  st->ts_min = kEmpty32;
-  (void)flush;
+  __syncthreads();
+  for (uint32_t h = threadIdx.x; h < H; h += blockDim.x) q.pane_key[h] = s_key[h];
 }
 
-__device__ __forceinline__ void ticket(const QueryDev& q, const WinRange& w, int flush) {
+// Last CTA (all threads): state advance + report.
+__device__ void finish(const QueryDev& q, const WinRange& w) {
+  DevState* st = q.state;
+  const bool lr1 = (q.kind == kLR1S || q.kind == kLR1T);
+  if (q.kind == kLR2S)
+    for (uint32_t i = threadIdx.x; i < 2 * q.n_agg_ctas; i += blockDim.x) q.part_tag[i] = kEmpty64;
+  if (w.any && !lr1) evict_rebuild_cta(q, w.k_last);      // LR1: k_lr1_evict frees the slots
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (w.any) {
+      const long long closed = w.k_last >= w.nk ? (w.k_last - w.nk + 1) : 0;
+      st->windows_closed += (unsigned long long)closed;
+      st->evict_upto = w.k_last;
+      st->next_k = w.k_last + 1 > w.nk ? w.k_last + 1 : w.nk;
+      st->next_k_valid = 1;
+    }
+    if (lr1) {
+      st->fifo_count[st->fifo_cur] = 0;
+      st->fifo_cur ^= 1u;
+    }
+    st->wm_prev = st->wm;
+    BatchReport* r = q.report;
+    r->n_records = st->n_records; r->bad = st->bad; r->late = st->late; r->overflow = st->overflow;
+    r->rows = st->rows; r->windows_closed = st->windows_closed;
+    r->watermark = st->wm ? (long long)st->wm - 1 : -1;
+    r->n_keys = st->n_keys; r->row_overflow = st->row_overflow; r->key_overflow = st->key_overflow;
+    r->fifo_overflow = st->fifo_overflow;
+    st->n_records = st->bad = st->late = st->overflow = st->rows = st->windows_closed = 0;
+    st->row_overflow = 0;
+    st->fifo_overflow = 0;
+    st->key_overflow = 0;
+    st->ts_min = kEmpty32;
+    st->close_ticket = 0;
+    __threadfence();
+  }
+}
+
+__device__ __forceinline__ bool ticket(DevState* st) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    const uint32_t t = atomicAdd(&q.state->close_ticket, 1u);
-    last = (t == gridDim.x - 1);
-    if (last) {
-      __threadfence();
-      finish(q, w, flush);
-      q.state->close_ticket = 0;
-      __threadfence();
+    last = atomicAdd(&st->close_ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last;
+}
+
+// LR2: merge the per-CTA partial tables (this batch) of keys [k0, k1) into the accumulators.
+__device__ void merge_partials(const QueryDev& q, uint32_t k0, uint32_t k1) {
+  __shared__ uint32_t s_g[kMaxG];
+  __shared__ uint8_t s_gl[kMaxPartEntries];
+  __shared__ uint32_t s_lo[kMaxG][kMaxSlice], s_hi[kMaxG][kMaxSlice], s_cnt[kMaxG][kMaxSlice];
+  const uint32_t ne = 2 * q.n_agg_ctas, nk = k1 - k0, K = q.K;
+  if (threadIdx.x < kMaxG) s_g[threadIdx.x] = kEmpty32;
+  for (uint32_t i = threadIdx.x; i < kMaxG * kMaxSlice; i += blockDim.x) {
+    (&s_lo[0][0])[i] = 0; (&s_hi[0][0])[i] = 0; (&s_cnt[0][0])[i] = 0;
+  }
+  __syncthreads();
+  for (uint32_t e = threadIdx.x; e < ne; e += blockDim.x) {
+    const unsigned long long tg = q.part_tag[e];
+    uint8_t gl = 0xFF;                                         // 0xFF: unused entry
+    if (tg != kEmpty64) {
+      const uint32_t slot = (uint32_t)(tg >> 32);
+      gl = kMaxG;                                              // kMaxG: merge with global atomics
+      for (int j = 0; j < kMaxG; j++) {
+        const uint32_t old = atomicCAS(&s_g[j], kEmpty32, slot);
+        if (old == kEmpty32 || old == slot) { gl = (uint8_t)j; break; }
+      }
     }
+    s_gl[e] = gl;
+  }
+  __syncthreads();
+  if (nk == 0) return;
+  const uint32_t total = ne * nk;
+  const uint32_t magic = (uint32_t)((0x100000000ull + nk - 1) / nk);   // e = item / nk (item < 2^16)
+#pragma unroll 4
+  for (uint32_t item = threadIdx.x; item < total; item += blockDim.x) {
+    const uint32_t e = __umulhi(item, magic);
+    const uint32_t kk = item - e * nk;
+    const uint32_t gl = s_gl[e];
+    if (gl == 0xFF) continue;
+    const uint32_t* part = q.part32 + (size_t)(2 * e) * K + k0 + kk;
+    const uint32_t cv = part[K];
+    if (!cv) continue;
+    const uint32_t sv = part[0];
+    if (gl < kMaxG) {
+      const uint32_t old = atomicAdd(&s_lo[gl][kk], sv);
+      if (old + sv < old) atomicAdd(&s_hi[gl][kk], 1u);          // carry into the high word
+      atomicAdd(&s_cnt[gl][kk], cv);
+    } else {
+      const size_t g = (size_t)(q.part_tag[e] >> 32) * K + k0 + kk;
+      atomicAdd(&q.acc_sum[g], (unsigned long long)sv);
+      atomicAdd(&q.acc_cnt[g], (unsigned long long)cv);
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kMaxG * nk; i += blockDim.x) {
+    const uint32_t gl = i / nk, kk = i - gl * nk;
+    const uint32_t slot = s_g[gl];
+    if (slot == kEmpty32 || s_cnt[gl][kk] == 0) continue;
+    const size_t g = (size_t)slot * K + k0 + kk;
+    q.acc_sum[g] += ((unsigned long long)s_hi[gl][kk] << 32) | s_lo[gl][kk];
+    q.acc_cnt[g] += s_cnt[gl][kk];
   }
 }
 
@@ -121,28 +221,11 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   const uint32_t k0 = (uint32_t)((unsigned long long)K * blockIdx.x / gridDim.x);
   const uint32_t k1 = (uint32_t)((unsigned long long)K * (blockIdx.x + 1) / gridDim.x);
   const uint32_t P = q.P;
-  __shared__ uint32_t wslots[256];   // ppw <= 256
+  __shared__ uint32_t wslots[256];   // R/S <= 256
 
   // 1. merge LR2 partials of this batch into the pane accumulators (my key slice)
-  if (q.kind == kLR2S) {
-    for (uint32_t c = 0; c < q.n_agg_ctas; c++) {
-      for (int sl = 0; sl < 2; sl++) {
-        const unsigned long long tg = q.part_tag[c * 2 + sl];
-        if (tg == kEmpty64) continue;
-        const size_t g = (size_t)(tg >> 32) * q.K;
-        uint32_t* part = q.part32 + ((size_t)c * 4 + sl * 2) * q.K;
-        for (uint32_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-          const uint32_t cv = part[q.K + k];
-          if (cv) {
-            q.acc_sum[g + k] += part[k];
-            q.acc_cnt[g + k] += cv;
-            part[k] = 0;
-            part[q.K + k] = 0;
-          }
-        }
-      }
-    }
-  }
+  if (q.kind == kLR2S) merge_partials(q, k0, k1);
+  __syncthreads();
 
   // 2. emit closing instances
   if (w.any && w.k_last >= w.nk) {
@@ -187,7 +270,6 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
             }
           }
         }
-        __syncthreads();
         continue;
       }
       // LR2 / CM2: one thread per key of my slice
@@ -232,7 +314,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
     }
   }
 
-  // 3. evict panes whose last instance has been emitted (my key slice)
+  // 3. zero my key slice of every pane whose last instance has been emitted
   if (w.any) {
     const uint32_t kk0 = (q.kind == kCM1S || q.kind == kCM1T) ? 0 : k0;
     const uint32_t kk1 = (q.kind == kCM1S || q.kind == kCM1T) ? q.K : k1;
@@ -246,7 +328,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
       }
     }
   }
-  ticket(q, w, a.flush);
+  if (ticket(st)) finish(q, w);
 }
 
 // LR1: probe retained rows whose pane is the newest slide of a closing instance.
@@ -301,10 +383,10 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
     base = __shfl_sync(0xffffffffu, base, 0);
     if (keep) dst[base + __popc(km & ((1u << (threadIdx.x & 31)) - 1u))] = r;
   }
-  ticket(q, w, a.flush);
+  if (ticket(st)) finish(q, w);
 }
 
-// LR1: zero the vehicle counts of evicted panes, then (last CTA) free their ring slots.
+// LR1: zero the vehicle counts of evicted panes, then (last CTA) free their slots.
 __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   DevState* st = q.state;
   const long long upto = st->evict_upto;
@@ -315,17 +397,9 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += gridDim.x * blockDim.x)
       q.acc_cnt32[(size_t)g * q.K + k] = 0;
   }
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    last = atomicAdd(&st->close_ticket, 1u) == gridDim.x - 1;
-    if (last) {
-      __threadfence();
-      evict_and_rebuild(q, upto);
-      st->close_ticket = 0;
-      __threadfence();
-    }
+  if (ticket(st)) {
+    evict_rebuild_cta(q, upto);
+    if (threadIdx.x == 0) { st->close_ticket = 0; __threadfence(); }
   }
 }
 

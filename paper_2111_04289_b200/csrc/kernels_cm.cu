@@ -6,35 +6,61 @@
 // variable)"; operators Scan (CSV) / Filtering / Projection / Aggregation (Table III).
 // Record grammar: DESIGN.md reading R1 (13-column task_events line, <= 255 B + '\n').
 //
-// Design (B200): persistent CTAs over contiguous 32 KB tiles; each tile is bulk-copied (TMA
-// engine, cp.async.bulk) into a 3-stage smem ring together with a 16 B left halo (to see the
-// byte before the tile) and a 256 B right halo (to finish the last record that STARTS in the
-// tile: a record belongs to the tile holding its first byte).  Thread j owns the 128 B chunk
-// j: it builds the chunk's newline bitmask with SWAR zero-byte tests, derives record starts
-// (byte after '\n'), then walks each of its records word by word to locate the 12 commas
-// and the terminating '\n' (SWAR again), validates and decodes ts, jobId, eventType,
-// category, cpu (fixed-point cpu*1e6).  CM2: survivors of eventType == 1 are compacted with
-// warp ballots into a dense smem list, then processed by full warps (dictionary jobId ->
-// index, two RED.64 into the pane accumulators).  CM1: per-warp ballot/REDUX reduction per
-// (pane, category), per-warp smem accumulators, one RED.64 pair per CTA and key at the end.
+// Design (B200).  A tile is a 32 KB window = 32512 B payload + 256 B right halo (the tail of
+// the last record that STARTS in the payload: a record belongs to the tile holding its first
+// byte) + a 16 B left halo (the byte before the tile).  Persistent CTAs walk a contiguous
+// tile range through a 2-stage smem ring filled by TMA-engine bulk copies (cp.async.bulk).
+//  * Pass 1 (all threads, round-robin 16 B pieces: conflict-free LDS.128): exact SWAR byte
+//    equality against '\n' and ',' (3 ops per class per word + a shared AND), gathered to one
+//    mask bit per byte with IDP.4A; masks go to smem.
+//  * Pass 2: thread t owns window chunk t (128 B): record starts = byte after a '\n'.
+//  * Pass 3, per record: the '\n' is the first newline bit of a 192-bit window; the 12 commas
+//    are counted with POPC; commas 0..5 are the 6 lowest bits of the 64-bit window at the
+//    record start, commas 6..11 the 6 highest bits of the 64-bit window ending at the '\n'
+//    (FLO), which covers every record of 130..255 B with the usual field widths; anything
+//    else (or any short line) takes an exact byte-serial path.  ts / eventType / category
+//    are parsed from smem bytes, the 10-digit jobId and the cpu field with SWAR arithmetic.
+//  * CM2: eventType == 1 survivors are compacted with warp ballots into a per-warp smem
+//    list and processed 32 at a time by full warps (dictionary jobId -> index, two RED.64
+//    into the pane accumulators) — no CTA barrier on the dependent-latency path.
+//    CM1: per-warp ballot/REDUX reduction per (pane, category) into per-warp smem
+//    accumulators, one RED.64 pair per CTA and key at the end.
 #include "common.cuh"
 
 namespace lms {
 namespace {
 
 constexpr int kCmThreads = 256;
-constexpr int kCmStages = 3;
-constexpr int kChunk = kCmTile / kCmThreads;   // 128 B per thread
-static_assert(kChunk == 128, "chunk");
+constexpr int kCmStages = 2;
+constexpr int kChunk = kCmWin / kCmThreads;                  // 128 B window chunk per thread
+constexpr int kMaskBits = kCmWin;                            // mask bit i <-> stage byte 16 + i
+constexpr int kMaskWords = kMaskBits / 64;                   // 512
+constexpr int kPieces = kMaskBits / 16;                      // 2048 pieces of 16 B
+static_assert(kChunk == 128 && kPieces == 8 * kCmThreads, "one 128 B chunk / 8 pieces per thread");
+constexpr int kSurvCap = 64;                                 // per-warp survivor list
+constexpr int kSmemPad = 16;                                 // SWAR loads may read 12 B past a stage
 
-__device__ __forceinline__ uint32_t zero_bytes(uint32_t y) {
-  // bit 7 of each byte set iff that byte of y is zero (exact, no borrow artefacts)
-  const uint32_t t = (y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu;
-  return ~(t | y | 0x7F7F7F7Fu);
+// Exact byte-equality flags of one 4-byte word (c < 0x80 per byte): bit 7 of byte k set iff
+// byte k == c.  Low 7 bits equal <=> ((w & 0x7F..) ^ c) + 0x7F.. leaves bit 7 clear, and the
+// byte's own bit 7 must be clear.
+__device__ __forceinline__ uint32_t eq_flags(uint32_t m7, uint32_t w, uint32_t c4) {
+  const uint32_t t = (m7 ^ c4) + 0x7F7F7F7Fu;
+  return ~(t | w) & 0x80808080u;
 }
-__device__ __forceinline__ uint32_t nibble(uint32_t flags) {
-  // compress bits 7,15,23,31 into bits 0..3
-  return ((flags >> 7) * 0x00204081u) >> 21 & 0xFu;
+// 16-bit mask of a 16 B piece from four flag words (IDP.4A gathers bytes {0,0x80} -> bits).
+__device__ __forceinline__ uint32_t gather16(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3) {
+  const uint32_t lo = __dp4a(f1, 0x80402010u, __dp4a(f0, 0x08040201u, 0u));   // 128 * bits 0..7
+  const uint32_t hi = __dp4a(f3, 0x80402010u, __dp4a(f2, 0x08040201u, 0u));
+  return (lo >> 7) | (hi << 1);
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
 }
 
 struct CmArgs {
@@ -52,7 +78,7 @@ __device__ __forceinline__ void seg_of_tile(const SegTable& s, unsigned long lon
 
 struct TileGeom {
   const uint8_t* seg;
-  unsigned long long seg_len, off;   // tile starts at seg + off
+  unsigned long long off;            // tile starts at seg + off
   uint32_t lo, hi;                   // valid smem bytes [lo, hi) (relative to stage start)
   uint32_t payload;                  // tile payload bytes (<= kCmTile)
 };
@@ -63,12 +89,11 @@ __device__ __forceinline__ TileGeom cm_geom(const SegTable& segs, unsigned long 
   seg_of_tile(segs, tile, si, lt);
   TileGeom g;
   g.seg = segs.s[si].ptr;
-  g.seg_len = segs.s[si].nbytes;
   g.off = lt * (unsigned long long)kCmTile;
-  const unsigned long long rem = g.seg_len - g.off;
+  const unsigned long long rem = segs.s[si].nbytes - g.off;
   g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
   g.lo = lt == 0 ? kCmHaloL : 0;
-  const unsigned long long end = (rem < (unsigned long long)(kCmTile + kCmHaloR)) ? rem : (kCmTile + kCmHaloR);
+  const unsigned long long end = rem < (unsigned long long)kCmWin ? rem : kCmWin;
   g.hi = kCmHaloL + (uint32_t)end;
   return g;
 }
@@ -87,115 +112,172 @@ struct CmRec {
   uint32_t event, cat, cpu_m;
 };
 
-// Parse one line starting at smem offset s (stage-relative); limit = first invalid byte.
-// Returns: 1 valid, 0 malformed.  *next = offset after the terminating '\n' (or limit).
-__device__ __forceinline__ int cm_parse(const uint8_t* buf, uint32_t s, uint32_t limit, CmRec& r,
-                                        uint32_t& end_out) {
-  uint32_t c[13];
+__device__ __forceinline__ bool digits_u32(const uint8_t* b, uint32_t n, uint32_t& v) {
+  v = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    const uint32_t d = (uint32_t)b[i] - 48u;
+    if (d > 9u) return false;
+    v = v * 10u + d;
+  }
+  return true;
+}
+__device__ __forceinline__ bool digits_u64(const uint8_t* b, uint32_t n, unsigned long long& v) {
+  v = 0;
+  for (uint32_t i = 0; i < n; i++) {
+    const uint32_t d = (uint32_t)b[i] - 48u;
+    if (d > 9u) return false;
+    v = v * 10ull + d;
+  }
+  return true;
+}
+
+// Bytes [p, p+12) of smem as three little-endian words (p arbitrary; reads 16 aligned bytes).
+__device__ __forceinline__ void load12(const uint8_t* buf, uint32_t p, uint32_t& d0, uint32_t& d1, uint32_t& d2) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(buf + (p & ~3u));
+  const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], sh = (p & 3u) * 8u;
+  d0 = __funnelshift_r(w0, w1, sh);
+  d1 = __funnelshift_r(w1, w2, sh);
+  d2 = __funnelshift_r(w2, w3, sh);
+}
+// 4 ASCII digits (first character in the low byte) -> value; caller validated the bytes.
+__device__ __forceinline__ uint32_t swar4(uint32_t x) {
+  x -= 0x30303030u;
+  x = x * 10u + (x >> 8);                   // bytes 0, 2: 10*d0+d1, 10*d2+d3
+  return (x & 0xFFu) * 100u + ((x >> 16) & 0xFFu);
+}
+// bit 7 of each byte set iff the byte is NOT an ASCII digit
+__device__ __forceinline__ uint32_t nondigit(uint32_t x) {
+  const uint32_t t = x ^ 0x30303030u;
+  return (((t & 0x7F7F7F7Fu) + 0x76767676u) | t) & 0x80808080u;
+}
+
+// Decode + validate given the separator positions (stage-byte offsets): s = record start,
+// c[0..9] the first 10 commas (the caller checked there are exactly 12 and the '\n').
+__device__ __forceinline__ bool cm_fields(const uint8_t* buf, uint32_t s, const uint32_t (&c)[10], CmRec& r) {
+  const uint32_t lts = c[0] - s;
+  if (lts < 1 || lts > 9) return false;
+  if (!digits_u32(buf + s, lts, r.ts)) return false;
+  if (c[1] != c[0] + 1) return false;                      // missing-info field is empty
+  const uint32_t lj = c[2] - c[1] - 1;
+  if (lj == 10) {                                           // common case: SWAR
+    uint32_t d0, d1, d2;
+    load12(buf, c[1] + 1, d0, d1, d2);
+    if ((nondigit(d0) | nondigit(d1) | (nondigit(d2) & 0x8080u)) != 0) return false;
+    const uint32_t hi8 = swar4(d0) * 10000u + swar4(d1);
+    const uint32_t lo2 = ((d2 & 0xFFu) - 48u) * 10u + (((d2 >> 8) & 0xFFu) - 48u);
+    r.job = (unsigned long long)hi8 * 100ull + lo2;
+  } else {
+    if (lj < 1 || lj > 19) return false;
+    if (!digits_u64(buf + c[1] + 1, lj, r.job)) return false;
+  }
+  if (c[5] != c[4] + 2 || c[7] != c[6] + 2 || c[9] != c[8] + 9) return false;
+  r.event = (uint32_t)buf[c[4] + 1] - 48u;
+  r.cat = (uint32_t)buf[c[6] + 1] - 48u;
+  if (r.event > 9u || r.cat > 9u) return false;
+  uint32_t d0, d1, d2;                                      // cpu = D.DDDDDD (8 bytes)
+  load12(buf, c[8] + 1, d0, d1, d2);
+  const uint32_t dot = (d0 >> 8) & 0xFFu;
+  const uint32_t nd = (nondigit(d0) & 0x80800080u) | nondigit(d1);   // bytes 0, 2..7 digits
+  if (dot != '.' || nd) return false;
+  const uint32_t ip = (d0 & 0xFFu) - 48u;
+  // fraction digits: d0 bytes 2,3 ; d1 bytes 0..3
+  const uint32_t f2 = (((d0 >> 16) & 0xFFu) - 48u) * 10u + (((d0 >> 24) & 0xFFu) - 48u);
+  r.cpu_m = ip * 1000000u + f2 * 10000u + swar4(d1);
+  (void)d2;
+  return true;
+}
+
+// Exact byte-serial path: any line the fast path does not cover (short / long / malformed).
+__device__ bool cm_parse_serial(const uint8_t* buf, uint32_t s, uint32_t limit, CmRec& r) {
+  uint32_t c[10];
   uint32_t nc = 0;
-  uint32_t e = 0xFFFFFFFFu;
-  const uint32_t stop = min(limit, s + kCmMaxLine + 1);   // '\n' must be at <= s + 255
-  uint32_t a = s & ~3u;
-  const uint32_t* wp = reinterpret_cast<const uint32_t*>(buf);
-  while (a < stop) {
-    const uint32_t w = wp[a >> 2];
-    uint32_t nl = nibble(zero_bytes(w ^ 0x0A0A0A0Au));
-    uint32_t cm = nibble(zero_bytes(w ^ 0x2C2C2C2Cu));
-    // clip to [s, stop)
-    uint32_t keep = 0xFu;
-    if (a < s) keep &= (0xFu << (s - a)) & 0xFu;
-    if (a + 4 > stop) keep &= (0xFu >> (a + 4 - stop));
-    nl &= keep;
-    cm &= keep;
-    if (nl) {
-      const uint32_t b = __ffs(nl) - 1;
-      e = a + b;
-      cm &= (1u << b) - 1u;
+  const uint32_t stop = min(limit, s + kCmMaxLine + 1);
+  for (uint32_t i = s; i < stop; i++) {
+    const uint8_t b = buf[i];
+    if (b == '\n') {
+      if (nc != 12) return false;
+      return cm_fields(buf, s, c, r);
     }
-    while (cm) {
-      const uint32_t b = __ffs(cm) - 1;
-      cm &= cm - 1;
-      if (nc < 13) c[nc] = a + b;
+    if (b == ',') {
+      if (nc >= 12) return false;
+      if (nc < 10) c[nc] = i;
       nc++;
     }
-    if (e != 0xFFFFFFFFu) break;
-    a += 4;
   }
-  if (e == 0xFFFFFFFFu) {   // no '\n' within 256 bytes or before the segment end
-    end_out = stop;
-    return 0;
-  }
-  end_out = e + 1;
-  if (nc != 12) return 0;
-  // f0 ts: 1..9 digits in [s, c0)
-  const uint32_t lts = c[0] - s;
-  if (lts < 1 || lts > 9) return 0;
-  uint32_t ts = 0;
-  for (uint32_t i = s; i < c[0]; i++) {
-    const uint32_t d = (uint32_t)buf[i] - 48u;
-    if (d > 9u) return 0;
-    ts = ts * 10u + d;
-  }
-  if (c[1] != c[0] + 1) return 0;   // f1 (missing info) empty
-  const uint32_t lj = c[2] - c[1] - 1;
-  if (lj < 1 || lj > 19) return 0;
-  unsigned long long job = 0;
-  for (uint32_t i = c[1] + 1; i < c[2]; i++) {
-    const uint32_t d = (uint32_t)buf[i] - 48u;
-    if (d > 9u) return 0;
-    job = job * 10ull + d;
-  }
-  if (c[5] != c[4] + 2 || c[7] != c[6] + 2 || c[9] != c[8] + 9) return 0;
-  const uint32_t ev = (uint32_t)buf[c[4] + 1] - 48u;
-  const uint32_t cat = (uint32_t)buf[c[6] + 1] - 48u;
-  if (ev > 9u || cat > 9u) return 0;
-  const uint8_t* cp = buf + c[8] + 1;
-  if (cp[1] != '.') return 0;
-  uint32_t m = (uint32_t)cp[0] - 48u;
-  if (m > 9u) return 0;
+  return false;   // no '\n' within 256 bytes or before the segment end
+}
+
+// 64 mask bits starting at bit b (b + 64 <= kMaskBits + 64).
+__device__ __forceinline__ unsigned long long win64(const unsigned long long* m, uint32_t b) {
+  const uint32_t w = b >> 6, sh = b & 63;
+  return (m[w] >> sh) | ((m[w + 1] << 1) << (63 - sh));
+}
+
+// Parse the record starting at mask bit sb.  Returns 1 valid, 0 malformed.
+__device__ __forceinline__ int cm_parse(const uint8_t* buf, const unsigned long long* nlm,
+                                        const unsigned long long* cmm, uint32_t sb, uint32_t hi_bits, CmRec& r) {
+  const uint32_t S = kCmHaloL + sb;
+  // terminating '\n' within 192 bits (records are 130..145 B; longer lines -> serial path)
+  const unsigned long long y0 = win64(nlm, sb), y1 = win64(nlm, sb + 64), y2 = win64(nlm, sb + 128);
+  const uint32_t L = y0 ? (uint32_t)__ffsll(y0) - 1
+                        : (y1 ? 63u + (uint32_t)__ffsll(y1) : (y2 ? 127u + (uint32_t)__ffsll(y2) : 0xFFFFu));
+  if (L < 64 || L > 191 || sb + L >= hi_bits) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  // comma count of [sb, sb+L)
+  const unsigned long long x0 = win64(cmm, sb), x1 = win64(cmm, sb + 64), x2 = win64(cmm, sb + 128);
+  const unsigned long long k1 = L >= 128 ? ~0ull : ((1ull << (L - 64)) - 1);
+  const unsigned long long k2 = L <= 128 ? 0ull : ((1ull << (L - 128)) - 1);
+  const uint32_t total = __popcll(x0) + __popcll(x1 & k1) + __popcll(x2 & k2);
+  if (total != 12) return 0;                                  // not 13 fields
+  unsigned long long h = x0;                                   // commas 0..5: lowest bits at the start
+  unsigned long long t = win64(cmm, sb + L - 64);              // commas 6..11: highest bits before '\n'
+  if (__popcll(h) < 6 || __popcll(t) < 6) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  uint32_t c[10];
 #pragma unroll
-  for (int i = 2; i < 8; i++) {
-    const uint32_t d = (uint32_t)cp[i] - 48u;
-    if (d > 9u) return 0;
-    m = m * 10u + d;
+  for (int k = 0; k < 6; k++) {
+    c[k] = S + (uint32_t)__ffsll(h) - 1;
+    h &= h - 1;
   }
-  r.ts = ts;
-  r.job = job;
-  r.event = ev;
-  r.cat = cat;
-  r.cpu_m = m;
-  return 1;
+  uint32_t c6 = 0;
+#pragma unroll
+  for (int k = 11; k >= 6; k--) {
+    const uint32_t b = 63u - (uint32_t)__clzll(t);
+    t ^= 1ull << b;
+    const uint32_t pos = S + L - 64 + b;
+    if (k < 10) c[k] = pos;
+    c6 = pos;
+  }
+  if (c6 <= c[5]) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;   // windows overlap
+  return cm_fields(buf, S, c, r) ? 1 : 0;
 }
 
 template <int KIND>
 __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
   constexpr bool kCM2 = (KIND == kCM2S);
+  constexpr int kWarps = kCmThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kCmStages];
   __shared__ unsigned long long slot_tag[2];
-  // CM2 compaction list
-  __shared__ unsigned long long l_job[kCmThreads];
-  __shared__ uint32_t l_m[kCmThreads], l_p[kCmThreads];
-  __shared__ uint32_t l_n;
-  // CM1 per-warp accumulators [warp][slot][cat] (sum, count)
-  __shared__ unsigned long long w_sum[kCmThreads / 32][2][10], w_cnt[kCmThreads / 32][2][10];
+  __shared__ __align__(16) unsigned long long nlm[kMaskWords + 2], cmm[kMaskWords + 2];
+  // CM2: per-warp survivor lists; CM1: per-warp accumulators [warp][slot][cat]
+  __shared__ unsigned long long sv_job[kCM2 ? kWarps : 1][kSurvCap];
+  __shared__ uint32_t sv_m[kCM2 ? kWarps : 1][kSurvCap], sv_p[kCM2 ? kWarps : 1][kSurvCap];
+  __shared__ unsigned long long w_sum[kCM2 ? 1 : kWarps][2][10], w_cnt[kCM2 ? 1 : kWarps][2][10];
 
   const QueryDev& q = a.q;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned long long T = a.total_tiles, G = gridDim.x;
   const unsigned long long t0 = T * blockIdx.x / G, t1 = T * (blockIdx.x + 1) / G;
 
-  if (!kCM2) {
-    for (int i = tid; i < (kCmThreads / 32) * 20; i += blockDim.x) {
+  if (!kCM2)
+    for (int i = tid; i < kWarps * 20; i += blockDim.x) {
       (&w_sum[0][0][0])[i] = 0;
       (&w_cnt[0][0][0])[i] = 0;
     }
-  }
   if (tid < 2) slot_tag[tid] = kEmpty64;
+  if (tid < 4) (tid < 2 ? nlm : cmm)[kMaskWords + (tid & 1)] = 0;   // window reads past the end
   if (tid == 0) {
     for (int s = 0; s < kCmStages; s++) mbar_init(&full[s], 1);
     mbar_fence_init();
-    l_n = 0;
   }
   __syncthreads();
   if (tid == 0)
@@ -205,6 +287,25 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
   const unsigned long long wm_prev = q.state->wm_prev;
   CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
+  uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
+  const uint32_t nl_s = smem_addr(nlm), cm_s = smem_addr(cmm);
+
+  // CM2: process entries [0, n) of the warp's survivor list with the warp's lanes
+  auto drain = [&](uint32_t n) {
+    __syncwarp();
+    if ((uint32_t)lane < n) {
+      const uint32_t pp = sv_p[kCM2 ? warp : 0][lane];
+      if (pp != c_pane) { c_pane = pp; c_gslot = claim_slot(q, pp); }
+      const uint32_t idx = c_gslot != kFail32 ? dict_get(q.dict, sv_job[kCM2 ? warp : 0][lane], q.state) : kEmpty32;
+      if (idx == kEmpty32) cnt.overflow++;
+      else {
+        const size_t gi = (size_t)c_gslot * q.K + idx;
+        atomicAdd(&q.acc_sum[gi], (unsigned long long)sv_m[kCM2 ? warp : 0][lane]);
+        atomicAdd(&q.acc_cnt[gi], 1ull);
+      }
+    }
+    __syncwarp();
+  };
 
   for (unsigned long long t = t0; t < t1; t++) {
     const int s = (int)((t - t0) % kCmStages);
@@ -219,76 +320,97 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
         __syncthreads();
       }
     }
-    // ---- framing: starts of records in my chunk --------------------------------------
-    const uint32_t c0 = kCmHaloL + tid * kChunk;                 // stage offset of my chunk
-    const uint32_t cend = kCmHaloL + g.payload;                  // end of tile payload
-    unsigned long long st_lo = 0, st_hi = 0;                     // start bits of bytes c0..c0+127
-    if (c0 < cend) {
-      const uint4* v = reinterpret_cast<const uint4*>(buf + c0);
-      unsigned long long nlm[2] = {0, 0};
+    const uint32_t hi_bits = g.hi - kCmHaloL;                  // mask bits beyond are invalid
+    // ---- Pass 1: exact '\n' / ',' masks of every 16 B piece (round robin: conflict-free LDS.128)
+    const uint32_t buf_s = smem_addr(buf) + kCmHaloL;
+    const bool partial = hi_bits < (uint32_t)kMaskBits;          // segment tail: mask stale bytes
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const uint4 x = v[k];
-        const uint32_t n = nibble(zero_bytes(x.x ^ 0x0A0A0A0Au)) | (nibble(zero_bytes(x.y ^ 0x0A0A0A0Au)) << 4) |
-                           (nibble(zero_bytes(x.z ^ 0x0A0A0A0Au)) << 8) | (nibble(zero_bytes(x.w ^ 0x0A0A0A0Au)) << 12);
-        nlm[k >> 2] |= (unsigned long long)n << ((k & 3) * 16);
+    for (int k = 0; k < kPieces / kCmThreads; k += 2) {
+      // two pieces p, p + 256 -> one 32-bit store per class (pieces p and p+256 are not
+      // adjacent, so store 16-bit halves through two u16 lanes of the same word pattern)
+      const int p0 = tid + k * kCmThreads, p1 = p0 + kCmThreads;
+      uint32_t nlv[2], cmv[2];
+#pragma unroll
+      for (int u = 0; u < 2; u++) {
+        const int p = u ? p1 : p0;
+        const uint4 v = lds128(buf_s + 16 * p);
+        const uint32_t m0 = v.x & 0x7F7F7F7Fu, m1 = v.y & 0x7F7F7F7Fu, m2 = v.z & 0x7F7F7F7Fu, m3 = v.w & 0x7F7F7F7Fu;
+        uint32_t nl = gather16(eq_flags(m0, v.x, 0x0A0A0A0Au), eq_flags(m1, v.y, 0x0A0A0A0Au),
+                               eq_flags(m2, v.z, 0x0A0A0A0Au), eq_flags(m3, v.w, 0x0A0A0A0Au));
+        uint32_t cm = gather16(eq_flags(m0, v.x, 0x2C2C2C2Cu), eq_flags(m1, v.y, 0x2C2C2C2Cu),
+                               eq_flags(m2, v.z, 0x2C2C2C2Cu), eq_flags(m3, v.w, 0x2C2C2C2Cu));
+        if (partial) {
+          const int valid = (int)hi_bits - 16 * p;
+          const uint32_t keep = valid <= 0 ? 0u : (valid >= 16 ? 0xFFFFu : ((1u << valid) - 1u));
+          nl &= keep;
+          cm &= keep;
+        }
+        nlv[u] = nl;
+        cmv[u] = cm;
       }
-      const bool carry = (c0 == kCmHaloL && g.lo == kCmHaloL) ? true : (buf[c0 - 1] == '\n');
-      st_lo = (nlm[0] << 1) | (carry ? 1ull : 0ull);
-      st_hi = (nlm[1] << 1) | (nlm[0] >> 63);
-      const uint32_t nvalid = min(128u, cend - c0);               // starts only inside the payload
+      // piece p's 16 bits live at byte offset 2p of the mask arrays
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)nlv[0]));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p1), "h"((uint16_t)nlv[1]));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p0), "h"((uint16_t)cmv[0]));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p1), "h"((uint16_t)cmv[1]));
+    }
+    __syncthreads();
+    // ---- Pass 2: record starts in my 128 B window chunk (byte after a '\n'), payload only
+    const uint32_t cb = tid * kChunk;
+    unsigned long long st_lo = 0, st_hi = 0;
+    if (cb < g.payload) {
+      const uint4 n = lds128(nl_s + 16 * tid);
+      const unsigned long long n0 = ((unsigned long long)n.y << 32) | n.x;
+      const unsigned long long n1 = ((unsigned long long)n.w << 32) | n.z;
+      const bool carry = tid == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
+                                  : ((nlm[2 * tid - 1] >> 63) != 0);
+      st_lo = (n0 << 1) | (carry ? 1ull : 0ull);
+      st_hi = (n1 << 1) | (n0 >> 63);
+      const uint32_t nvalid = min((uint32_t)kChunk, g.payload - cb);
       if (nvalid < 128) {
         if (nvalid <= 64) { st_hi = 0; st_lo &= (nvalid == 64) ? ~0ull : ((1ull << nvalid) - 1); }
         else st_hi &= (1ull << (nvalid - 64)) - 1;
       }
     }
-    // ---- parse my records (rounds: one record per thread per round) -------------------
+    // ---- Pass 3: decode my records; aggregate (one record per thread per round)
     while (true) {
-      int have = 0;
       CmRec r{0, 0, 0, 0, 0};
       bool surv = false;
-      if (st_lo | st_hi) {
+      const bool have = (st_lo | st_hi) != 0;
+      if (have) {
         uint32_t b;
         if (st_lo) { b = __ffsll(st_lo) - 1; st_lo &= st_lo - 1; }
         else { b = 64 + __ffsll(st_hi) - 1; st_hi &= st_hi - 1; }
-        uint32_t endo;
-        have = 1;
         cnt.n++;
-        const int ok = cm_parse(buf, c0 + b, g.hi, r, endo);
-        if (!ok) { cnt.bad++; have = 0; }
-        else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) { cnt.late++; have = 0; }
+        if (!cm_parse(buf, nlm, cmm, cb + b, hi_bits, r)) cnt.bad++;
+        else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;
         else {
           cnt.ts_min = min(cnt.ts_min, r.ts);
           cnt.ts_max1 = max(cnt.ts_max1, r.ts + 1u);
           surv = kCM2 ? (r.event == 1u) : true;                   // WHERE (eventType == 1)
         }
       }
-      uint32_t p = surv ? pane_of(r.ts, q.S, q.div_magic) : 0;
+      const uint32_t p = surv ? pane_of(r.ts, q.S, q.div_magic) : 0;
       if (kCM2) {
-        // warp-ballot compaction of survivors into the dense CTA list
+        // warp-ballot stream compaction into the warp's survivor list
         const uint32_t bal = __ballot_sync(0xffffffffu, surv);
-        uint32_t base = 0;
-        if (lane == 0 && bal) base = atomicAdd(&l_n, __popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
         if (surv) {
-          const uint32_t pos = base + __popc(bal & ((1u << lane) - 1u));
-          l_job[pos] = r.job;
-          l_m[pos] = r.cpu_m;
-          l_p[pos] = p;
+          const uint32_t pos = sv_n + __popc(bal & ((1u << lane) - 1u));
+          sv_job[warp][pos] = r.job;
+          sv_m[warp][pos] = r.cpu_m;
+          sv_p[warp][pos] = p;
         }
-        __syncthreads();
-        const uint32_t n = l_n;
-        for (uint32_t i = tid; i < n; i += blockDim.x) {          // full warps on survivors
-          const uint32_t pp = l_p[i];
-          if (pp != c_pane) { c_pane = pp; c_gslot = claim_slot(q, pp); }
-          const uint32_t idx = c_gslot != kFail32 ? dict_get(q.dict, l_job[i], q.state) : kEmpty32;
-          if (idx == kEmpty32) { cnt.overflow++; continue; }
-          const size_t gi = (size_t)c_gslot * q.K + idx;
-          atomicAdd(&q.acc_sum[gi], (unsigned long long)l_m[i]);
-          atomicAdd(&q.acc_cnt[gi], 1ull);
+        sv_n += __popc(bal);
+        if (sv_n >= 32) {
+          drain(32);
+          if (sv_n > 32 && (uint32_t)lane < sv_n - 32) {        // move the remainder down
+            sv_job[warp][lane] = sv_job[warp][32 + lane];
+            sv_m[warp][lane] = sv_m[warp][32 + lane];
+            sv_p[warp][lane] = sv_p[warp][32 + lane];
+          }
+          sv_n -= 32;
+          __syncwarp();
         }
-        __syncthreads();
-        if (tid == 0) l_n = 0;
       } else {
         // CM1: reduce per (pane, category) inside the warp
         bool pend = surv;
@@ -301,10 +423,7 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
           const uint32_t mm = __ballot_sync(0xffffffffu, me);
           const uint32_t sm = __reduce_add_sync(0xffffffffu, me ? r.cpu_m : 0u);   // < 32 * 1e7
           if (lane == leader) {
-            if (lp != c_pane) {
-              c_pane = lp;
-              local_slot(slot_tag, q, lp, c_slot, c_gslot);
-            }
+            if (lp != c_pane) { c_pane = lp; local_slot(slot_tag, q, lp, c_slot, c_gslot); }
             if (c_gslot == kFail32) cnt.overflow += __popc(mm);
             else if (c_slot < 2) {
               w_sum[warp][c_slot][lc] += sm;
@@ -320,20 +439,22 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
           __syncwarp();   // order the leader's smem accumulator update before the next leader's
         }
       }
-      if (!__syncthreads_or(st_lo | st_hi ? 1 : 0)) break;
+      if (!__any_sync(0xffffffffu, (st_lo | st_hi) != 0)) break;   // warp-local rounds
     }
-    __syncthreads();   // stage s consumed
+    __syncthreads();   // stage s and the masks consumed
     if (tid == 0 && t + kCmStages < t1) cm_issue(a.segs, t + kCmStages, buf, &full[s]);
   }
 
-  if (!kCM2) {
+  if (kCM2) {
+    if (sv_n) drain(sv_n);
+  } else {
     __syncthreads();
     if (tid < 20) {
       const int sl = tid / 10, c = tid % 10;
       const unsigned long long tg = slot_tag[sl];
       if (tg != kEmpty64 && (uint32_t)(tg >> 32) != kFail32) {
         unsigned long long sv = 0, cv = 0;
-        for (int w = 0; w < kCmThreads / 32; w++) { sv += w_sum[w][sl][c]; cv += w_cnt[w][sl][c]; }
+        for (int w = 0; w < kWarps; w++) { sv += w_sum[w][sl][c]; cv += w_cnt[w][sl][c]; }
         if (cv) {
           const size_t gi = (size_t)(tg >> 32) * q.K + c;
           atomicAdd(&q.acc_sum[gi], sv);
@@ -364,7 +485,7 @@ cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   a.segs = segs;
   a.total_tiles = segs.tile_prefix[segs.n];
   if (a.total_tiles == 0) return cudaSuccess;
-  const size_t smem = (size_t)kCmStages * kCmStage;
+  const size_t smem = (size_t)kCmStages * kCmStage + kSmemPad;
   const int grid = (int)q.n_agg_ctas;
   cudaError_t e;
   if (q.kind == kCM2S) {

@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   constexpr bool kLR1 = (KIND == kLR1S || KIND == kLR1T);
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kLrStages];
-  __shared__ unsigned long long slot_tag[2];
+  __shared__ unsigned long long slot_tag[2], loaded_tag[2];
   const QueryDev& q = a.q;
   uint8_t* stage = smem;
   uint32_t* tsum = reinterpret_cast<uint32_t*>(smem + kLrStages * kLrTileBytes);   // [2][K]
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
 
   if (!kLR1) {
     for (uint32_t i = tid; i < 4 * K; i += blockDim.x) tsum[i] = 0;
-    if (tid < 2) slot_tag[tid] = q.part_tag[blockIdx.x * 2 + tid];
+    if (tid < 2) slot_tag[tid] = loaded_tag[tid] = q.part_tag[blockIdx.x * 2 + tid];
   }
   if (tid == 0) {
     for (int s = 0; s < kLrStages; s++) mbar_init(&full[s], 1);
@@ -249,14 +249,19 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
 
   if (!kLR1) {
     __syncthreads();
-    // write this CTA's pane partials (+= : several launches may feed one batch)
+    // write this CTA's pane partials: overwrite on the batch's first launch (the tag was
+    // empty when loaded), accumulate when an earlier launch of the same batch wrote the slot
     uint32_t* part = q.part32 + (size_t)blockIdx.x * 4 * K;
     for (int sl = 0; sl < 2; sl++) {
       const unsigned long long tg = slot_tag[sl];
       if (tg == kEmpty64 || (uint32_t)(tg >> 32) == kFail32) continue;
+      const bool fresh = loaded_tag[sl] == kEmpty64;
       for (uint32_t k = tid; k < K; k += blockDim.x) {
         const uint32_t sv = tsum[sl * K + k], cv = tcnt[sl * K + k];
-        if (cv) {
+        if (fresh) {
+          part[(sl * 2 + 0) * K + k] = sv;
+          part[(sl * 2 + 1) * K + k] = cv;
+        } else if (cv) {
           part[(sl * 2 + 0) * K + k] += sv;
           part[(sl * 2 + 1) * K + k] += cv;
         }

@@ -354,9 +354,9 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     if (q->S == 0 || q->S > q->R || q->R % q->S) { delete q; return fail(LMS_EINVAL, "window needs 0 < S <= R, S | R"); }
     q->ppw = q->R / q->S;
     q->P = cfg->pane_slots ? cfg->pane_slots : 2 * q->ppw + 64;
-    if (q->P < q->ppw + 1 || q->ppw > 256 || q->P > (1u << 16)) {
+    if (q->P < q->ppw + 1 || q->ppw > 256 || q->P > 1024) {
       delete q;
-      return fail(LMS_EINVAL, "need R/S <= 256 and R/S + 1 <= pane_slots <= 65536");
+      return fail(LMS_EINVAL, "need R/S <= 256 and R/S + 1 <= pane_slots <= 1024");
     }
     q->infpt = cfg->inf_pt_bytes;
     q->next_trigger = cfg->trigger_s;

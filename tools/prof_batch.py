@@ -1,0 +1,32 @@
+"""Profiling driver: run a few 10M-record micro-batches of one workload (for ncu / sanitizers).
+
+  python tools/prof_batch.py --workload cm2 --batches 3 [--records 10000000]
+"""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2111_04289_b200 as P  # noqa: E402
+from lmsgen import cuda as gcu  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="cm2")
+ap.add_argument("--batches", type=int, default=3)
+ap.add_argument("--records", type=int, default=10_000_000)
+a = ap.parse_args()
+kind, fam = {"cm2": ("CM2S", "CM"), "lr2": ("LR2S", "LR"), "cm1": ("CM1S", "CM"), "lr1": ("LR1S", "LR")}[a.workload]
+bufs = [gcu.second_tensor(fam, t, a.records) for t in range(a.batches)]
+q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20)
+for t, (b, n) in enumerate(bufs):
+    q.push_device(b.data_ptr(), n, float(t))
+    q.force(t + 1.0)
+    q.sync()
+    rows = q.read_lr1() if kind.startswith("LR1") else q.read_agg()
+    bt, at, ct = q.kernel_times()
+    print(f"batch {t}: {n} B, rows {len(rows)}, batch {bt*1e3:.3f} ms agg {at*1e3:.3f} ms close {ct*1e3:.3f} ms "
+          f"agg {n / at / 1e9:.0f} GB/s", flush=True)
+q.close()
