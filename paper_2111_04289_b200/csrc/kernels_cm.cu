@@ -207,42 +207,61 @@ __device__ bool cm_parse_serial(const uint8_t* buf, uint32_t s, uint32_t limit, 
   return false;   // no '\n' within 256 bytes or before the segment end
 }
 
-// 64 mask bits starting at bit b (b + 64 <= kMaskBits + 64).
-__device__ __forceinline__ unsigned long long win64(const unsigned long long* m, uint32_t b) {
-  const uint32_t w = b >> 6, sh = b & 63;
-  return (m[w] >> sh) | ((m[w + 1] << 1) << (63 - sh));
+// Bits [b, b+64) of the 64-bit words (a at word index w0, then b1, b2) with b - 64*w0 < 128.
+__device__ __forceinline__ void bits64_at(uint32_t rel, unsigned long long a, unsigned long long b,
+                                          unsigned long long c, uint32_t& lo, uint32_t& hi) {
+  // rel = b - 64*w0 in [0, 128): take the 64 bits starting at rel from the 192-bit a|b|c
+  const unsigned long long x = rel < 64 ? a : b, y = rel < 64 ? b : c;
+  const uint32_t sh = rel & 63;
+  const unsigned long long v = sh ? ((x >> sh) | (y << (64 - sh))) : x;
+  lo = (uint32_t)v;
+  hi = (uint32_t)(v >> 32);
 }
 
-// Parse the record starting at mask bit sb.  Returns 1 valid, 0 malformed.
-__device__ __forceinline__ int cm_parse(const uint8_t* buf, const unsigned long long* nlm,
-                                        const unsigned long long* cmm, uint32_t sb, uint32_t hi_bits, CmRec& r) {
+// Parse the record starting at mask bit sb whose '\n' is at mask bit e (e > sb).
+// Returns 1 valid, 0 malformed.
+__device__ __forceinline__ int cm_parse(const uint8_t* buf, const unsigned long long* cmm, uint32_t sb, uint32_t e,
+                                        uint32_t hi_bits, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
-  // terminating '\n' within 192 bits (records are 130..145 B; longer lines -> serial path)
-  const unsigned long long y0 = win64(nlm, sb), y1 = win64(nlm, sb + 64), y2 = win64(nlm, sb + 128);
-  const uint32_t L = y0 ? (uint32_t)__ffsll(y0) - 1
-                        : (y1 ? 63u + (uint32_t)__ffsll(y1) : (y2 ? 127u + (uint32_t)__ffsll(y2) : 0xFFFFu));
-  if (L < 64 || L > 191 || sb + L >= hi_bits) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
-  // comma count of [sb, sb+L)
-  const unsigned long long x0 = win64(cmm, sb), x1 = win64(cmm, sb + 64), x2 = win64(cmm, sb + 128);
-  const unsigned long long k1 = L >= 128 ? ~0ull : ((1ull << (L - 64)) - 1);
-  const unsigned long long k2 = L <= 128 ? 0ull : ((1ull << (L - 128)) - 1);
-  const uint32_t total = __popcll(x0) + __popcll(x1 & k1) + __popcll(x2 & k2);
-  if (total != 12) return 0;                                  // not 13 fields
-  unsigned long long h = x0;                                   // commas 0..5: lowest bits at the start
-  unsigned long long t = win64(cmm, sb + L - 64);              // commas 6..11: highest bits before '\n'
-  if (__popcll(h) < 6 || __popcll(t) < 6) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  const uint32_t L = e - sb;
+  if (L < 64 || L > 191) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  // four 64-bit comma words covering [sb, e)  (e < sb + 192 <= 64*(w0+4))
+  const uint32_t w0 = sb >> 6, o = sb & 63;
+  const unsigned long long a0 = cmm[w0], a1 = cmm[w0 + 1], a2 = cmm[w0 + 2], a3 = cmm[w0 + 3];
+  // comma count of [sb, e): bits at absolute positions p with sb <= p < e
+  const uint32_t eo = e - 64 * w0;                             // e relative to word w0, in (o, o+192)
+  auto below = [](uint32_t n) -> unsigned long long { return n >= 64 ? ~0ull : ((1ull << n) - 1); };
+  const unsigned long long m0 = (a0 & ~below(o)) & below(eo);
+  const unsigned long long m1 = eo > 64 ? (a1 & below(eo - 64)) : 0ull;
+  const unsigned long long m2 = eo > 128 ? (a2 & below(eo - 128)) : 0ull;
+  const unsigned long long m3 = eo > 192 ? (a3 & below(eo - 192)) : 0ull;
+  if (__popcll(m0) + __popcll(m1) + __popcll(m2) + __popcll(m3) != 12) return 0;   // not 13 fields
+  // commas 0..5 = lowest 6 bits of the 64-bit head window at sb; commas 6..11 = highest 6 bits
+  // of the 64-bit tail window ending at e
+  uint32_t hlo, hhi, tlo, thi;
+  bits64_at(o, a0, a1, a2, hlo, hhi);
+  const uint32_t trel = eo - 64;                               // tail window start, relative to w0
+  if (trel < 128) bits64_at(trel, a0, a1, a2, tlo, thi);
+  else bits64_at(trel - 64, a1, a2, a3, tlo, thi);
+  if (__popc(hlo) + __popc(hhi) < 6 || __popc(tlo) + __popc(thi) < 6)
+    return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
   uint32_t c[10];
 #pragma unroll
   for (int k = 0; k < 6; k++) {
-    c[k] = S + (uint32_t)__ffsll(h) - 1;
-    h &= h - 1;
+    const bool l = hlo != 0;
+    const uint32_t t = l ? hlo : hhi;
+    c[k] = S + (uint32_t)__ffs(t) - 1 + (l ? 0u : 32u);
+    if (l) hlo &= hlo - 1; else hhi &= hhi - 1;
   }
+  const uint32_t T0 = kCmHaloL + e - 64;                       // stage offset of tail bit 0
   uint32_t c6 = 0;
 #pragma unroll
   for (int k = 11; k >= 6; k--) {
-    const uint32_t b = 63u - (uint32_t)__clzll(t);
-    t ^= 1ull << b;
-    const uint32_t pos = S + L - 64 + b;
+    const bool h = thi != 0;
+    const uint32_t t = h ? thi : tlo;
+    const uint32_t b = 31u - (uint32_t)__clz(t);
+    if (h) thi ^= 1u << b; else tlo ^= 1u << b;
+    const uint32_t pos = T0 + b + (h ? 32u : 0u);
     if (k < 10) c[k] = pos;
     c6 = pos;
   }
@@ -258,6 +277,7 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
   __shared__ __align__(8) uint64_t full[kCmStages];
   __shared__ unsigned long long slot_tag[2];
   __shared__ __align__(16) unsigned long long nlm[kMaskWords + 2], cmm[kMaskWords + 2];
+  __shared__ uint16_t fnl[kCmThreads + 2];                     // first newline of each chunk
   // CM2: per-warp survivor lists; CM1: per-warp accumulators [warp][slot][cat]
   __shared__ unsigned long long sv_job[kCM2 ? kWarps : 1][kSurvCap];
   __shared__ uint32_t sv_m[kCM2 ? kWarps : 1][kSurvCap], sv_p[kCM2 ? kWarps : 1][kSurvCap];
@@ -275,6 +295,7 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
     }
   if (tid < 2) slot_tag[tid] = kEmpty64;
   if (tid < 4) (tid < 2 ? nlm : cmm)[kMaskWords + (tid & 1)] = 0;   // window reads past the end
+  if (tid < 2) fnl[kCmThreads + tid] = 0xFFFFu;                      // no chunk beyond the window
   if (tid == 0) {
     for (int s = 0; s < kCmStages; s++) mbar_init(&full[s], 1);
     mbar_fence_init();
@@ -355,13 +376,15 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
       asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p1), "h"((uint16_t)cmv[1]));
     }
     __syncthreads();
-    // ---- Pass 2: record starts in my 128 B window chunk (byte after a '\n'), payload only
+    // ---- Pass 2: record starts in my 128 B window chunk (byte after a '\n'), payload only;
+    // first newline of every chunk (record ends of the previous chunks' records)
     const uint32_t cb = tid * kChunk;
     unsigned long long st_lo = 0, st_hi = 0;
+    const uint4 n = lds128(nl_s + 16 * tid);
+    const unsigned long long n0 = ((unsigned long long)n.y << 32) | n.x;
+    const unsigned long long n1 = ((unsigned long long)n.w << 32) | n.z;
+    fnl[tid] = n0 ? (uint16_t)(cb + __ffsll(n0) - 1) : (n1 ? (uint16_t)(cb + 63 + __ffsll(n1)) : (uint16_t)0xFFFFu);
     if (cb < g.payload) {
-      const uint4 n = lds128(nl_s + 16 * tid);
-      const unsigned long long n0 = ((unsigned long long)n.y << 32) | n.x;
-      const unsigned long long n1 = ((unsigned long long)n.w << 32) | n.z;
       const bool carry = tid == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
                                   : ((nlm[2 * tid - 1] >> 63) != 0);
       st_lo = (n0 << 1) | (carry ? 1ull : 0ull);
@@ -372,6 +395,7 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
         else st_hi &= (1ull << (nvalid - 64)) - 1;
       }
     }
+    __syncthreads();   // fnl[] complete
     // ---- Pass 3: decode my records; aggregate (one record per thread per round)
     while (true) {
       CmRec r{0, 0, 0, 0, 0};
@@ -382,7 +406,15 @@ __global__ void __launch_bounds__(kCmThreads, 2) k_cm_agg(const CmArgs a) {
         if (st_lo) { b = __ffsll(st_lo) - 1; st_lo &= st_lo - 1; }
         else { b = 64 + __ffsll(st_hi) - 1; st_hi &= st_hi - 1; }
         cnt.n++;
-        if (!cm_parse(buf, nlm, cmm, cb + b, hi_bits, r)) cnt.bad++;
+        // terminating '\n': next newline in my chunk, else the first newline of chunk t+1 / t+2
+        const unsigned long long x0 = b >= 63 ? 0ull : (n0 & (~0ull << (b + 1)));
+        const unsigned long long x1 = b < 64 ? n1 : (b >= 127 ? 0ull : (n1 & (~0ull << (b - 63))));
+        const uint32_t f1 = fnl[tid + 1], f2 = fnl[tid + 2];      // branch-free selection
+        const uint32_t ef = f1 != 0xFFFFu ? f1 : f2;
+        const uint32_t e = x0 ? cb + __ffsll(x0) - 1 : (x1 ? cb + 63 + __ffsll(x1) : ef);
+        const int ok = e == 0xFFFFu ? (cm_parse_serial(buf, kCmHaloL + cb + b, g.hi, r) ? 1 : 0)
+                                    : cm_parse(buf, cmm, cb + b, e, hi_bits, r);
+        if (!ok) cnt.bad++;
         else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;
         else {
           cnt.ts_min = min(cnt.ts_min, r.ts);
