@@ -64,10 +64,12 @@ def ncu_traffic(workload):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
 
-    def __init__(self, index):
+    def __init__(self, index, period_ms=20):
         self.index = index
-        self.samples = []
+        self.period_ms = period_ms
+        self.samples = []          # (wall time, [fields])
         self.proc = None
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
@@ -75,10 +77,13 @@ class ClockSampler:
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period_ms)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t_end = time.time() + 5.0          # wait for the first sample (nvidia-smi startup)
+            while not self.samples and time.time() < t_end:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
         return self
@@ -87,7 +92,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 6:
-                self.samples.append(parts)
+                self.samples.append((time.time(), parts))
+
+    def mark(self, start: bool):
+        if start:
+            self.t0 = time.time()
+        else:
+            self.t1 = time.time()
+            time.sleep(2.5 * self.period_ms / 1e3)   # let the sample covering the end arrive
 
     def __exit__(self, *a):
         if self.proc:
@@ -98,14 +110,18 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        """Samples taken during the timed region (+- one sampling period)."""
+        pad = 1.5 * self.period_ms / 1e3
+        win = [p for t, p in self.samples
+               if self.t0 is not None and self.t0 - pad <= t <= (self.t1 or t) + pad]
+        if not win:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in win if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in win if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        reasons = sorted({names[i] for s in win for i in range(4) if s[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(win), "period_ms": self.period_ms}
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -137,11 +153,12 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
     for i in range(warmup):
         step(*inputs[i])
     launches0 = q.kernel_launches()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk.mark(True)
         e0.record()
         for i in range(warmup, warmup + steps):
             out["rows"] += step(*inputs[i])
@@ -151,8 +168,9 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
             out["close_s"].append(c)
         e1.record()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+        if world > 1:
+            dist.barrier()
+        clk.mark(False)
     el = e0.elapsed_time(e1) / 1e3
     out["elapsed_s"] = el
     out["launches"] = q.kernel_launches() - launches0

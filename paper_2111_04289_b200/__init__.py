@@ -99,29 +99,19 @@ class Query:
         return check(L.lms_flush(self.h, now), "lms_flush", ok)
 
     # -- results
-    def read_agg(self, cap: int = 1 << 16) -> np.ndarray:
-        out = []
-        while True:
-            arr = np.zeros(cap, AGG_DTYPE)
-            n, rem = C.c_uint64(), C.c_uint64()
-            check(L.lms_read_agg(self.h, arr.ctypes.data_as(C.POINTER(L.lms_agg_row)), cap, C.byref(n),
-                                 C.byref(rem)), "lms_read_agg")
-            out.append(arr[:n.value])
-            if rem.value == 0:
-                break
-        return np.concatenate(out)
+    def _drain(self, fn, dtype, ctype, name):
+        n, rem = C.c_uint64(), C.c_uint64()
+        check(fn(self.h, None, 0, C.byref(n), C.byref(rem)), name)      # how many are queued
+        arr = np.empty(rem.value, dtype)
+        if rem.value:
+            check(fn(self.h, arr.ctypes.data_as(C.POINTER(ctype)), rem.value, C.byref(n), C.byref(rem)), name)
+        return arr[:n.value]
 
-    def read_lr1(self, cap: int = 1 << 18) -> np.ndarray:
-        out = []
-        while True:
-            arr = np.zeros(cap, LR1_DTYPE)
-            n, rem = C.c_uint64(), C.c_uint64()
-            check(L.lms_read_lr1(self.h, arr.ctypes.data_as(C.POINTER(L.lms_lr1_row)), cap, C.byref(n),
-                                 C.byref(rem)), "lms_read_lr1")
-            out.append(arr[:n.value])
-            if rem.value == 0:
-                break
-        return np.concatenate(out)
+    def read_agg(self) -> np.ndarray:
+        return self._drain(L.lms_read_agg, AGG_DTYPE, L.lms_agg_row, "lms_read_agg")
+
+    def read_lr1(self) -> np.ndarray:
+        return self._drain(L.lms_read_lr1, LR1_DTYPE, L.lms_lr1_row, "lms_read_lr1")
 
     def num_batches(self) -> int:
         n = C.c_uint64()

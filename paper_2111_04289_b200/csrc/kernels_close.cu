@@ -171,8 +171,9 @@ __device__ void merge_partials(const QueryDev& q, uint32_t k0, uint32_t k1) {
     if (tg != kEmpty64) {
       const uint32_t slot = (uint32_t)(tg >> 32);
       gl = kMaxG;                                              // kMaxG: merge with global atomics
-      for (int j = 0; j < kMaxG; j++) {
-        const uint32_t old = atomicCAS(&s_g[j], kEmpty32, slot);
+      for (int j = 0; j < kMaxG; j++) {   // read first: nearly all entries share one pane slot
+        uint32_t old = *(volatile uint32_t*)&s_g[j];
+        if (old == kEmpty32) old = atomicCAS(&s_g[j], kEmpty32, slot);
         if (old == kEmpty32 || old == slot) { gl = (uint8_t)j; break; }
       }
     }

@@ -71,6 +71,22 @@ uint64_t next_pow2(uint64_t v) {
   return p;
 }
 
+// FIFO of result rows drained by lms_read_* (contiguous storage + read offset).
+template <typename T>
+struct RowFifo {
+  std::vector<T> v;
+  size_t off = 0;
+  void append(const T* p, uint64_t n) { v.insert(v.end(), p, p + n); }
+  uint64_t size() const { return v.size() - off; }
+  uint64_t read(T* dst, uint64_t cap) {
+    const uint64_t n = std::min<uint64_t>(cap, size());
+    if (n) std::memcpy(dst, v.data() + off, n * sizeof(T));
+    off += n;
+    if (off == v.size()) { v.clear(); off = 0; }
+    return n;
+  }
+};
+
 }  // namespace
 
 struct lms_query {
@@ -101,8 +117,10 @@ struct lms_query {
   cudaEvent_t ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
   lms_batch_record cur{};
   std::vector<lms_batch_record> records;
-  std::deque<lms_agg_row> agg_rows;
-  std::deque<lms_lr1_row> lr1_rows;
+  RowFifo<lms_agg_row> agg_rows;
+  RowFifo<lms_lr1_row> lr1_rows;
+  void* h_rows = nullptr;          // pinned staging for result rows
+  uint64_t h_rows_cap = 0;         // rows it holds
   uint64_t launches = 0;
   double last_batch_s = 0, last_agg_s = 0, last_close_s = 0;
   lms_status last_completion = LMS_OK;
@@ -112,6 +130,7 @@ struct lms_query {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : dallocs) cudaFree(p);
     if (h_report) cudaFreeHost(h_report);
+    if (h_rows) cudaFreeHost(h_rows);
     for (cudaEvent_t e : {ev_start, ev_agg, ev_close, ev_end})
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -246,14 +265,16 @@ lms_status complete(lms_query* q) {
   double d2h = 0;
   if (nrows) {
     const double t0 = now_host();
-    if (is_lr1(q->kind)) {
-      std::vector<lms_lr1_row> tmp(nrows);
-      CUDA_TRY(cudaMemcpy(tmp.data(), q->qd.rows, nrows * sizeof(lms_lr1_row), cudaMemcpyDeviceToHost));
-      q->lr1_rows.insert(q->lr1_rows.end(), tmp.begin(), tmp.end());
-    } else {
-      std::vector<lms_agg_row> tmp(nrows);
-      CUDA_TRY(cudaMemcpy(tmp.data(), q->qd.rows, nrows * sizeof(lms_agg_row), cudaMemcpyDeviceToHost));
-      q->agg_rows.insert(q->agg_rows.end(), tmp.begin(), tmp.end());
+    // device rows -> pinned staging (chunks) -> host FIFO
+    const size_t rsz = is_lr1(q->kind) ? sizeof(lms_lr1_row) : sizeof(lms_agg_row);
+    const uint8_t* src = static_cast<const uint8_t*>(q->qd.rows);
+    for (uint64_t done = 0; done < nrows;) {
+      const uint64_t n = std::min<uint64_t>(nrows - done, q->h_rows_cap);
+      CUDA_TRY(cudaMemcpyAsync(q->h_rows, src + done * rsz, n * rsz, cudaMemcpyDeviceToHost, q->stream));
+      CUDA_TRY(cudaStreamSynchronize(q->stream));
+      if (is_lr1(q->kind)) q->lr1_rows.append(static_cast<const lms_lr1_row*>(q->h_rows), n);
+      else q->agg_rows.append(static_cast<const lms_agg_row*>(q->h_rows), n);
+      done += n;
     }
     d2h = now_host() - t0;
   }
@@ -368,6 +389,9 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     QC_TRY(cudaStreamCreateWithFlags(&q->copy_stream, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&q->ev_start, &q->ev_agg, &q->ev_close, &q->ev_end}) QC_TRY(cudaEventCreate(e));
     QC_TRY(cudaHostAlloc((void**)&q->h_report, sizeof(BatchReport), cudaHostAllocDefault));
+    q->h_rows_cap = std::min<uint64_t>(cfg->max_result_rows, 1ull << 16);
+    QC_TRY(cudaHostAlloc(&q->h_rows, q->h_rows_cap * std::max(sizeof(lms_agg_row), sizeof(lms_lr1_row)),
+                         cudaHostAllocDefault));
     std::memset(q->h_report, 0, sizeof(BatchReport));
 
     QueryDev& d = q->qd;
@@ -601,8 +625,7 @@ lms_status lms_flush(lms_query* q, double now) {
 lms_status lms_read_agg(lms_query* q, lms_agg_row* rows, uint64_t cap, uint64_t* n, uint64_t* remaining) {
   if (!q || (!rows && cap)) return fail(LMS_EINVAL, "null argument");
   if (is_lr1(q->kind)) return fail(LMS_EINVAL, "LR1 queries emit lms_lr1_row (use lms_read_lr1)");
-  uint64_t k = 0;
-  while (k < cap && !q->agg_rows.empty()) { rows[k++] = q->agg_rows.front(); q->agg_rows.pop_front(); }
+  const uint64_t k = q->agg_rows.read(rows, cap);
   if (n) *n = k;
   if (remaining) *remaining = q->agg_rows.size();
   return LMS_OK;
@@ -611,8 +634,7 @@ lms_status lms_read_agg(lms_query* q, lms_agg_row* rows, uint64_t cap, uint64_t*
 lms_status lms_read_lr1(lms_query* q, lms_lr1_row* rows, uint64_t cap, uint64_t* n, uint64_t* remaining) {
   if (!q || (!rows && cap)) return fail(LMS_EINVAL, "null argument");
   if (!is_lr1(q->kind)) return fail(LMS_EINVAL, "not an LR1 query (use lms_read_agg)");
-  uint64_t k = 0;
-  while (k < cap && !q->lr1_rows.empty()) { rows[k++] = q->lr1_rows.front(); q->lr1_rows.pop_front(); }
+  const uint64_t k = q->lr1_rows.read(rows, cap);
   if (n) *n = k;
   if (remaining) *remaining = q->lr1_rows.size();
   return LMS_OK;

@@ -1,0 +1,17 @@
+#!/bin/bash
+# One GPU call: tests, smoke, bench, ncu launch list + full captures of the dominant kernels.
+# Usage (under gpurun): bash tools/gpu_round.sh <tag>
+set -u
+TAG=${1:-r01}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_power_cap --format=csv > $OUT/nvsmi.txt 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x > $OUT/pytest_gpu.txt 2>&1; tail -3 $OUT/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; tail -2 $OUT/smoke.txt
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; tail -2 $OUT/bench.err; cat $OUT/bench.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_cm2.csv python bench.py --steps 2 --warmup 3 --secondary '' --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_lr2.csv python bench.py --workload lr2 --steps 2 --warmup 3 --secondary '' --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cm_agg -s 2 -c 1 -o $OUT/cm2_agg python tools/prof_batch.py --workload cm2 --batches 3 > $OUT/ncu_cm2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lr_agg -s 2 -c 1 -o $OUT/lr2_agg python tools/prof_batch.py --workload lr2 --batches 3 > $OUT/ncu_lr2.log 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:k_close -s 2 -c 1 -o $OUT/lr2_close python tools/prof_batch.py --workload lr2 --batches 3 > $OUT/ncu_lr2c.log 2>&1
+ls -la $OUT
