@@ -26,7 +26,7 @@ constexpr int kMaxSegs = 16;
 constexpr int kLrRecBytes = 70;
 constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records
 constexpr int kLrTileBytes = kLrTileRecs * kLrRecBytes; // 35840 = 16 * 2240
-constexpr int kCmWin = 32768;                          // CM tile window: payload + right halo
+constexpr int kCmWin = 16384;                          // CM tile window: payload + right halo
 constexpr int kCmHaloL = 16;
 constexpr int kCmHaloR = 256;                          // >= max line (255) + '\n'
 constexpr int kCmTile = kCmWin - kCmHaloR;             // CM tile payload bytes (32512)
