@@ -31,7 +31,7 @@ namespace lms {
 namespace {
 
 constexpr int kCmThreads = 128;
-constexpr int kCtasPerSm = 4;
+constexpr int kCtasPerSm = 5;
 constexpr int kCmStages = 2;
 constexpr int kChunk = kCmWin / kCmThreads;                  // 128 B window chunk per thread
 constexpr int kMaskBits = kCmWin;                            // mask bit i <-> stage byte 16 + i
@@ -271,7 +271,7 @@ __device__ __forceinline__ int cm_parse(const uint8_t* buf, const unsigned long 
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kCmThreads, 4) k_cm_agg(const CmArgs a) {
+__global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs a) {
   constexpr bool kCM2 = (KIND == kCM2S);
   constexpr int kWarps = kCmThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
