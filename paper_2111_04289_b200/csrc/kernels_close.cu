@@ -181,26 +181,36 @@ __device__ void merge_partials(const QueryDev& q, uint32_t k0, uint32_t k1) {
   }
   __syncthreads();
   if (nk == 0) return;
-  const uint32_t total = ne * nk;
-  const uint32_t magic = (uint32_t)((0x100000000ull + nk - 1) / nk);   // e = item / nk (item < 2^16)
+  // thread -> (key kk, entry lane le): lane le walks entries le, le+L, ... with register
+  // accumulators per merged pane slot and independent (pipelined) loads
+  const uint32_t L = blockDim.x / nk;
+  if (threadIdx.x < L * nk) {
+    const uint32_t kk = threadIdx.x % nk, le = threadIdx.x / nk;
+    unsigned long long as[kMaxG] = {0, 0, 0, 0};
+    uint32_t ac[kMaxG] = {0, 0, 0, 0};
+    const uint32_t* base = q.part32 + k0 + kk;
 #pragma unroll 4
-  for (uint32_t item = threadIdx.x; item < total; item += blockDim.x) {
-    const uint32_t e = __umulhi(item, magic);
-    const uint32_t kk = item - e * nk;
-    const uint32_t gl = s_gl[e];
-    if (gl == 0xFF) continue;
-    const uint32_t* part = q.part32 + (size_t)(2 * e) * K + k0 + kk;
-    const uint32_t cv = part[K];
-    if (!cv) continue;
-    const uint32_t sv = part[0];
-    if (gl < kMaxG) {
-      const uint32_t old = atomicAdd(&s_lo[gl][kk], sv);
-      if (old + sv < old) atomicAdd(&s_hi[gl][kk], 1u);          // carry into the high word
-      atomicAdd(&s_cnt[gl][kk], cv);
-    } else {
-      const size_t g = (size_t)(q.part_tag[e] >> 32) * K + k0 + kk;
-      atomicAdd(&q.acc_sum[g], (unsigned long long)sv);
-      atomicAdd(&q.acc_cnt[g], (unsigned long long)cv);
+    for (uint32_t e = le; e < ne; e += L) {
+      const uint32_t gl = s_gl[e];
+      const uint32_t* part = base + (size_t)(2 * e) * K;
+      const uint32_t cv = gl == 0xFF ? 0u : part[K];
+      const uint32_t sv = gl == 0xFF ? 0u : part[0];
+      if (gl < kMaxG) {
+#pragma unroll
+        for (int j = 0; j < kMaxG; j++)
+          if ((uint32_t)j == gl) { as[j] += sv; ac[j] += cv; }
+      } else if (gl == kMaxG && cv) {                          // more than kMaxG panes: direct
+        const size_t g = (size_t)(q.part_tag[e] >> 32) * K + k0 + kk;
+        atomicAdd(&q.acc_sum[g], (unsigned long long)sv);
+        atomicAdd(&q.acc_cnt[g], (unsigned long long)cv);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxG; j++) {
+      if (!ac[j]) continue;
+      const uint32_t lo = (uint32_t)as[j], old = atomicAdd(&s_lo[j][kk], lo);
+      atomicAdd(&s_hi[j][kk], (uint32_t)(as[j] >> 32) + (old + lo < old ? 1u : 0u));
+      atomicAdd(&s_cnt[j][kk], ac[j]);
     }
   }
   __syncthreads();
@@ -319,9 +329,12 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   if (w.any) {
     const uint32_t kk0 = (q.kind == kCM1S || q.kind == kCM1T) ? 0 : k0;
     const uint32_t kk1 = (q.kind == kCM1S || q.kind == kCM1T) ? q.K : k1;
+    __shared__ uint32_t s_sp[1024];                            // slot -> pane (P <= 1024)
+    __syncthreads();
+    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x) s_sp[g] = q.slot_pane[g];
     __syncthreads();
     for (uint32_t g = 0; g < P; g++) {
-      const uint32_t p = q.slot_pane[g];
+      const uint32_t p = s_sp[g];
       if (p == kEmpty32 || (long long)p > w.k_last) continue;
       for (uint32_t k = kk0 + threadIdx.x; k < kk1; k += blockDim.x) {
         q.acc_sum[(size_t)g * q.K + k] = 0;
@@ -414,7 +427,9 @@ int close_ctas(const QueryDev& q) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  return nsm;
+  // LR2: ~3 keys per CTA, so each (key, entry-lane) thread walks only ~7 of the 2C partial
+  // entries (the merge is load-latency bound, not bandwidth bound)
+  return q.kind == kLR2S ? 4 * nsm : nsm;
 }
 
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {

@@ -443,7 +443,9 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       lms_lr1_row* rows;
       Q_TRY(q->dalloc(&rows, d.row_cap, 0));
       d.rows = rows;
-      d.fifo_cap = 2 * (cfg->max_batch_bytes / kLrRecBytes) + 1024;
+      // every retained row is emitted exactly once (as an L row of its pane's instance), so
+      // the FIFO never needs more room than the rows one close may emit
+      d.fifo_cap = cfg->max_result_rows + 1024;
       Q_TRY(q->dalloc(&d.fifo[0], d.fifo_cap, 0));
       Q_TRY(q->dalloc(&d.fifo[1], d.fifo_cap, 0));
     } else {

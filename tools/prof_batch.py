@@ -20,7 +20,7 @@ ap.add_argument("--records", type=int, default=10_000_000)
 a = ap.parse_args()
 kind, fam = {"cm2": ("CM2S", "CM"), "lr2": ("LR2S", "LR"), "cm1": ("CM1S", "CM"), "lr1": ("LR1S", "LR")}[a.workload]
 bufs = [gcu.second_tensor(fam, t, a.records) for t in range(a.batches)]
-q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20)
+q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=max(1 << 20, 2 * a.records))
 for t, (b, n) in enumerate(bufs):
     q.push_device(b.data_ptr(), n, float(t))
     q.force(t + 1.0)
