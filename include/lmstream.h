@@ -100,6 +100,12 @@ typedef struct {
   uint64_t max_result_rows;  /* result rows one batch may emit                    */
   uint32_t pane_slots;       /* distinct live panes (accumulator slots); 0 -> 2*R/S + 64 */
   uint32_t flags;            /* LMS_FLAG_*                                        */
+  int32_t  rank, world;      /* multi-GPU row partition: this handle's rank of `world`
+                                (1 -> single GPU).  world > 1 (LR2S, CM1*, CM2S): every
+                                rank aggregates its own rows; windows close per rank as
+                                PARTIAL rows that are exchanged by key owner
+                                (hash(key) % world) and merged on the owner — see
+                                lms_run_close / lms_partials / lms_merge.               */
 } lms_config;
 
 #define LMS_FLAG_ONLINE_INFPT 0x1u  /* Eq. 10 online regression of InfPT */
@@ -218,6 +224,26 @@ lms_status  lms_read_lr1(lms_query* q, lms_lr1_row* rows, uint64_t cap, uint64_t
                          uint64_t* remaining);
 lms_status  lms_num_batches(lms_query* q, uint64_t* n);
 lms_status  lms_get_batch_record(lms_query* q, uint64_t batch_index, lms_batch_record* out);
+
+/* ------------------------------------------------------------------ multi-GPU (world > 1)
+ * One handle per GPU / rank; the caller owns the collectives (NCCL via torch.distributed in
+ * paper_2111_04289_b200/dist.py).  Per micro-batch:
+ *   lms_force_batch / lms_poll   admit + launch the aggregate pass only (rank-local rows)
+ *   all-reduce MAX of *wm, MIN of *ts_min on `stream` (lms_watermark_ptrs): one global
+ *                                watermark (reading R7) on every rank
+ *   lms_run_close                close windows as PARTIAL rows (count, exact sum, no HAVING /
+ *                                rank) bucketed by owner rank = fmix64(key) % world
+ *   lms_sync                     wait; partial rows stay on the device
+ *   lms_partials                 device pointer of the bucketed rows + per-owner counts
+ *   all-to-all of the rows (lms_agg_row bytes)
+ *   lms_merge                    owner merge of the received rows -> final rows (AVG,
+ *                                HAVING, ORDER BY rank) -> host row FIFO (lms_read_agg)   */
+/* Device pointers of the live watermark (max kept ts + 1, 0 = none; u64) and of the batch's
+ * minimum kept ts (u64, 0xFFFFFFFF = none), and the handle's cudaStream_t.               */
+lms_status  lms_watermark_ptrs(lms_query* q, void** wm_dptr, void** tsmin_dptr, void** stream);
+lms_status  lms_run_close(lms_query* q);
+lms_status  lms_partials(lms_query* q, const void** rows_dptr, uint64_t* counts /*[world]*/);
+lms_status  lms_merge(lms_query* q, const void* rows_dptr, uint64_t n_rows);
 
 /* ------------------------------------------------------------------ timing hooks */
 /* Device time of the last completed batch's kernels, and of its dominant

@@ -42,7 +42,7 @@ class lms_config(C.Structure):
                 ("range_s", C.c_double), ("slide_s", C.c_double), ("num_cores", C.c_int32),
                 ("num_xways", C.c_int32), ("inf_pt_bytes", C.c_double), ("base_trans_cost", C.c_double),
                 ("max_batch_bytes", C.c_uint64), ("max_keys", C.c_uint64), ("max_result_rows", C.c_uint64),
-                ("pane_slots", C.c_uint32), ("flags", C.c_uint32)]
+                ("pane_slots", C.c_uint32), ("flags", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32)]
 
 
 class lms_agg_row(C.Structure):
@@ -96,6 +96,10 @@ _PROTOS = {
     "lms_read_lr1": (C.c_int32, [_Q, _P(lms_lr1_row), C.c_uint64, _P(C.c_uint64), _P(C.c_uint64)]),
     "lms_num_batches": (C.c_int32, [_Q, _P(C.c_uint64)]),
     "lms_get_batch_record": (C.c_int32, [_Q, C.c_uint64, _P(lms_batch_record)]),
+    "lms_watermark_ptrs": (C.c_int32, [_Q, _P(C.c_void_p), _P(C.c_void_p), _P(C.c_void_p)]),
+    "lms_run_close": (C.c_int32, [_Q]),
+    "lms_partials": (C.c_int32, [_Q, _P(C.c_void_p), _P(C.c_uint64)]),
+    "lms_merge": (C.c_int32, [_Q, C.c_void_p, C.c_uint64]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "lms_kernel_launches": (C.c_int32, [_Q, _P(C.c_uint64)]),
     "lms_est_max_lat": (C.c_int32, [_P(C.c_double), _P(C.c_uint64), C.c_uint64, C.c_double, _P(C.c_double)]),

@@ -194,7 +194,7 @@ __device__ __forceinline__ void flush_counters(CtaCounters c, DevState* st) {
       if (bad) atomicAdd(&st->bad, bad);
       if (late) atomicAdd(&st->late, late);
       if (ovf) atomicAdd(&st->overflow, ovf);
-      if (mn != kEmpty32) atomicMin(&st->ts_min, mn);
+      if (mn != kEmpty32) atomicMin(&st->ts_min, (unsigned long long)mn);
       if (mx) atomicMax(&st->wm, (unsigned long long)mx);
     }
   }

@@ -23,6 +23,7 @@ constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 constexpr uint32_t kFail32 = 0xFFFFFFFEu;   // pane table full: the pane's records overflow
 constexpr unsigned long long kEmpty64 = ~0ull;
 constexpr int kMaxSegs = 16;
+constexpr int kMaxWorld = 64;                          // multi-GPU ranks
 constexpr int kLrRecBytes = 70;
 constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records
 constexpr int kLrTileBytes = kLrTileRecs * kLrRecBytes; // 35840 = 16 * 2240
@@ -42,7 +43,8 @@ struct DevState {
   long long next_k;             // first window instance not yet emitted
   long long evict_upto;         // LR1: panes <= this are evicted by k_lr1_evict
   unsigned int next_k_valid;
-  unsigned int ts_min;          // min kept ts of the current batch (0xFFFFFFFF = none)
+  unsigned long long ts_min;    // min kept ts of the current batch (0xFFFFFFFF = none); u64 so
+                                // that multi-GPU ranks can all-reduce it as int64
   unsigned long long n_records, bad, late, overflow, rows, windows_closed;
   unsigned int row_overflow;
   unsigned int close_ticket;
@@ -53,6 +55,10 @@ struct DevState {
   unsigned int fifo_overflow;
   int free_top;                 // free accumulator slots on the stack
   unsigned int pane_fail;       // a pane found no free slot (table entry marked kFail32)
+  long long close_k_first, close_k_last;   // instances closed by the last close (multi-GPU)
+  unsigned long long part_rows;            // partial rows of the last close (multi-GPU)
+  unsigned int owner_count[kMaxWorld];     // partial rows per owner rank
+  unsigned int owner_cursor[kMaxWorld];
 };
 
 // Copied to the host after every batch.
@@ -60,6 +66,9 @@ struct BatchReport {
   unsigned long long n_records, bad, late, overflow, rows, windows_closed;
   long long watermark;          // -1 if none
   unsigned int n_keys, row_overflow, key_overflow, fifo_overflow;
+  long long close_k_first, close_k_last;
+  unsigned long long part_rows;
+  unsigned int owner_count[kMaxWorld];
 };
 
 struct Segment {
@@ -114,6 +123,12 @@ struct QueryDev {
   unsigned long long row_cap;
   Lr1Retained* fifo[2];
   unsigned long long fifo_cap;
+  // multi-GPU (world > 1): partial rows bucketed by owner, owner-side merge accumulators
+  uint32_t rank, world;
+  void* send_rows;              // lms_agg_row[row_cap], grouped by owner rank
+  unsigned long long* macc_sum; // [Wmerge][K]
+  unsigned long long* macc_cnt; // [Wmerge][K]
+  uint32_t Wmerge;              // instances merged per merge pass
 };
 
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
@@ -124,7 +139,9 @@ cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
 cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st);
 cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st);
-cudaError_t launch_state_init(const QueryDev& q, cudaStream_t st);
+cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st);
+cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
+                         uint32_t nwin, cudaStream_t st);
 int close_ctas(const QueryDev& q);
 
 }  // namespace lms

@@ -113,10 +113,18 @@ __device__ void finish(const QueryDev& q, const WinRange& w) {
     for (uint32_t i = threadIdx.x; i < 2 * q.n_agg_ctas; i += blockDim.x) q.part_tag[i] = kEmpty64;
   if (w.any && !lr1) evict_rebuild_cta(q, w.k_last);      // LR1: k_lr1_evict frees the slots
   __syncthreads();
+  for (uint32_t i = threadIdx.x; i < kMaxWorld; i += blockDim.x) {   // bucket counters (multi-GPU)
+    st->owner_count[i] = 0;
+    st->owner_cursor[i] = 0;
+  }
   if (threadIdx.x == 0) {
+    st->close_k_first = 0;
+    st->close_k_last = -1;
     if (w.any) {
       const long long closed = w.k_last >= w.nk ? (w.k_last - w.nk + 1) : 0;
       st->windows_closed += (unsigned long long)closed;
+      st->close_k_first = w.nk;
+      st->close_k_last = w.k_last;
       st->evict_upto = w.k_last;
       st->next_k = w.k_last + 1 > w.nk ? w.k_last + 1 : w.nk;
       st->next_k_valid = 1;
@@ -126,12 +134,16 @@ __device__ void finish(const QueryDev& q, const WinRange& w) {
       st->fifo_cur ^= 1u;
     }
     st->wm_prev = st->wm;
+    st->part_rows = st->rows < q.row_cap ? st->rows : q.row_cap;
     BatchReport* r = q.report;
     r->n_records = st->n_records; r->bad = st->bad; r->late = st->late; r->overflow = st->overflow;
     r->rows = st->rows; r->windows_closed = st->windows_closed;
     r->watermark = st->wm ? (long long)st->wm - 1 : -1;
     r->n_keys = st->n_keys; r->row_overflow = st->row_overflow; r->key_overflow = st->key_overflow;
     r->fifo_overflow = st->fifo_overflow;
+    r->close_k_first = st->close_k_first;
+    r->close_k_last = st->close_k_last;
+    r->part_rows = st->part_rows;
     st->n_records = st->bad = st->late = st->overflow = st->rows = st->windows_closed = 0;
     st->row_overflow = 0;
     st->fifo_overflow = 0;
@@ -261,7 +273,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
           const uint32_t c = threadIdx.x;
           const bool want = c < 10 && s_cnt[c] > 0;
           uint32_t rank = 0;
-          if (want)
+          if (want && q.world == 1)                             // multi-GPU: the owner ranks
             for (uint32_t j = 0; j < 10; j++)
               if (s_cnt[j] > 0 && (s_sum[j] < s_sum[c] || (s_sum[j] == s_sum[c] && j < c))) rank++;
           const unsigned long long pos = row_slot(st, want);
@@ -299,7 +311,8 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
         if (q.kind == kLR2S) {
           sum = (double)s;                 // integer speed sum, exact below 2^53
           avg = want ? sum / (double)c : 0.0;
-          want = want && (avg < 40.0);     // HAVING (avgSpeed < 40.0)
+          // HAVING (avgSpeed < 40.0); multi-GPU partial rows are filtered by the owner
+          want = want && (q.world > 1 || avg < 40.0);
         } else {
           sum = (double)s / 1e6;           // SUM(cpu) from the exact fixed-point sum (R20)
           avg = want ? sum / (double)c : 0.0;

@@ -1,0 +1,209 @@
+// Multi-GPU row partitioning: owner bucketing of partial window rows and the owner-side merge.
+//
+// PAPER.md: the paper's micro-batch is split into partitions processed in parallel by the
+// executors and aggregated after a shuffle ("Shuffling", Table III P:751;
+// "shuffle aggregate" P:962).  Here every rank (GPU) aggregates its own rows of each micro-
+// batch; when instances close, each rank emits PARTIAL rows (count, exact integer sum per
+// (instance, key)), the rows are exchanged by owner rank (NCCL all-to-all, dist.py) and the
+// owner merges them and applies what needs the whole group: AVG, HAVING (LR2), ORDER BY rank
+// (CM1).  Owner = fmix64(key) % world for LR2/CM2 (no cross-key operation); for CM1 the
+// owner of an instance is k % world so that one rank sees every category of it (ORDER BY).
+#include "../../include/lmstream.h"
+#include "common.cuh"
+
+namespace lms {
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t owner_of(const QueryDev& q, const lms_agg_row& r) {
+  if (q.kind == kCM1S || q.kind == kCM1T) {
+    const long long k = floor_div(r.win_start_s, (long long)q.S);
+    const long long m = k % (long long)q.world;
+    return (uint32_t)(m < 0 ? m + q.world : m);
+  }
+  return (uint32_t)(fmix64(r.key) % q.world);
+}
+
+__global__ void __launch_bounds__(kThreads) k_bucket_count(const QueryDev q) {
+  __shared__ uint32_t s_cnt[kMaxWorld];
+  DevState* st = q.state;
+  const unsigned long long n = st->part_rows;
+  for (uint32_t i = threadIdx.x; i < q.world; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const lms_agg_row* rows = reinterpret_cast<const lms_agg_row*>(q.rows);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    atomicAdd(&s_cnt[owner_of(q, rows[i])], 1u);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < q.world; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&st->owner_count[i], s_cnt[i]);
+}
+
+__global__ void __launch_bounds__(kThreads) k_bucket_scatter(const QueryDev q) {
+  __shared__ uint32_t s_off[kMaxWorld];
+  DevState* st = q.state;
+  const unsigned long long n = st->part_rows;
+  if (threadIdx.x == 0) {
+    uint32_t o = 0;
+    for (uint32_t i = 0; i < q.world; i++) { s_off[i] = o; o += st->owner_count[i]; }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (uint32_t i = threadIdx.x; i < q.world; i += blockDim.x) q.report->owner_count[i] = st->owner_count[i];
+  const lms_agg_row* rows = reinterpret_cast<const lms_agg_row*>(q.rows);
+  lms_agg_row* out = reinterpret_cast<lms_agg_row*>(q.send_rows);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const lms_agg_row r = rows[i];
+    const uint32_t o = owner_of(q, r);
+    out[s_off[o] + atomicAdd(&st->owner_cursor[o], 1u)] = r;
+  }
+}
+
+// Received partial rows of instances [k_lo, k_lo + nwin) -> merge accumulators.
+__global__ void __launch_bounds__(kThreads) k_merge(const QueryDev q, const lms_agg_row* rows,
+                                                    unsigned long long n, long long k_lo, uint32_t nwin) {
+  DevState* st = q.state;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const lms_agg_row r = rows[i];
+    const long long w = floor_div(r.win_start_s, (long long)q.S) - k_lo;
+    if (w < 0 || w >= (long long)nwin) continue;
+    uint32_t idx;
+    if (q.kind == kCM2S) idx = dict_get(q.dict, r.key, st);
+    else idx = (uint32_t)r.key;
+    if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
+    const size_t g = (size_t)w * q.K + idx;
+    atomicAdd(&q.macc_sum[g], r.sum_fixed);
+    atomicAdd(&q.macc_cnt[g], r.count);
+  }
+}
+
+__device__ __forceinline__ unsigned long long append_row(DevState* st, bool want) {
+  const uint32_t act = __activemask();
+  const uint32_t m = __ballot_sync(act, want);
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  const int leader = m ? __ffs(m) - 1 : 0;
+  if (m && (int)lane == leader) base = atomicAdd(&st->rows, (unsigned long long)__popc(m));
+  base = __shfl_sync(act, base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
+// Merged accumulators -> final rows (AVG, HAVING) for LR2 / CM2; zeroes what it reads.
+__global__ void __launch_bounds__(kThreads) k_finalize(const QueryDev q, long long k_lo, uint32_t nwin) {
+  DevState* st = q.state;
+  const uint32_t K = q.kind == kCM2S ? min(st->n_keys, q.K) : q.K;
+  lms_agg_row* rows = reinterpret_cast<lms_agg_row*>(q.rows);
+  const unsigned long long total = (unsigned long long)nwin * K;
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  const unsigned long long iters = (total + stride - 1) / stride;
+  for (unsigned long long it = 0; it < iters; it++) {
+    const unsigned long long i = it * stride + blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+    unsigned long long s = 0, c = 0;
+    uint32_t w = 0, key = 0;
+    if (i < total) {
+      w = (uint32_t)(i / K);
+      key = (uint32_t)(i - (unsigned long long)w * K);
+      const size_t g = (size_t)w * q.K + key;
+      s = q.macc_sum[g];
+      c = q.macc_cnt[g];
+      if (c) { q.macc_sum[g] = 0; q.macc_cnt[g] = 0; }
+    }
+    bool want = c > 0;
+    double sum, avg;
+    if (q.kind == kLR2S) {
+      sum = (double)s;
+      avg = want ? sum / (double)c : 0.0;
+      want = want && (avg < 40.0);                             // HAVING (avgSpeed < 40.0)
+    } else {
+      sum = (double)s / 1e6;
+      avg = want ? sum / (double)c : 0.0;
+    }
+    const unsigned long long pos = append_row(st, want);
+    if (want) {
+      if (pos < q.row_cap) {
+        lms_agg_row r;
+        const long long k = k_lo + (long long)w;
+        r.win_start_s = k * (long long)q.S;
+        r.win_end_s = r.win_start_s + (long long)q.R;
+        r.count = c; r.sum_fixed = s; r.sum = sum; r.avg = avg; r.rank = 0;
+        if (q.kind == kLR2S) {
+          r.key = key; r.key_xway = key / 200u; r.key_dir = (key / 100u) % 2u; r.key_seg = key % 100u;
+        } else {
+          r.key = q.dict.key_by_idx[key]; r.key_xway = r.key_dir = r.key_seg = 0;
+        }
+        rows[pos] = r;
+      } else {
+        atomicExch(&st->row_overflow, 1u);
+      }
+    }
+  }
+}
+
+// CM1: one CTA per instance; ORDER BY SUM(cpu) ascending, ties by category (reading R9).
+__global__ void __launch_bounds__(32) k_finalize_cm1(const QueryDev q, long long k_lo) {
+  DevState* st = q.state;
+  const uint32_t w = blockIdx.x, c = threadIdx.x;
+  __shared__ unsigned long long s_sum[10], s_cnt[10];
+  if (c < 10) {
+    const size_t g = (size_t)w * q.K + c;
+    s_sum[c] = q.macc_sum[g];
+    s_cnt[c] = q.macc_cnt[g];
+    q.macc_sum[g] = 0;
+    q.macc_cnt[g] = 0;
+  }
+  __syncwarp();
+  const bool want = c < 10 && s_cnt[c] > 0;
+  uint32_t rank = 0;
+  if (want)
+    for (uint32_t j = 0; j < 10; j++)
+      if (s_cnt[j] > 0 && (s_sum[j] < s_sum[c] || (s_sum[j] == s_sum[c] && j < c))) rank++;
+  const unsigned long long pos = append_row(st, want);
+  if (want) {
+    lms_agg_row* rows = reinterpret_cast<lms_agg_row*>(q.rows);
+    if (pos < q.row_cap) {
+      lms_agg_row r;
+      const long long k = k_lo + (long long)w;
+      r.win_start_s = k * (long long)q.S;
+      r.win_end_s = r.win_start_s + (long long)q.R;
+      r.key = c; r.count = s_cnt[c]; r.sum_fixed = s_sum[c];
+      r.sum = (double)s_sum[c] / 1e6;
+      r.avg = r.sum / (double)s_cnt[c];
+      r.key_xway = r.key_dir = r.key_seg = 0;
+      r.rank = rank;
+      rows[pos] = r;
+    } else {
+      atomicExch(&st->row_overflow, 1u);
+    }
+  }
+}
+
+int sm_count() {
+  static int nsm = -1;
+  if (nsm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+
+}  // namespace
+
+cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st) {
+  k_bucket_count<<<sm_count(), kThreads, 0, st>>>(q);
+  k_bucket_scatter<<<sm_count(), kThreads, 0, st>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
+                         uint32_t nwin, cudaStream_t st) {
+  if (n) k_merge<<<sm_count(), kThreads, 0, st>>>(q, static_cast<const lms_agg_row*>(rows), n, k_lo, nwin);
+  if (q.kind == kCM1S || q.kind == kCM1T) k_finalize_cm1<<<nwin, 32, 0, st>>>(q, k_lo);
+  else k_finalize<<<sm_count(), kThreads, 0, st>>>(q, k_lo, nwin);
+  return cudaGetLastError();
+}
+
+}  // namespace lms

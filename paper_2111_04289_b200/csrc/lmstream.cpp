@@ -114,6 +114,8 @@ struct lms_query {
   bool in_flight = false;
   int in_flight_buf = 0;
   bool in_flight_flush = false;
+  bool awaiting_close = false;     // multi-GPU: aggregate pass launched, close not yet
+  BatchReport last_report{};
   cudaEvent_t ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
   lms_batch_record cur{};
   std::vector<lms_batch_record> records;
@@ -170,8 +172,15 @@ lms_status validate_config(const lms_config* c) {
   if (c->max_batch_bytes == 0 || c->max_batch_bytes > (1ull << 40)) return fail(LMS_EINVAL, "max_batch_bytes");
   if (c->max_keys == 0 || c->max_keys > (1ull << 30)) return fail(LMS_EINVAL, "max_keys");
   if (c->max_result_rows == 0 || c->max_result_rows > (1ull << 32)) return fail(LMS_EINVAL, "max_result_rows");
+  if (c->world < 1 || c->world > kMaxWorld || c->rank < 0 || c->rank >= c->world)
+    return fail(LMS_EINVAL, "need 0 <= rank < world <= 64");
+  if (c->world > 1 && is_lr1(c->kind)) return fail(LMS_EINVAL, "LR1 runs on one GPU (world must be 1)");
+  if (c->world > 1 && c->mode != LMS_MODE_MANUAL)
+    return fail(LMS_EINVAL, "multi-GPU handles use LMS_MODE_MANUAL (the caller forms batches in lockstep)");
   return LMS_OK;
 }
+
+lms_status launch_close_stage(lms_query* q);
 
 lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bool flush) {
   // ---- batch composition: every pending dataset (Alg. 1 admits tmpMicroBatch whole)
@@ -232,17 +241,31 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
     q->launches++;
   }
   CUDA_TRY(cudaEventRecord(q->ev_agg, q->stream));
-  CUDA_TRY(launch_close(q->qd, flush ? 1 : 0, q->stream));
+  q->in_flight_flush = flush;
+  if (q->qd.world > 1) {            // multi-GPU: the caller all-reduces the watermark first
+    q->awaiting_close = true;
+    return LMS_OK;
+  }
+  return launch_close_stage(q);
+}
+
+// Window close (+ LR1 eviction, + multi-GPU owner bucketing), batch report, end event.
+lms_status launch_close_stage(lms_query* q) {
+  CUDA_TRY(launch_close(q->qd, q->in_flight_flush ? 1 : 0, q->stream));
   q->launches++;
   if (is_lr1(q->kind)) {
     CUDA_TRY(launch_lr1_evict(q->qd, q->stream));
     q->launches++;
   }
+  if (q->qd.world > 1) {
+    CUDA_TRY(launch_bucket(q->qd, q->stream));
+    q->launches += 2;
+  }
   CUDA_TRY(cudaEventRecord(q->ev_close, q->stream));
   CUDA_TRY(cudaMemcpyAsync(q->h_report, q->qd.report, sizeof(BatchReport), cudaMemcpyDeviceToHost, q->stream));
   CUDA_TRY(cudaEventRecord(q->ev_end, q->stream));
+  q->awaiting_close = false;
   q->in_flight = true;
-  q->in_flight_flush = flush;
   return LMS_OK;
 }
 
@@ -260,8 +283,9 @@ lms_status complete(lms_query* q) {
   q->last_batch_s = ms_total * 1e-3;
   q->last_agg_s = ms_agg * 1e-3;
   q->last_close_s = ms_close * 1e-3;
-  // result rows -> host FIFO
-  const uint64_t nrows = std::min<uint64_t>(rep.rows, q->cfg.max_result_rows);
+  // result rows -> host FIFO (multi-GPU: partial rows stay on the device for lms_merge)
+  q->last_report = rep;
+  const uint64_t nrows = q->qd.world > 1 ? 0 : std::min<uint64_t>(rep.rows, q->cfg.max_result_rows);
   double d2h = 0;
   if (nrows) {
     const double t0 = now_host();
@@ -351,6 +375,8 @@ lms_status lms_config_init(lms_config* c, int32_t kind) {
   c->max_result_rows = is_lr1(kind) ? (1ull << 22) : (1ull << 20);
   c->pane_slots = 0;
   c->flags = 0;
+  c->rank = 0;
+  c->world = 1;
   return LMS_OK;
 }
 
@@ -405,8 +431,18 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       default: d.K = (uint32_t)cfg->max_keys; break;
     }
     d.n_agg_ctas = (uint32_t)(is_lr(q->kind) ? lr_agg_ctas(d) : cm_agg_ctas(d));
+    d.rank = (uint32_t)cfg->rank;
+    d.world = (uint32_t)cfg->world;
     Q_TRY(q->dalloc(&d.state, 1, 0));
     Q_TRY(q->dalloc(&d.report, 1, 0));
+    if (d.world > 1) {                // owner-side merge of partial rows
+      lms_agg_row* send;
+      Q_TRY(q->dalloc(&send, cfg->max_result_rows, 0));
+      d.send_rows = send;
+      d.Wmerge = q->ppw + 8;
+      Q_TRY(q->dalloc(&d.macc_sum, (size_t)d.Wmerge * d.K, 0));
+      Q_TRY(q->dalloc(&d.macc_cnt, (size_t)d.Wmerge * d.K, 0));
+    }
     {
       const uint64_t H = next_pow2(4ull * q->P);
       d.H_mask = (uint32_t)(H - 1);
@@ -587,8 +623,9 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
     if (bidx) *bidx = UINT64_MAX;
-    if (q->in_flight) return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
-    if (q->pending.empty()) return LMS_OK;
+    if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
+    // multi-GPU ranks run their batches in lockstep: an empty rank still runs the batch
+    if (q->pending.empty() && q->qd.world == 1) return LMS_OK;
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status s = launch_batch(q, now, kAdmitForced, std::nan(""), false);
     if (s) return s;
@@ -602,6 +639,7 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
 lms_status lms_sync(lms_query* q) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
+    if (q->awaiting_close) return fail(LMS_ESTATE, "multi-GPU batch: call lms_run_close first");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     if (!q->in_flight) return LMS_OK;
     return complete(q);
@@ -613,10 +651,12 @@ lms_status lms_sync(lms_query* q) {
 lms_status lms_flush(lms_query* q, double now) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
+    if (q->awaiting_close) return fail(LMS_ESTATE, "multi-GPU batch: call lms_run_close first");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status s1 = complete(q);
     lms_status s = launch_batch(q, now, kAdmitFlush, std::nan(""), true);
     if (s) return s;
+    if (q->qd.world > 1) return s1;   // the caller completes the multi-GPU protocol
     lms_status s2 = complete(q);
     return s2 ? s2 : s1;
   } catch (...) {
@@ -667,6 +707,76 @@ lms_status lms_kernel_launches(lms_query* q, uint64_t* n) {
   if (!q || !n) return fail(LMS_EINVAL, "null argument");
   *n = q->launches;
   return LMS_OK;
+}
+
+// ------------------------------------------------------------------ multi-GPU protocol
+lms_status lms_watermark_ptrs(lms_query* q, void** wm, void** tsmin, void** stream) {
+  if (!q || !wm || !tsmin || !stream) return fail(LMS_EINVAL, "null argument");
+  *wm = &q->qd.state->wm;
+  *tsmin = &q->qd.state->ts_min;
+  *stream = q->stream;
+  return LMS_OK;
+}
+
+lms_status lms_run_close(lms_query* q) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    if (!q->awaiting_close) return fail(LMS_ESTATE, "no aggregate pass awaiting its close");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    return launch_close_stage(q);
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in run_close");
+  }
+}
+
+lms_status lms_partials(lms_query* q, const void** rows, uint64_t* counts) {
+  if (!q || !rows || !counts) return fail(LMS_EINVAL, "null argument");
+  if (q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU handle");
+  if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
+  *rows = q->qd.send_rows;
+  for (uint32_t r = 0; r < q->qd.world; r++) counts[r] = q->last_report.owner_count[r];
+  return LMS_OK;
+}
+
+lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
+  try {
+    if (!q || (n && !rows)) return fail(LMS_EINVAL, "null argument");
+    if (q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU handle");
+    if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    const double t0 = now_host();
+    const BatchReport& rep = q->last_report;
+    for (long long k = rep.close_k_first; k <= rep.close_k_last; k += q->qd.Wmerge) {
+      const uint32_t nwin = (uint32_t)std::min<long long>(q->qd.Wmerge, rep.close_k_last - k + 1);
+      CUDA_TRY(launch_merge(q->qd, rows, n, k, nwin, q->stream));
+      q->launches += 2;
+    }
+    // final rows -> pinned staging -> host FIFO
+    unsigned long long* d_rows = &q->qd.state->rows;
+    CUDA_TRY(cudaMemcpyAsync(q->h_rows, d_rows, sizeof(unsigned long long), cudaMemcpyDeviceToHost, q->stream));
+    CUDA_TRY(cudaStreamSynchronize(q->stream));
+    const uint64_t total = *static_cast<unsigned long long*>(q->h_rows);
+    const uint64_t nrows = std::min<uint64_t>(total, q->cfg.max_result_rows);
+    const uint8_t* src = static_cast<const uint8_t*>(q->qd.rows);
+    for (uint64_t done = 0; done < nrows;) {
+      const uint64_t m = std::min<uint64_t>(nrows - done, q->h_rows_cap);
+      CUDA_TRY(cudaMemcpyAsync(q->h_rows, src + done * sizeof(lms_agg_row), m * sizeof(lms_agg_row),
+                               cudaMemcpyDeviceToHost, q->stream));
+      CUDA_TRY(cudaStreamSynchronize(q->stream));
+      q->agg_rows.append(static_cast<const lms_agg_row*>(q->h_rows), m);
+      done += m;
+    }
+    CUDA_TRY(cudaMemsetAsync(d_rows, 0, sizeof(unsigned long long), q->stream));
+    if (!q->records.empty()) {
+      lms_batch_record& r = q->records.back();
+      r.rows_emitted = nrows;
+      r.d2h_s += now_host() - t0;
+    }
+    if (total > nrows) return fail(LMS_EOVERFLOW, "merged rows exceed max_result_rows");
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in merge");
+  }
 }
 
 // ------------------------------------------------------------------ pure functions

@@ -1,0 +1,195 @@
+"""Multi-GPU execution: row-partitioned micro-batches + partial-aggregate exchange.
+
+PAPER.md: the micro-batch is split into partitions processed in parallel and the
+partial aggregates are shuffled before the final aggregation ("Shuffling", Table III P:751;
+"shuffle aggregate" P:962).  Here one process drives one GPU (torchrun; NCCL via
+torch.distributed — PyTorch is the process-group plumbing only).  Every rank owns one
+lms_query (lms_config.rank/world) and processes its own rows of each micro-batch; per batch:
+
+  1. lms_force_batch          aggregate pass over the rank's rows (CUDA kernel)
+  2. all-reduce MAX / MIN      global watermark and first-batch ts_min (reading R7) — NCCL on
+                               the handle's stream, no host round trip
+  3. lms_run_close             partial rows of the closing instances, bucketed by owner rank
+                               (kernels)
+  4. lms_sync                  wait
+  5. all-to-all                partial rows to their owners (NCCL, bytes of lms_agg_row)
+  6. lms_merge                 owner-side merge + AVG / HAVING / ORDER BY rank (kernels)
+
+`Exchange` implementations: TorchDistExchange (one handle per process, any torch.distributed
+backend: NCCL on GPUs, gloo for the CPU protocol tests) and LocalExchange (several handles on
+one GPU in one process — "virtual shards", used to test the kernels of the protocol on a
+single GPU).  The fused device-initiated exchange (NCCL device API / NVLS) is the next step
+(SURVEY §8f f1), not this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import check
+
+ROW_BYTES = C.sizeof(L.lms_agg_row)
+
+
+class _CudaPtr:
+    """Raw device pointer exposed through __cuda_array_interface__ (for torch.as_tensor)."""
+
+    def __init__(self, ptr: int, nbytes: int, typestr: str = "|u1", itemsize: int = 1):
+        self.__cuda_array_interface__ = {"shape": (nbytes // itemsize,), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def device_view(ptr: int, nbytes: int, dtype="u1"):
+    import torch
+    typestr, size = {"u1": ("|u1", 1), "i8": ("<i8", 8)}[dtype]
+    if nbytes == 0:
+        return torch.empty(0, dtype=torch.uint8 if dtype == "u1" else torch.int64, device="cuda")
+    return torch.as_tensor(_CudaPtr(ptr, nbytes, typestr, size), device="cuda")
+
+
+# ----------------------------------------------------------------------------- host split
+
+def split_points(family: str, data, world: int) -> list[tuple[int, int]]:
+    """Row partition of one dataset at record boundaries: [(offset, nbytes)] per rank.
+
+    LR: multiples of 70 B; CM: each cut advanced to the byte after the next '\\n' (records
+    are <= 256 B, so the host scans at most one record per cut).
+    """
+    buf = memoryview(data).cast("B") if not isinstance(data, np.ndarray) else data
+    n = len(buf)
+    cuts = [0]
+    for r in range(1, world):
+        c = n * r // world
+        if family == "LR":
+            c -= c % 70
+        else:
+            while c < n and (c == 0 or buf[c - 1] != ord("\n")):
+                c += 1
+        cuts.append(max(c, cuts[-1]))
+    cuts.append(n)
+    return [(cuts[i], cuts[i + 1] - cuts[i]) for i in range(world)]
+
+
+# ----------------------------------------------------------------------------- handles
+
+class RankHandle:
+    """One rank's lms_query plus typed views of its protocol buffers."""
+
+    def __init__(self, query):
+        self.q = query
+        self.world = query.cfg.world
+        wm, tsmin, stream = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        check(L.lms_watermark_ptrs(query.h, C.byref(wm), C.byref(tsmin), C.byref(stream)), "lms_watermark_ptrs")
+        self.wm_ptr, self.tsmin_ptr, self.stream_ptr = wm.value, tsmin.value, stream.value or 0
+
+    def watermark_tensors(self):
+        return device_view(self.wm_ptr, 8, "i8"), device_view(self.tsmin_ptr, 8, "i8")
+
+    def partials(self):
+        """(uint8 device tensor of the bucketed partial rows, per-owner row counts)."""
+        ptr = C.c_void_p()
+        counts = (C.c_uint64 * self.world)()
+        check(L.lms_partials(self.q.h, C.byref(ptr), counts), "lms_partials")
+        cnt = [int(c) for c in counts]
+        return device_view(ptr.value or 0, sum(cnt) * ROW_BYTES), cnt
+
+    def merge(self, rows_u8):
+        n = rows_u8.numel() // ROW_BYTES
+        ptr = rows_u8.data_ptr() if n else None
+        return check(L.lms_merge(self.q.h, C.c_void_p(ptr), n), "lms_merge", (L.LMS_OK, L.LMS_EOVERFLOW))
+
+
+# ----------------------------------------------------------------------------- exchanges
+
+class TorchDistExchange:
+    """torch.distributed collectives (one handle per process)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def _on(self, h):
+        import torch
+        if h is None or not getattr(h, "stream_ptr", 0):
+            return _Null()
+        return torch.cuda.stream(torch.cuda.ExternalStream(h.stream_ptr))
+
+    def allreduce_watermarks(self, handles):
+        (h,) = handles
+        wm, tsmin = h.watermark_tensors()
+        with self._on(h):
+            self.dist.all_reduce(wm, op=self.dist.ReduceOp.MAX, group=self.group)
+            self.dist.all_reduce(tsmin, op=self.dist.ReduceOp.MIN, group=self.group)
+
+    def all_to_all(self, handles, sends):
+        """sends[0] = (uint8 rows tensor grouped by owner, per-owner counts) -> received rows."""
+        import torch
+        (h,), ((rows, counts),) = handles, sends
+        dev = rows.device
+        send_c = torch.tensor(counts, dtype=torch.int64, device=dev)
+        recv_c = torch.empty_like(send_c)
+        with self._on(h):
+            self.dist.all_to_all_single(recv_c, send_c, group=self.group)
+            rc = [int(x) for x in recv_c.tolist()]
+            recv = torch.empty(sum(rc) * ROW_BYTES, dtype=torch.uint8, device=dev)
+            self.dist.all_to_all_single(recv, rows, output_split_sizes=[c * ROW_BYTES for c in rc],
+                                        input_split_sizes=[c * ROW_BYTES for c in counts], group=self.group)
+        return [recv]
+
+
+class LocalExchange:
+    """All ranks' handles in one process (virtual shards on one GPU)."""
+
+    def allreduce_watermarks(self, handles):
+        import torch
+        torch.cuda.synchronize()
+        wms, tss = zip(*(h.watermark_tensors() for h in handles))
+        wm = torch.stack(list(wms)).max(0).values
+        ts = torch.stack(list(tss)).min(0).values
+        for a, b in zip(wms, tss):
+            a.copy_(wm)
+            b.copy_(ts)
+        torch.cuda.synchronize()
+
+    def all_to_all(self, handles, sends):
+        import torch
+        world = len(handles)
+        out = []
+        for d in range(world):
+            parts = []
+            for rows, counts in sends:
+                off = sum(counts[:d]) * ROW_BYTES
+                parts.append(rows[off:off + counts[d] * ROW_BYTES])
+            out.append(torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8, device="cuda"))
+        torch.cuda.synchronize()
+        return out
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+# ----------------------------------------------------------------------------- protocol
+
+def run_batch(handles, exchange, now: float, flush: bool = False) -> list[int]:
+    """One micro-batch on every local handle (steps 1-6 above).  Returns the sync statuses."""
+    for h in handles:
+        st = L.lms_flush(h.q.h, now) if flush else L.lms_force_batch(h.q.h, now, None)
+        check(st, "lms_flush" if flush else "lms_force_batch", (L.LMS_OK, L.LMS_EFORMAT))
+    exchange.allreduce_watermarks(handles)
+    for h in handles:
+        check(L.lms_run_close(h.q.h), "lms_run_close")
+    sts = [h.q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW)) for h in handles]
+    recvs = exchange.all_to_all(handles, [h.partials() for h in handles])
+    for h, rows in zip(handles, recvs):
+        h.merge(rows)
+    return sts

@@ -1,0 +1,111 @@
+"""Multi-GPU protocol on CPU: world_size-2 gloo processes run the exact TorchDistExchange code of
+paper_2111_04289_b200/dist.py on CPU tensors (watermark all-reduce + owner all-to-all of
+partial rows), plus the host-side record-boundary split.  The CUDA kernels of the protocol are
+covered by tests/test_gpu_dist.py (virtual shards on one GPU)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import lmsgen as g
+
+M64 = (1 << 64) - 1
+
+
+def fmix64(k):
+    k ^= k >> 33
+    k = (k * 0xff51afd7ed558ccd) & M64
+    k ^= k >> 33
+    k = (k * 0xc4ceb9fe1a85ec53) & M64
+    return k ^ (k >> 33)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class FakeHandle:
+    """CPU stand-in for dist.RankHandle: same interface, tensors on the CPU."""
+
+    def __init__(self, rank, world, rows, wm, tsmin):
+        from paper_2111_04289_b200 import AGG_DTYPE
+        self.world, self.stream_ptr = world, 0
+        owner = np.array([fmix64(int(k)) % world for k in rows["key"]], dtype=np.int64)
+        order = np.argsort(owner, kind="stable")
+        self.rows = rows[order]
+        self.counts = [int((owner == r).sum()) for r in range(world)]
+        self.wm = torch.tensor([wm], dtype=torch.int64)
+        self.ts = torch.tensor([tsmin], dtype=torch.int64)
+        self.dtype = AGG_DTYPE
+
+    def watermark_tensors(self):
+        return self.wm, self.ts
+
+    def partials(self):
+        return torch.from_numpy(self.rows.view(np.uint8).copy()), self.counts
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2111_04289_b200 import AGG_DTYPE
+        from paper_2111_04289_b200.dist import TorchDistExchange
+        rng = np.random.default_rng(rank)
+        rows = np.zeros(50 + 10 * rank, AGG_DTYPE)
+        rows["key"] = rng.integers(10 ** 9, 10 ** 10, len(rows))
+        rows["win_start_s"] = rng.integers(0, 5, len(rows)) * 5
+        rows["count"] = rank + 1
+        h = FakeHandle(rank, world, rows, wm=100 + 7 * rank, tsmin=3 - rank)
+        ex = TorchDistExchange()
+        ex.allreduce_watermarks([h])
+        (recv,) = ex.all_to_all([h], [h.partials()])
+        got = recv.numpy().view(AGG_DTYPE)
+        q.put((rank, int(h.wm.item()), int(h.ts.item()), got.tobytes(), rows.tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_exchange():
+    from paper_2111_04289_b200 import AGG_DTYPE
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    sent = np.concatenate([np.frombuffer(r[4], AGG_DTYPE) for r in res])
+    for rank, wm, ts, got_b, _ in res:
+        assert wm == 107 and ts == 2                                 # MAX / MIN over ranks
+        got = np.frombuffer(got_b, AGG_DTYPE)
+        want = sent[[fmix64(int(k)) % world == rank for k in sent["key"]]]
+        assert sorted(map(bytes, got)) == sorted(map(bytes, want))   # exactly the rows it owns
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_split_points_record_boundaries(world):
+    from paper_2111_04289_b200.dist import split_points
+    cm = b"".join(d for _, d in g.stream_datasets("CM", "B(0.5)", 3))
+    parts = split_points("CM", cm, world)
+    assert sum(n for _, n in parts) == len(cm)
+    assert b"".join(cm[o:o + n] for o, n in parts) == cm
+    for o, n in parts:
+        assert o == 0 or cm[o - 1] == ord("\n")
+        assert n == 0 or cm[o + n - 1] == ord("\n")
+    lr = b"".join(d for _, d in g.stream_datasets("LR", "B(0.3)", 2))
+    parts = split_points("LR", lr, world)
+    assert all(o % 70 == 0 and n % 70 == 0 for o, n in parts)
+    assert sum(n for _, n in parts) == len(lr)
