@@ -140,13 +140,19 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
     import paper_2111_04289_b200 as P
     dev = torch.cuda.current_device()
     inputs = gen_inputs(wl, warmup + steps, 0, seed, torch)
-    q = P.Query(wl["kind"], mode="manual", device=dev, max_batch_bytes=1 << 20)
+    q = P.Query(wl["kind"], mode="manual", device=dev, max_batch_bytes=1 << 20, rank=rank, world=world)
     out = {"agg_s": [], "close_s": [], "batch_s": [], "rows": 0}
+    if world > 1:
+        from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
+        h, ex = RankHandle(q), TorchDistExchange()
 
     def step(buf, n, t):
         q.push_device(buf.data_ptr(), n, float(t))
-        q.force(float(t) + 1.0)
-        q.sync()
+        if world > 1:                     # partial aggregates merged by key owner over NCCL
+            run_batch([h], ex, float(t) + 1.0)
+        else:
+            q.force(float(t) + 1.0)
+            q.sync()
         rows = q.read_agg()
         return len(rows)
 
@@ -184,8 +190,10 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
     return out
 
 
-def e2e_run(wl, steps, warmup, seed, torch):
-    """Inputs in pinned host memory; each step: lms_push (H2D) + batch + rows to host."""
+def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None):
+    """Inputs in pinned host memory; each step: lms_push (H2D) + batch + rows to host.
+    N > 1: every rank pushes its own partition; batches run the dist.py protocol; the time is
+    the max over ranks."""
     import numpy as np
     import paper_2111_04289_b200 as P
     dev = torch.cuda.current_device()
@@ -200,19 +208,27 @@ def e2e_run(wl, steps, warmup, seed, torch):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     cap = max(n for _, n, _ in host) + 4096
-    q = P.Query(wl["kind"], mode="manual", device=dev, max_batch_bytes=cap)
+    q = P.Query(wl["kind"], mode="manual", device=dev, max_batch_bytes=cap, rank=rank, world=world)
+    if world > 1:
+        from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
+        hd, ex = RankHandle(q), TorchDistExchange()
     d2h = []
 
     def step(h, n, t):
         q.push((h.data_ptr(), n), float(t))
-        q.force(float(t) + 1.0)
-        q.sync()
+        if world > 1:
+            run_batch([hd], ex, float(t) + 1.0)
+        else:
+            q.force(float(t) + 1.0)
+            q.sync()
         rows = q.read_agg()
         d2h.append(rows.nbytes + 88)
         return rows
 
     for i in range(warmup):
         step(*host[i])
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -220,7 +236,13 @@ def e2e_run(wl, steps, warmup, seed, torch):
         step(*host[i])
     e1.record()
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     el = e0.elapsed_time(e1) / 1e3
+    if world > 1:
+        t = torch.tensor([el], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
     recs = [q.record(i) for i in range(warmup, n_sec)]
     q.close()
     return {"elapsed_s": el, "h2d_bytes_per_step": float(np.mean([n for _, n, _ in host[warmup:]])),
@@ -332,9 +354,9 @@ def main():
                "batch_device_ms_p99": 1e3 * pct(r2["batch_s"], 99),
                "traffic_ncu_bytes": ncu_traffic(args.secondary), "clocks": r2["clocks"]}
     e2e = None
-    if rank == 0 and args.e2e_steps > 0:
-        e = e2e_run(wl, args.e2e_steps, 1, seed, torch)
-        e2e = {"value": wl["records"] * args.e2e_steps / e["elapsed_s"], "unit": "records/s",
+    if args.e2e_steps > 0:
+        e = e2e_run(wl, args.e2e_steps, 1, seed, torch, rank, world, dist)
+        e2e = {"value": wl["records"] * world * args.e2e_steps / e["elapsed_s"], "unit": "records/s",
                "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
                "steps": args.e2e_steps, "proc_ms_p50": 1e3 * pct(e["proc_s"], 50),
                "proc_ms_p99": 1e3 * pct(e["proc_s"], 99), "h2d_ms_mean": 1e3 * statistics.mean(e["h2d_s"])}
