@@ -30,7 +30,7 @@ constexpr int kLrTileBytes = kLrTileRecs * kLrRecBytes; // 35840 = 16 * 2240
 constexpr int kCmWin = 16384;                          // CM tile window: payload + right halo
 constexpr int kCmHaloL = 16;
 constexpr int kCmHaloR = 256;                          // >= max line (255) + '\n'
-constexpr int kCmTile = kCmWin - kCmHaloR;             // CM tile payload bytes (32512)
+constexpr int kCmTile = kCmWin - kCmHaloR;             // CM tile payload bytes (16128)
 constexpr int kCmStage = kCmHaloL + kCmWin;
 constexpr int kCmMaxLine = 255;
 

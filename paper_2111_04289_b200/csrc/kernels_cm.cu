@@ -6,10 +6,11 @@
 // variable)"; operators Scan (CSV) / Filtering / Projection / Aggregation (Table III).
 // Record grammar: DESIGN.md reading R1 (13-column task_events line, <= 255 B + '\n').
 //
-// Design (B200).  A tile is a 32 KB window = 32512 B payload + 256 B right halo (the tail of
+// Design (B200).  A tile is a 16 KB window = 16128 B payload + 256 B right halo (the tail of
 // the last record that STARTS in the payload: a record belongs to the tile holding its first
-// byte) + a 16 B left halo (the byte before the tile).  Persistent CTAs walk a contiguous
-// tile range through a 2-stage smem ring filled by TMA-engine bulk copies (cp.async.bulk).
+// byte) + a 16 B left halo (the byte before the tile).  Persistent CTAs (128 threads, 5 per
+// SM) walk a contiguous tile range through a 2-stage smem ring filled by TMA-engine bulk
+// copies (cp.async.bulk).
 //  * Pass 1 (all threads, round-robin 16 B pieces: conflict-free LDS.128): exact SWAR byte
 //    equality against '\n' and ',' (3 ops per class per word + a shared AND), gathered to one
 //    mask bit per byte with IDP.4A; masks go to smem.
