@@ -36,7 +36,7 @@ constexpr int kCtasPerSm = 5;
 constexpr int kCmStages = 2;
 constexpr int kChunk = kCmWin / kCmThreads;                  // 128 B window chunk per thread
 constexpr int kMaskBits = kCmWin;                            // mask bit i <-> stage byte 16 + i
-constexpr int kMaskWords = kMaskBits / 64;                   // 512
+constexpr int kMaskWords = kMaskBits / 64;                   // 256
 constexpr int kPieces = kMaskBits / 16;                      // 2048 pieces of 16 B
 static_assert(kChunk == 128 && kPieces == 8 * kCmThreads, "one 128 B chunk / 8 pieces per thread");
 constexpr int kSurvCap = 64;                                 // per-warp survivor list
@@ -209,65 +209,84 @@ __device__ bool cm_parse_serial(const uint8_t* buf, uint32_t s, uint32_t limit, 
   return false;   // no '\n' within 256 bytes or before the segment end
 }
 
-// Bits [b, b+64) of the 64-bit words (a at word index w0, then b1, b2) with b - 64*w0 < 128.
-__device__ __forceinline__ void bits64_at(uint32_t rel, unsigned long long a, unsigned long long b,
-                                          unsigned long long c, uint32_t& lo, uint32_t& hi) {
-  // rel = b - 64*w0 in [0, 128): take the 64 bits starting at rel from the 192-bit a|b|c
-  const unsigned long long x = rel < 64 ? a : b, y = rel < 64 ? b : c;
-  const uint32_t sh = rel & 63;
-  const unsigned long long v = sh ? ((x >> sh) | (y << (64 - sh))) : x;
-  lo = (uint32_t)v;
-  hi = (uint32_t)(v >> 32);
+// ---- 32-bit mask helpers (the '\n' / ',' masks are read as 32-bit words: bit i of the
+// window <-> word i >> 5, bit i & 31)
+__device__ __forceinline__ uint32_t lsb32(uint32_t x) { return (uint32_t)__ffs(x) - 1u; }   // x != 0
+__device__ __forceinline__ uint32_t msb32(uint32_t x) {                                   // x != 0
+  uint32_t r;
+  asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(x));
+  return r;
+}
+// low n bits set, n in [0, 32] (PTX shl clamps: 1 << 32 == 0)
+__device__ __forceinline__ uint32_t low_bits(uint32_t n) {
+  uint32_t r;
+  asm("{\n\t.reg .b32 t;\n\tshl.b32 t, 1, %1;\n\tsub.u32 %0, t, 1;\n\t}" : "=r"(r) : "r"(n));
+  return r;
+}
+__device__ __forceinline__ uint32_t clamp32(int n) { return (uint32_t)min(max(n, 0), 32); }
+
+// Pop the lowest set bit of the 128-bit chunk mask s0..s3 into b (chunk-relative).
+__device__ __forceinline__ bool pop_lowest(uint32_t& s0, uint32_t& s1, uint32_t& s2, uint32_t& s3, uint32_t& b) {
+  const uint32_t w = s0 ? s0 : (s1 ? s1 : (s2 ? s2 : s3));
+  if (!w) return false;
+  const uint32_t k = s0 ? 0u : (s1 ? 1u : (s2 ? 2u : 3u));
+  b = 32u * k + lsb32(w);
+  const uint32_t wc = w & (w - 1u);
+  s0 = k == 0 ? wc : s0;
+  s1 = k == 1 ? wc : s1;
+  s2 = k == 2 ? wc : s2;
+  s3 = k == 3 ? wc : s3;
+  return true;
 }
 
 // Parse the record starting at mask bit sb whose '\n' is at mask bit e (e > sb).
-// Returns 1 valid, 0 malformed.
-__device__ __forceinline__ int cm_parse(const uint8_t* buf, const unsigned long long* cmm, uint32_t sb, uint32_t e,
+// Returns 1 valid, 0 malformed.  Fast path (64 <= L = e - sb <= 191): the comma count of
+// [sb, e) from a 192-bit window at sb (must be 12: 13 fields); commas 0..5 are the 6 lowest
+// bits of its first 64 bits, commas 6..11 the 6 highest bits of the 64-bit window ending at
+// e.  Anything else takes the exact byte-serial path.
+__device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e,
                                         uint32_t hi_bits, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
-  if (L < 64 || L > 191) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
-  // four 64-bit comma words covering [sb, e)  (e < sb + 192 <= 64*(w0+4))
-  const uint32_t w0 = sb >> 6, o = sb & 63;
-  const unsigned long long a0 = cmm[w0], a1 = cmm[w0 + 1], a2 = cmm[w0 + 2], a3 = cmm[w0 + 3];
-  // comma count of [sb, e): bits at absolute positions p with sb <= p < e
-  const uint32_t eo = e - 64 * w0;                             // e relative to word w0, in (o, o+192)
-  auto below = [](uint32_t n) -> unsigned long long { return n >= 64 ? ~0ull : ((1ull << n) - 1); };
-  const unsigned long long m0 = (a0 & ~below(o)) & below(eo);
-  const unsigned long long m1 = eo > 64 ? (a1 & below(eo - 64)) : 0ull;
-  const unsigned long long m2 = eo > 128 ? (a2 & below(eo - 128)) : 0ull;
-  const unsigned long long m3 = eo > 192 ? (a3 & below(eo - 192)) : 0ull;
-  if (__popcll(m0) + __popcll(m1) + __popcll(m2) + __popcll(m3) != 12) return 0;   // not 13 fields
-  // commas 0..5 = lowest 6 bits of the 64-bit head window at sb; commas 6..11 = highest 6 bits
-  // of the 64-bit tail window ending at e
-  uint32_t hlo, hhi, tlo, thi;
-  bits64_at(o, a0, a1, a2, hlo, hhi);
-  const uint32_t trel = eo - 64;                               // tail window start, relative to w0
-  if (trel < 128) bits64_at(trel, a0, a1, a2, tlo, thi);
-  else bits64_at(trel - 64, a1, a2, a3, tlo, thi);
-  if (__popc(hlo) + __popc(hhi) < 6 || __popc(tlo) + __popc(thi) < 6)
-    return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  if (L - 64u > 127u) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  const uint32_t* w = cm32 + (sb >> 5);
+  const uint32_t sh = sb & 31u;
+  const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4], v5 = w[5], v6 = w[6];
+  uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
+  const uint32_t x2 = __funnelshift_r(v2, v3, sh) & low_bits(clamp32((int)L - 64));
+  const uint32_t x3 = __funnelshift_r(v3, v4, sh) & low_bits(clamp32((int)L - 96));
+  const uint32_t x4 = __funnelshift_r(v4, v5, sh) & low_bits(clamp32((int)L - 128));
+  const uint32_t x5 = __funnelshift_r(v5, v6, sh) & low_bits(clamp32((int)L - 160));
+  const uint32_t nh = __popc(h0) + __popc(h1);
+  if (nh + __popc(x2) + __popc(x3) + __popc(x4) + __popc(x5) != 12u) return 0;   // not 13 fields
+  // tail window [e - 64, e)
+  const uint32_t tp = e - 64u;
+  const uint32_t* u = cm32 + (tp >> 5);
+  const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
+  uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
+  if (nh < 6u || __popc(t0) + __popc(t1) < 6u) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
   uint32_t c[10];
 #pragma unroll
   for (int k = 0; k < 6; k++) {
-    const bool l = hlo != 0;
-    const uint32_t t = l ? hlo : hhi;
-    c[k] = S + (uint32_t)__ffs(t) - 1 + (l ? 0u : 32u);
-    if (l) hlo &= hlo - 1; else hhi &= hhi - 1;
+    const bool l = h0 != 0;
+    const uint32_t t = l ? h0 : h1;
+    const uint32_t bit = lsb32(t);
+    c[k] = S + bit + (l ? 0u : 32u);
+    const uint32_t tc = t & (t - 1u);
+    h0 = l ? tc : h0;
+    h1 = l ? h1 : tc;
   }
-  const uint32_t T0 = kCmHaloL + e - 64;                       // stage offset of tail bit 0
-  uint32_t c6 = 0;
+  const uint32_t T0 = kCmHaloL + tp;
 #pragma unroll
   for (int k = 11; k >= 6; k--) {
-    const bool h = thi != 0;
-    const uint32_t t = h ? thi : tlo;
-    const uint32_t b = 31u - (uint32_t)__clz(t);
-    if (h) thi ^= 1u << b; else tlo ^= 1u << b;
-    const uint32_t pos = T0 + b + (h ? 32u : 0u);
-    if (k < 10) c[k] = pos;
-    c6 = pos;
+    const bool h = t1 != 0;
+    const uint32_t t = h ? t1 : t0;
+    const uint32_t bit = msb32(t);
+    if (k < 10) c[k] = T0 + bit + (h ? 32u : 0u);
+    const uint32_t tc = t ^ (1u << bit);
+    t1 = h ? tc : t1;
+    t0 = h ? t0 : tc;
   }
-  if (c6 <= c[5]) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;   // windows overlap
   return cm_fields(buf, S, c, r) ? 1 : 0;
 }
 
@@ -278,7 +297,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kCmStages];
   __shared__ unsigned long long slot_tag[2];
-  __shared__ __align__(16) unsigned long long nlm[kMaskWords + 2], cmm[kMaskWords + 2];
+  __shared__ __align__(16) unsigned long long nlm[kMaskWords + 4], cmm[kMaskWords + 4];
   __shared__ uint16_t fnl[kCmThreads + 2];                     // first newline of each chunk
   // CM2: per-warp survivor lists; CM1: per-warp accumulators [warp][slot][cat]
   __shared__ unsigned long long sv_job[kCM2 ? kWarps : 1][kSurvCap];
@@ -296,7 +315,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       (&w_cnt[0][0][0])[i] = 0;
     }
   if (tid < 2) slot_tag[tid] = kEmpty64;
-  if (tid < 4) (tid < 2 ? nlm : cmm)[kMaskWords + (tid & 1)] = 0;   // window reads past the end
+  if (tid < 8) (tid < 4 ? nlm : cmm)[kMaskWords + (tid & 3)] = 0;   // window reads past the end
   if (tid < 2) fnl[kCmThreads + tid] = 0xFFFFu;                      // no chunk beyond the window
   if (tid == 0) {
     for (int s = 0; s < kCmStages; s++) mbar_init(&full[s], 1);
@@ -312,6 +331,9 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
   uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
   const uint32_t nl_s = smem_addr(nlm), cm_s = smem_addr(cmm);
+  uint32_t* const nl32 = reinterpret_cast<uint32_t*>(nlm);
+  uint32_t* const cm32 = reinterpret_cast<uint32_t*>(cmm);
+  uint32_t pc_lo = 0, pc_p = 0;                                 // cached pane [pc_lo, pc_lo + S)
 
   // CM2: process entries [0, n) of the warp's survivor list with the warp's lanes
   auto drain = [&](uint32_t n) {
@@ -346,11 +368,8 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const uint32_t hi_bits = g.hi - kCmHaloL;                  // mask bits beyond are invalid
     // ---- Pass 1: exact '\n' / ',' masks of every 16 B piece (round robin: conflict-free LDS.128)
     const uint32_t buf_s = smem_addr(buf) + kCmHaloL;
-    const bool partial = hi_bits < (uint32_t)kMaskBits;          // segment tail: mask stale bytes
 #pragma unroll
     for (int k = 0; k < kPieces / kCmThreads; k += 2) {
-      // two pieces p, p + 256 -> one 32-bit store per class (pieces p and p+256 are not
-      // adjacent, so store 16-bit halves through two u16 lanes of the same word pattern)
       const int p0 = tid + k * kCmThreads, p1 = p0 + kCmThreads;
       uint32_t nlv[2], cmv[2];
 #pragma unroll
@@ -358,18 +377,10 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
         const int p = u ? p1 : p0;
         const uint4 v = lds128(buf_s + 16 * p);
         const uint32_t m0 = v.x & 0x7F7F7F7Fu, m1 = v.y & 0x7F7F7F7Fu, m2 = v.z & 0x7F7F7F7Fu, m3 = v.w & 0x7F7F7F7Fu;
-        uint32_t nl = gather16(eq_flags(m0, v.x, 0x0A0A0A0Au), eq_flags(m1, v.y, 0x0A0A0A0Au),
-                               eq_flags(m2, v.z, 0x0A0A0A0Au), eq_flags(m3, v.w, 0x0A0A0A0Au));
-        uint32_t cm = gather16(eq_flags(m0, v.x, 0x2C2C2C2Cu), eq_flags(m1, v.y, 0x2C2C2C2Cu),
-                               eq_flags(m2, v.z, 0x2C2C2C2Cu), eq_flags(m3, v.w, 0x2C2C2C2Cu));
-        if (partial) {
-          const int valid = (int)hi_bits - 16 * p;
-          const uint32_t keep = valid <= 0 ? 0u : (valid >= 16 ? 0xFFFFu : ((1u << valid) - 1u));
-          nl &= keep;
-          cm &= keep;
-        }
-        nlv[u] = nl;
-        cmv[u] = cm;
+        nlv[u] = gather16(eq_flags(m0, v.x, 0x0A0A0A0Au), eq_flags(m1, v.y, 0x0A0A0A0Au),
+                          eq_flags(m2, v.z, 0x0A0A0A0Au), eq_flags(m3, v.w, 0x0A0A0A0Au));
+        cmv[u] = gather16(eq_flags(m0, v.x, 0x2C2C2C2Cu), eq_flags(m1, v.y, 0x2C2C2C2Cu),
+                          eq_flags(m2, v.z, 0x2C2C2C2Cu), eq_flags(m3, v.w, 0x2C2C2C2Cu));
       }
       // piece p's 16 bits live at byte offset 2p of the mask arrays
       asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)nlv[0]));
@@ -378,44 +389,64 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p1), "h"((uint16_t)cmv[1]));
     }
     __syncthreads();
-    // ---- Pass 2: record starts in my 128 B window chunk (byte after a '\n'), payload only;
-    // first newline of every chunk (record ends of the previous chunks' records)
-    const uint32_t cb = tid * kChunk;
-    unsigned long long st_lo = 0, st_hi = 0;
-    const uint4 n = lds128(nl_s + 16 * tid);
-    const unsigned long long n0 = ((unsigned long long)n.y << 32) | n.x;
-    const unsigned long long n1 = ((unsigned long long)n.w << 32) | n.z;
-    fnl[tid] = n0 ? (uint16_t)(cb + __ffsll(n0) - 1) : (n1 ? (uint16_t)(cb + 63 + __ffsll(n1)) : (uint16_t)0xFFFFu);
-    if (cb < g.payload) {
-      const bool carry = tid == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
-                                  : ((nlm[2 * tid - 1] >> 63) != 0);
-      st_lo = (n0 << 1) | (carry ? 1ull : 0ull);
-      st_hi = (n1 << 1) | (n0 >> 63);
-      const uint32_t nvalid = min((uint32_t)kChunk, g.payload - cb);
-      if (nvalid < 128) {
-        if (nvalid <= 64) { st_hi = 0; st_lo &= (nvalid == 64) ? ~0ull : ((1ull << nvalid) - 1); }
-        else st_hi &= (1ull << (nvalid - 64)) - 1;
+    if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (block-uniform): clear stale bits
+      for (uint32_t wi = tid; wi < (uint32_t)kMaskBits / 32; wi += kCmThreads) {
+        const uint32_t keep = low_bits(clamp32((int)hi_bits - 32 * (int)wi));
+        nl32[wi] &= keep;
+        cm32[wi] &= keep;
       }
+      __syncthreads();
+    }
+    // ---- Pass 2: thread t owns window chunk t (128 B, mask words 4t..4t+3).  Record starts
+    // (payload only) = the byte after a '\n'; first newline of the chunk -> fnl[t].
+    const uint32_t cb = tid * kChunk;
+    const uint4 nw = lds128(nl_s + 16 * tid);
+    const uint32_t pn = tid == 0 ? (((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n') ? 0x80000000u : 0u)
+                                 : nl32[4 * tid - 1];
+    uint32_t st0 = __funnelshift_l(pn, nw.x, 1), st1 = __funnelshift_l(nw.x, nw.y, 1),
+             st2 = __funnelshift_l(nw.y, nw.z, 1), st3 = __funnelshift_l(nw.z, nw.w, 1);
+    bool straddle = false;                      // the payload ends inside my chunk
+    if (cb + kChunk > g.payload) {
+      const int nv = (int)g.payload - (int)cb;
+      st0 &= low_bits(clamp32(nv));
+      st1 &= low_bits(clamp32(nv - 32));
+      st2 &= low_bits(clamp32(nv - 64));
+      st3 &= low_bits(clamp32(nv - 96));
+      straddle = nv > 0;
+    }
+    {
+      const uint32_t w = nw.x ? nw.x : (nw.y ? nw.y : (nw.z ? nw.z : nw.w));
+      const uint32_t k = nw.x ? 0u : (nw.y ? 32u : (nw.z ? 64u : 96u));
+      fnl[tid] = w ? (uint16_t)(cb + k + lsb32(w)) : (uint16_t)0xFFFFu;
     }
     __syncthreads();   // fnl[] complete
+    // '\n' ending a record of my chunk that has no later start in my chunk: my chunk's last
+    // byte, else the first newline of chunk t+1, else of chunk t+2 (else: > 256 B, serial)
+    const uint32_t e_after = (nw.w >> 31) ? cb + kChunk - 1
+                                          : (fnl[tid + 1] != 0xFFFFu ? (uint32_t)fnl[tid + 1] : (uint32_t)fnl[tid + 2]);
+    uint32_t b_cur = 0;
+    bool have = pop_lowest(st0, st1, st2, st3, b_cur);
     // ---- Pass 3: decode my records; aggregate (one record per thread per round)
     while (true) {
       CmRec r{0, 0, 0, 0, 0};
       bool surv = false;
-      const bool have = (st_lo | st_hi) != 0;
+      uint32_t b_nxt = 0;
+      const bool more = have && pop_lowest(st0, st1, st2, st3, b_nxt);
       if (have) {
-        uint32_t b;
-        if (st_lo) { b = __ffsll(st_lo) - 1; st_lo &= st_lo - 1; }
-        else { b = 64 + __ffsll(st_hi) - 1; st_hi &= st_hi - 1; }
         cnt.n++;
-        // terminating '\n': next newline in my chunk, else the first newline of chunk t+1 / t+2
-        const unsigned long long x0 = b >= 63 ? 0ull : (n0 & (~0ull << (b + 1)));
-        const unsigned long long x1 = b < 64 ? n1 : (b >= 127 ? 0ull : (n1 & (~0ull << (b - 63))));
-        const uint32_t f1 = fnl[tid + 1], f2 = fnl[tid + 2];      // branch-free selection
-        const uint32_t ef = f1 != 0xFFFFu ? f1 : f2;
-        const uint32_t e = x0 ? cb + __ffsll(x0) - 1 : (x1 ? cb + 63 + __ffsll(x1) : ef);
-        const int ok = e == 0xFFFFu ? (cm_parse_serial(buf, kCmHaloL + cb + b, g.hi, r) ? 1 : 0)
-                                    : cm_parse(buf, cmm, cb + b, e, hi_bits, r);
+        uint32_t e = more ? cb + b_nxt - 1u : e_after;          // the next start follows my '\n'
+        if (straddle) {                          // starts past the payload are masked: search
+          const uint32_t nv4[4] = {nw.x, nw.y, nw.z, nw.w};
+          e = e_after;
+#pragma unroll
+          for (int k = 3; k >= 0; k--) {
+            const int above = (int)b_cur - 32 * k;                // bits >= b_cur in word k
+            const uint32_t m = nv4[k] & ~low_bits(clamp32(above));
+            if (m) e = cb + 32u * k + lsb32(m);
+          }
+        }
+        const int ok = e == 0xFFFFu ? (cm_parse_serial(buf, kCmHaloL + cb + b_cur, g.hi, r) ? 1 : 0)
+                                    : cm_parse(buf, cm32, cb + b_cur, e, hi_bits, r);
         if (!ok) cnt.bad++;
         else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;
         else {
@@ -424,7 +455,13 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           surv = kCM2 ? (r.event == 1u) : true;                   // WHERE (eventType == 1)
         }
       }
-      const uint32_t p = surv ? pane_of(r.ts, q.S, q.div_magic) : 0;
+      have = more;
+      b_cur = b_nxt;
+      if (surv && r.ts - pc_lo >= q.S) {         // pane = floor(ts / S), cached per thread
+        pc_p = pane_of(r.ts, q.S, q.div_magic);
+        pc_lo = pc_p * q.S;
+      }
+      const uint32_t p = surv ? pc_p : 0;
       if (kCM2) {
         // warp-ballot stream compaction into the warp's survivor list
         const uint32_t bal = __ballot_sync(0xffffffffu, surv);
@@ -473,7 +510,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           __syncwarp();   // order the leader's smem accumulator update before the next leader's
         }
       }
-      if (!__any_sync(0xffffffffu, (st_lo | st_hi) != 0)) break;   // warp-local rounds
+      if (!__any_sync(0xffffffffu, have)) break;   // warp-local rounds
     }
     __syncthreads();   // stage s and the masks consumed
     if (tid == 0 && t + kCmStages < t1) cm_issue(a.segs, t + kCmStages, buf, &full[s]);
