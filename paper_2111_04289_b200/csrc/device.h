@@ -27,10 +27,10 @@ constexpr int kMaxWorld = 64;                          // multi-GPU ranks
 constexpr int kLrRecBytes = 70;
 constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records
 constexpr int kLrTileBytes = kLrTileRecs * kLrRecBytes; // 35840 = 16 * 2240
-constexpr int kCmWin = 16384;                          // CM tile window: payload + right halo
+constexpr int kCmWin = 4352;                           // CM warp-tile window: payload + right halo
 constexpr int kCmHaloL = 16;
 constexpr int kCmHaloR = 256;                          // >= max line (255) + '\n'
-constexpr int kCmTile = kCmWin - kCmHaloR;             // CM tile payload bytes (16128)
+constexpr int kCmTile = kCmWin - kCmHaloR;             // CM warp-tile payload bytes (4096)
 constexpr int kCmStage = kCmHaloL + kCmWin;
 constexpr int kCmMaxLine = 255;
 

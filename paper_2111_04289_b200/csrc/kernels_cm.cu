@@ -32,13 +32,16 @@ namespace lms {
 namespace {
 
 constexpr int kCmThreads = 128;
+constexpr int kWarps = kCmThreads / 32;
 constexpr int kCtasPerSm = 5;
-constexpr int kCmStages = 2;
-constexpr int kChunk = kCmWin / kCmThreads;                  // 128 B window chunk per thread
+constexpr int kCmStages = 2;                                 // per-warp smem ring
+constexpr int kChunk = 128;                                  // window chunk per lane
+constexpr int kChunks = kCmTile / kChunk;                    // 32 payload chunks per warp tile
+static_assert(kChunks == 32, "one payload chunk per lane");
 constexpr int kMaskBits = kCmWin;                            // mask bit i <-> stage byte 16 + i
-constexpr int kMaskWords = kMaskBits / 64;                   // 256
-constexpr int kPieces = kMaskBits / 16;                      // 2048 pieces of 16 B
-static_assert(kChunk == 128 && kPieces == 8 * kCmThreads, "one 128 B chunk / 8 pieces per thread");
+constexpr int kMaskW32 = kMaskBits / 32;                     // 136
+constexpr int kPieces = kMaskBits / 16;                      // 272 pieces of 16 B
+static_assert(kPieces % 64 == 16, "4 piece pairs + a half row per lane");
 constexpr int kSurvCap = 64;                                 // per-warp survivor list
 constexpr int kSmemPad = 16;                                 // SWAR loads may read 12 B past a stage
 
@@ -293,12 +296,12 @@ __device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32
 template <int KIND>
 __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs a) {
   constexpr bool kCM2 = (KIND == kCM2S);
-  constexpr int kWarps = kCmThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kCmStages];
+  __shared__ __align__(8) uint64_t full[kWarps][kCmStages];
   __shared__ unsigned long long slot_tag[2];
-  __shared__ __align__(16) unsigned long long nlm[kMaskWords + 4], cmm[kMaskWords + 4];
-  __shared__ uint16_t fnl[kCmThreads + 2];                     // first newline of each chunk
+  // per-warp '\n' / ',' masks of the warp's current window (+ zero words for reads past it)
+  __shared__ __align__(16) uint32_t nlm[kWarps][kMaskW32 + 8], cmm[kWarps][kMaskW32 + 8];
+  __shared__ uint16_t fnl_s[kWarps][kChunks + 4];              // first newline of each chunk
   // CM2: per-warp survivor lists; CM1: per-warp accumulators [warp][slot][cat]
   __shared__ unsigned long long sv_job[kCM2 ? kWarps : 1][kSurvCap];
   __shared__ uint32_t sv_m[kCM2 ? kWarps : 1][kSurvCap], sv_p[kCM2 ? kWarps : 1][kSurvCap];
@@ -306,8 +309,14 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
 
   const QueryDev& q = a.q;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned long long T = a.total_tiles, G = gridDim.x;
-  const unsigned long long t0 = T * blockIdx.x / G, t1 = T * (blockIdx.x + 1) / G;
+  // every warp walks its own contiguous range of warp tiles: no CTA barrier in the loop
+  const unsigned long long T = a.total_tiles, GW = (unsigned long long)gridDim.x * kWarps;
+  const unsigned long long gw = (unsigned long long)blockIdx.x * kWarps + warp;
+  const unsigned long long t0 = T * gw / GW, t1 = T * (gw + 1) / GW;
+  uint8_t* const wsmem = smem + warp * (kCmStages * kCmStage);
+  uint32_t* const nl32 = nlm[warp];
+  uint32_t* const cm32 = cmm[warp];
+  uint16_t* const fnl = fnl_s[warp];
 
   if (!kCM2)
     for (int i = tid; i < kWarps * 20; i += blockDim.x) {
@@ -315,24 +324,22 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       (&w_cnt[0][0][0])[i] = 0;
     }
   if (tid < 2) slot_tag[tid] = kEmpty64;
-  if (tid < 8) (tid < 4 ? nlm : cmm)[kMaskWords + (tid & 3)] = 0;   // window reads past the end
-  if (tid < 2) fnl[kCmThreads + tid] = 0xFFFFu;                      // no chunk beyond the window
-  if (tid == 0) {
-    for (int s = 0; s < kCmStages; s++) mbar_init(&full[s], 1);
+  if (lane < 8) { nl32[kMaskW32 + lane] = 0; cm32[kMaskW32 + lane] = 0; }   // reads past the end
+  if (lane < 2) fnl[kChunks + 2 + lane] = 0xFFFFu;                        // no chunk beyond
+  if (lane == 0) {
+    for (int s = 0; s < kCmStages; s++) mbar_init(&full[warp][s], 1);
     mbar_fence_init();
   }
   __syncthreads();
-  if (tid == 0)
+  if (lane == 0)
     for (int s = 0; s < kCmStages; s++)
-      if (t0 + s < t1) cm_issue(a.segs, t0 + s, smem + s * kCmStage, &full[s]);
+      if (t0 + s < t1) cm_issue(a.segs, t0 + s, wsmem + s * kCmStage, &full[warp][s]);
 
   const unsigned long long wm_prev = q.state->wm_prev;
   CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
   uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
-  const uint32_t nl_s = smem_addr(nlm), cm_s = smem_addr(cmm);
-  uint32_t* const nl32 = reinterpret_cast<uint32_t*>(nlm);
-  uint32_t* const cm32 = reinterpret_cast<uint32_t*>(cmm);
+  const uint32_t nl_s = smem_addr(nl32), cm_s = smem_addr(cm32);
   uint32_t pc_lo = 0, pc_p = 0;                                 // cached pane [pc_lo, pc_lo + S)
 
   // CM2: process entries [0, n) of the warp's survivor list with the warp's lanes
@@ -355,54 +362,61 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   for (unsigned long long t = t0; t < t1; t++) {
     const int s = (int)((t - t0) % kCmStages);
     const uint32_t ph = (uint32_t)(((t - t0) / kCmStages) & 1);
-    uint8_t* buf = smem + s * kCmStage;
+    uint8_t* buf = wsmem + s * kCmStage;
     const TileGeom g = cm_geom(a.segs, t);
-    mbar_wait(&full[s], ph);
+    mbar_wait(&full[warp][s], ph);
     {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
       const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
       if (bulk_end < g.hi) {
-        if ((uint32_t)tid < g.hi - bulk_end) buf[bulk_end + tid] = g.seg[g.off - kCmHaloL + bulk_end + tid];
-        __syncthreads();
+        if ((uint32_t)lane < g.hi - bulk_end) buf[bulk_end + lane] = g.seg[g.off - kCmHaloL + bulk_end + lane];
+        __syncwarp();
       }
     }
     const uint32_t hi_bits = g.hi - kCmHaloL;                  // mask bits beyond are invalid
     // ---- Pass 1: exact '\n' / ',' masks of every 16 B piece (round robin: conflict-free LDS.128)
     const uint32_t buf_s = smem_addr(buf) + kCmHaloL;
+    auto piece = [&](int p, uint32_t& nl, uint32_t& cm) {
+      const uint4 v = lds128(buf_s + 16 * p);
+      const uint32_t m0 = v.x & 0x7F7F7F7Fu, m1 = v.y & 0x7F7F7F7Fu, m2 = v.z & 0x7F7F7F7Fu, m3 = v.w & 0x7F7F7F7Fu;
+      nl = gather16(eq_flags(m0, v.x, 0x0A0A0A0Au), eq_flags(m1, v.y, 0x0A0A0A0Au),
+                    eq_flags(m2, v.z, 0x0A0A0A0Au), eq_flags(m3, v.w, 0x0A0A0A0Au));
+      cm = gather16(eq_flags(m0, v.x, 0x2C2C2C2Cu), eq_flags(m1, v.y, 0x2C2C2C2Cu),
+                    eq_flags(m2, v.z, 0x2C2C2C2Cu), eq_flags(m3, v.w, 0x2C2C2C2Cu));
+    };
+    // piece p's 16 bits live at byte offset 2p of the mask arrays
 #pragma unroll
-    for (int k = 0; k < kPieces / kCmThreads; k += 2) {
-      const int p0 = tid + k * kCmThreads, p1 = p0 + kCmThreads;
-      uint32_t nlv[2], cmv[2];
-#pragma unroll
-      for (int u = 0; u < 2; u++) {
-        const int p = u ? p1 : p0;
-        const uint4 v = lds128(buf_s + 16 * p);
-        const uint32_t m0 = v.x & 0x7F7F7F7Fu, m1 = v.y & 0x7F7F7F7Fu, m2 = v.z & 0x7F7F7F7Fu, m3 = v.w & 0x7F7F7F7Fu;
-        nlv[u] = gather16(eq_flags(m0, v.x, 0x0A0A0A0Au), eq_flags(m1, v.y, 0x0A0A0A0Au),
-                          eq_flags(m2, v.z, 0x0A0A0A0Au), eq_flags(m3, v.w, 0x0A0A0A0Au));
-        cmv[u] = gather16(eq_flags(m0, v.x, 0x2C2C2C2Cu), eq_flags(m1, v.y, 0x2C2C2C2Cu),
-                          eq_flags(m2, v.z, 0x2C2C2C2Cu), eq_flags(m3, v.w, 0x2C2C2C2Cu));
-      }
-      // piece p's 16 bits live at byte offset 2p of the mask arrays
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)nlv[0]));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p1), "h"((uint16_t)nlv[1]));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p0), "h"((uint16_t)cmv[0]));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p1), "h"((uint16_t)cmv[1]));
+    for (int k = 0; k < kPieces - 32; k += 64) {
+      const int p0 = lane + k, p1 = p0 + 32;
+      uint32_t n0, c0, n1, c1;
+      piece(p0, n0, c0);
+      piece(p1, n1, c1);
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)n0));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p1), "h"((uint16_t)n1));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p0), "h"((uint16_t)c0));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p1), "h"((uint16_t)c1));
     }
-    __syncthreads();
-    if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (block-uniform): clear stale bits
-      for (uint32_t wi = tid; wi < (uint32_t)kMaskBits / 32; wi += kCmThreads) {
+    if (lane < kPieces % 64) {                  // the last 16 pieces (halo end)
+      const int p0 = lane + (kPieces / 64) * 64;
+      uint32_t n0, c0;
+      piece(p0, n0, c0);
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)n0));
+      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p0), "h"((uint16_t)c0));
+    }
+    __syncwarp();
+    if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (warp-uniform): clear stale bits
+      for (uint32_t wi = lane; wi < (uint32_t)kMaskW32; wi += 32) {
         const uint32_t keep = low_bits(clamp32((int)hi_bits - 32 * (int)wi));
         nl32[wi] &= keep;
         cm32[wi] &= keep;
       }
-      __syncthreads();
+      __syncwarp();
     }
-    // ---- Pass 2: thread t owns window chunk t (128 B, mask words 4t..4t+3).  Record starts
-    // (payload only) = the byte after a '\n'; first newline of the chunk -> fnl[t].
-    const uint32_t cb = tid * kChunk;
-    const uint4 nw = lds128(nl_s + 16 * tid);
-    const uint32_t pn = tid == 0 ? (((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n') ? 0x80000000u : 0u)
-                                 : nl32[4 * tid - 1];
+    // ---- Pass 2: lane l owns payload chunk l (128 B, mask words 4l..4l+3).  Record starts
+    // (payload only) = the byte after a '\n'; first newline of each chunk (+ 2 halo chunks).
+    const uint32_t cb = lane * kChunk;
+    const uint4 nw = lds128(nl_s + 16 * lane);
+    const uint32_t pn = lane == 0 ? (((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n') ? 0x80000000u : 0u)
+                                  : nl32[4 * lane - 1];
     uint32_t st0 = __funnelshift_l(pn, nw.x, 1), st1 = __funnelshift_l(nw.x, nw.y, 1),
              st2 = __funnelshift_l(nw.y, nw.z, 1), st3 = __funnelshift_l(nw.z, nw.w, 1);
     bool straddle = false;                      // the payload ends inside my chunk
@@ -417,16 +431,23 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     {
       const uint32_t w = nw.x ? nw.x : (nw.y ? nw.y : (nw.z ? nw.z : nw.w));
       const uint32_t k = nw.x ? 0u : (nw.y ? 32u : (nw.z ? 64u : 96u));
-      fnl[tid] = w ? (uint16_t)(cb + k + lsb32(w)) : (uint16_t)0xFFFFu;
+      fnl[lane] = w ? (uint16_t)(cb + k + lsb32(w)) : (uint16_t)0xFFFFu;
+      if (lane < 2) {                           // halo chunks kChunks, kChunks + 1
+        const uint32_t hb = (kChunks + lane) * kChunk;
+        const uint4 hw = lds128(nl_s + hb / 8);
+        const uint32_t w2 = hw.x ? hw.x : (hw.y ? hw.y : (hw.z ? hw.z : hw.w));
+        const uint32_t k2 = hw.x ? 0u : (hw.y ? 32u : (hw.z ? 64u : 96u));
+        fnl[kChunks + lane] = w2 ? (uint16_t)(hb + k2 + lsb32(w2)) : (uint16_t)0xFFFFu;
+      }
     }
-    __syncthreads();   // fnl[] complete
+    __syncwarp();      // fnl[] complete
     // '\n' ending a record of my chunk that has no later start in my chunk: my chunk's last
-    // byte, else the first newline of chunk t+1, else of chunk t+2 (else: > 256 B, serial)
+    // byte, else the first newline of chunk l+1, else of chunk l+2 (else: > 256 B, serial)
     const uint32_t e_after = (nw.w >> 31) ? cb + kChunk - 1
-                                          : (fnl[tid + 1] != 0xFFFFu ? (uint32_t)fnl[tid + 1] : (uint32_t)fnl[tid + 2]);
+                                          : (fnl[lane + 1] != 0xFFFFu ? (uint32_t)fnl[lane + 1] : (uint32_t)fnl[lane + 2]);
     uint32_t b_cur = 0;
     bool have = pop_lowest(st0, st1, st2, st3, b_cur);
-    // ---- Pass 3: decode my records; aggregate (one record per thread per round)
+    // ---- Pass 3: decode my records; aggregate (one record per lane per round)
     while (true) {
       CmRec r{0, 0, 0, 0, 0};
       bool surv = false;
@@ -512,8 +533,8 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
       if (!__any_sync(0xffffffffu, have)) break;   // warp-local rounds
     }
-    __syncthreads();   // stage s and the masks consumed
-    if (tid == 0 && t + kCmStages < t1) cm_issue(a.segs, t + kCmStages, buf, &full[s]);
+    __syncwarp();      // stage s and the masks consumed by every lane
+    if (lane == 0 && t + kCmStages < t1) cm_issue(a.segs, t + kCmStages, buf, &full[warp][s]);
   }
 
   if (kCM2) {
@@ -556,7 +577,7 @@ cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   a.segs = segs;
   a.total_tiles = segs.tile_prefix[segs.n];
   if (a.total_tiles == 0) return cudaSuccess;
-  const size_t smem = (size_t)kCmStages * kCmStage + kSmemPad;
+  const size_t smem = (size_t)kWarps * kCmStages * kCmStage + kSmemPad;
   const int grid = (int)q.n_agg_ctas;
   cudaError_t e;
   if (q.kind == kCM2S) {
