@@ -74,13 +74,6 @@ struct CmArgs {
   unsigned long long total_tiles;
 };
 
-__device__ __forceinline__ void seg_of_tile(const SegTable& s, unsigned long long tile, int& si,
-                                            unsigned long long& local) {
-  si = 0;
-  while (si + 1 < s.n && tile >= s.tile_prefix[si + 1]) si++;
-  local = tile - s.tile_prefix[si];
-}
-
 struct TileGeom {
   const uint8_t* seg;
   unsigned long long off;            // tile starts at seg + off
@@ -88,24 +81,26 @@ struct TileGeom {
   uint32_t payload;                  // tile payload bytes (<= kCmTile)
 };
 
-__device__ __forceinline__ TileGeom cm_geom(const SegTable& segs, unsigned long long tile) {
+// Segment of a monotonically advancing tile index (a warp walks its tiles in order).
+struct SegCursor {
   int si;
-  unsigned long long lt;
-  seg_of_tile(segs, tile, si, lt);
-  TileGeom g;
-  g.seg = segs.s[si].ptr;
-  g.off = lt * (unsigned long long)kCmTile;
-  const unsigned long long rem = segs.s[si].nbytes - g.off;
-  g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
-  g.lo = lt == 0 ? kCmHaloL : 0;
-  const unsigned long long end = rem < (unsigned long long)kCmWin ? rem : kCmWin;
-  g.hi = kCmHaloL + (uint32_t)end;
-  return g;
-}
+  unsigned long long base, end;      // tiles [base, end) belong to segment si
+  __device__ __forceinline__ void init(const SegTable& s) { si = 0; base = 0; end = s.tile_prefix[1]; }
+  __device__ __forceinline__ TileGeom geom(const SegTable& s, unsigned long long tile) {
+    while (tile >= end && si + 1 < s.n) { si++; base = end; end = s.tile_prefix[si + 1]; }
+    TileGeom g;
+    const unsigned long long lt = tile - base;
+    g.seg = s.s[si].ptr;
+    g.off = lt * (unsigned long long)kCmTile;
+    const unsigned long long rem = s.s[si].nbytes - g.off;
+    g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
+    g.lo = lt == 0 ? kCmHaloL : 0;
+    g.hi = kCmHaloL + (uint32_t)(rem < (unsigned long long)kCmWin ? rem : kCmWin);
+    return g;
+  }
+};
 
-__device__ __forceinline__ void cm_issue(const SegTable& segs, unsigned long long tile, uint8_t* dst,
-                                         uint64_t* bar) {
-  const TileGeom g = cm_geom(segs, tile);
+__device__ __forceinline__ void cm_issue(const TileGeom& g, uint8_t* dst, uint64_t* bar) {
   const uint32_t bulk = (g.hi - g.lo) & ~15u;
   mbar_arrive_expect_tx(bar, bulk);
   if (bulk) bulk_g2s(dst + g.lo, g.seg + g.off - kCmHaloL + g.lo, bulk, bar);
@@ -331,9 +326,14 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     mbar_fence_init();
   }
   __syncthreads();
-  if (lane == 0)
-    for (int s = 0; s < kCmStages; s++)
-      if (t0 + s < t1) cm_issue(a.segs, t0 + s, wsmem + s * kCmStage, &full[warp][s]);
+  SegCursor cur, iss;                          // consumer / producer (2 tiles ahead) cursors
+  cur.init(a.segs);
+  iss.init(a.segs);
+  for (int s = 0; s < kCmStages; s++)
+    if (t0 + s < t1) {
+      const TileGeom gi = iss.geom(a.segs, t0 + s);
+      if (lane == 0) cm_issue(gi, wsmem + s * kCmStage, &full[warp][s]);
+    }
 
   const unsigned long long wm_prev = q.state->wm_prev;
   CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const int s = (int)((t - t0) % kCmStages);
     const uint32_t ph = (uint32_t)(((t - t0) / kCmStages) & 1);
     uint8_t* buf = wsmem + s * kCmStage;
-    const TileGeom g = cm_geom(a.segs, t);
+    const TileGeom g = cur.geom(a.segs, t);
     mbar_wait(&full[warp][s], ph);
     {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
       const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
@@ -411,23 +411,13 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
       __syncwarp();
     }
-    // ---- Pass 2: lane l owns payload chunk l (128 B, mask words 4l..4l+3).  Record starts
-    // (payload only) = the byte after a '\n'; first newline of each chunk (+ 2 halo chunks).
+    // ---- Pass 2: lane l owns payload chunk l (128 B, mask words 4l..4l+3); fnl[] = first
+    // newline of each chunk (+ the 2 halo chunks).  A record starts after a '\n' (or at a
+    // segment start) and belongs to the chunk holding its first byte.
     const uint32_t cb = lane * kChunk;
     const uint4 nw = lds128(nl_s + 16 * lane);
-    const uint32_t pn = lane == 0 ? (((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n') ? 0x80000000u : 0u)
-                                  : nl32[4 * lane - 1];
-    uint32_t st0 = __funnelshift_l(pn, nw.x, 1), st1 = __funnelshift_l(nw.x, nw.y, 1),
-             st2 = __funnelshift_l(nw.y, nw.z, 1), st3 = __funnelshift_l(nw.z, nw.w, 1);
-    bool straddle = false;                      // the payload ends inside my chunk
-    if (cb + kChunk > g.payload) {
-      const int nv = (int)g.payload - (int)cb;
-      st0 &= low_bits(clamp32(nv));
-      st1 &= low_bits(clamp32(nv - 32));
-      st2 &= low_bits(clamp32(nv - 64));
-      st3 &= low_bits(clamp32(nv - 96));
-      straddle = nv > 0;
-    }
+    const bool prev_nl = lane == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
+                                   : (nl32[4 * lane - 1] >> 31) != 0;
     {
       const uint32_t w = nw.x ? nw.x : (nw.y ? nw.y : (nw.z ? nw.z : nw.w));
       const uint32_t k = nw.x ? 0u : (nw.y ? 32u : (nw.z ? 64u : 96u));
@@ -441,31 +431,32 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
     }
     __syncwarp();      // fnl[] complete
-    // '\n' ending a record of my chunk that has no later start in my chunk: my chunk's last
-    // byte, else the first newline of chunk l+1, else of chunk l+2 (else: > 256 B, serial)
-    const uint32_t e_after = (nw.w >> 31) ? cb + kChunk - 1
-                                          : (fnl[lane + 1] != 0xFFFFu ? (uint32_t)fnl[lane + 1] : (uint32_t)fnl[lane + 2]);
-    uint32_t b_cur = 0;
-    bool have = pop_lowest(st0, st1, st2, st3, b_cur);
+    // '\n' of the last record starting in my chunk: first newline of chunk l+1, else l+2
+    // (else the line is > 256 B: serial path)
+    const uint32_t e_after = fnl[lane + 1] != 0xFFFFu ? (uint32_t)fnl[lane + 1] : (uint32_t)fnl[lane + 2];
+    const uint32_t limit = min(cb + (uint32_t)kChunk, g.payload);   // starts must lie below
+    uint32_t n0 = nw.x, n1 = nw.y, n2 = nw.z, n3 = nw.w;             // my unconsumed newlines
+    uint32_t prev = cb - 1u;                    // '\n' before the next record (cb - 1: wraps at 0)
+    bool have = prev_nl;
+    if (!have) {
+      uint32_t b0;
+      have = pop_lowest(n0, n1, n2, n3, b0);
+      prev = cb + b0;
+    }
+    have = have && prev + 1u < limit;
     // ---- Pass 3: decode my records; aggregate (one record per lane per round)
     while (true) {
       CmRec r{0, 0, 0, 0, 0};
       bool surv = false;
-      uint32_t b_nxt = 0;
-      const bool more = have && pop_lowest(st0, st1, st2, st3, b_nxt);
+      const uint32_t b_cur = prev + 1u - cb;
+      bool next = false;
       if (have) {
         cnt.n++;
-        uint32_t e = more ? cb + b_nxt - 1u : e_after;          // the next start follows my '\n'
-        if (straddle) {                          // starts past the payload are masked: search
-          const uint32_t nv4[4] = {nw.x, nw.y, nw.z, nw.w};
-          e = e_after;
-#pragma unroll
-          for (int k = 3; k >= 0; k--) {
-            const int above = (int)b_cur - 32 * k;                // bits >= b_cur in word k
-            const uint32_t m = nv4[k] & ~low_bits(clamp32(above));
-            if (m) e = cb + 32u * k + lsb32(m);
-          }
-        }
+        uint32_t bn;
+        const bool inchunk = pop_lowest(n0, n1, n2, n3, bn);
+        const uint32_t e = inchunk ? cb + bn : e_after;           // my record's '\n'
+        prev = e;
+        next = inchunk && e + 1u < limit;
         const int ok = e == 0xFFFFu ? (cm_parse_serial(buf, kCmHaloL + cb + b_cur, g.hi, r) ? 1 : 0)
                                     : cm_parse(buf, cm32, cb + b_cur, e, hi_bits, r);
         if (!ok) cnt.bad++;
@@ -476,8 +467,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           surv = kCM2 ? (r.event == 1u) : true;                   // WHERE (eventType == 1)
         }
       }
-      have = more;
-      b_cur = b_nxt;
+      have = next;
       if (surv && r.ts - pc_lo >= q.S) {         // pane = floor(ts / S), cached per thread
         pc_p = pane_of(r.ts, q.S, q.div_magic);
         pc_lo = pc_p * q.S;
@@ -534,7 +524,10 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       if (!__any_sync(0xffffffffu, have)) break;   // warp-local rounds
     }
     __syncwarp();      // stage s and the masks consumed by every lane
-    if (lane == 0 && t + kCmStages < t1) cm_issue(a.segs, t + kCmStages, buf, &full[warp][s]);
+    if (t + kCmStages < t1) {
+      const TileGeom gi = iss.geom(a.segs, t + kCmStages);
+      if (lane == 0) cm_issue(gi, buf, &full[warp][s]);
+    }
   }
 
   if (kCM2) {
