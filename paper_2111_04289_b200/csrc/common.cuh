@@ -39,6 +39,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Segment of a monotonically advancing tile index (a CTA / warp walks its tiles in order):
+// tiles [base, end) belong to segment si.  O(1) per tile instead of a search.
+struct SegCursor {
+  int si;
+  unsigned long long base, end;
+  __device__ __forceinline__ void init(const SegTable& s) { si = 0; base = 0; end = s.tile_prefix[1]; }
+  __device__ __forceinline__ void seek(const SegTable& s, unsigned long long tile) {
+    while (tile >= end && si + 1 < s.n) { si++; base = end; end = s.tile_prefix[si + 1]; }
+  }
+};
+
 // ---- arithmetic ----------------------------------------------------------------------
 // pane = ts / S exactly for ts < 2^32, S <= 2^31 (magic = ceil(2^64 / S), S > 1).
 __device__ __forceinline__ uint32_t pane_of(uint32_t ts, uint32_t S, unsigned long long magic) {

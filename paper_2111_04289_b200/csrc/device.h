@@ -22,7 +22,7 @@ namespace lms {
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 constexpr uint32_t kFail32 = 0xFFFFFFFEu;   // pane table full: the pane's records overflow
 constexpr unsigned long long kEmpty64 = ~0ull;
-constexpr int kMaxSegs = 16;
+constexpr int kMaxSegs = 128;                          // input segments per aggregate launch
 constexpr int kMaxWorld = 64;                          // multi-GPU ranks
 constexpr int kLrRecBytes = 70;
 constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records

@@ -81,24 +81,18 @@ struct TileGeom {
   uint32_t payload;                  // tile payload bytes (<= kCmTile)
 };
 
-// Segment of a monotonically advancing tile index (a warp walks its tiles in order).
-struct SegCursor {
-  int si;
-  unsigned long long base, end;      // tiles [base, end) belong to segment si
-  __device__ __forceinline__ void init(const SegTable& s) { si = 0; base = 0; end = s.tile_prefix[1]; }
-  __device__ __forceinline__ TileGeom geom(const SegTable& s, unsigned long long tile) {
-    while (tile >= end && si + 1 < s.n) { si++; base = end; end = s.tile_prefix[si + 1]; }
-    TileGeom g;
-    const unsigned long long lt = tile - base;
-    g.seg = s.s[si].ptr;
-    g.off = lt * (unsigned long long)kCmTile;
-    const unsigned long long rem = s.s[si].nbytes - g.off;
-    g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
-    g.lo = lt == 0 ? kCmHaloL : 0;
-    g.hi = kCmHaloL + (uint32_t)(rem < (unsigned long long)kCmWin ? rem : kCmWin);
-    return g;
-  }
-};
+__device__ __forceinline__ TileGeom cm_geom(const SegTable& s, SegCursor& c, unsigned long long tile) {
+  c.seek(s, tile);
+  TileGeom g;
+  const unsigned long long lt = tile - c.base;
+  g.seg = s.s[c.si].ptr;
+  g.off = lt * (unsigned long long)kCmTile;
+  const unsigned long long rem = s.s[c.si].nbytes - g.off;
+  g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
+  g.lo = lt == 0 ? kCmHaloL : 0;
+  g.hi = kCmHaloL + (uint32_t)(rem < (unsigned long long)kCmWin ? rem : kCmWin);
+  return g;
+}
 
 __device__ __forceinline__ void cm_issue(const TileGeom& g, uint8_t* dst, uint64_t* bar) {
   const uint32_t bulk = (g.hi - g.lo) & ~15u;
@@ -331,7 +325,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   iss.init(a.segs);
   for (int s = 0; s < kCmStages; s++)
     if (t0 + s < t1) {
-      const TileGeom gi = iss.geom(a.segs, t0 + s);
+      const TileGeom gi = cm_geom(a.segs, iss, t0 + s);
       if (lane == 0) cm_issue(gi, wsmem + s * kCmStage, &full[warp][s]);
     }
 
@@ -363,7 +357,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const int s = (int)((t - t0) % kCmStages);
     const uint32_t ph = (uint32_t)(((t - t0) / kCmStages) & 1);
     uint8_t* buf = wsmem + s * kCmStage;
-    const TileGeom g = cur.geom(a.segs, t);
+    const TileGeom g = cm_geom(a.segs, cur, t);
     mbar_wait(&full[warp][s], ph);
     {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
       const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
@@ -525,7 +519,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     }
     __syncwarp();      // stage s and the masks consumed by every lane
     if (t + kCmStages < t1) {
-      const TileGeom gi = iss.geom(a.segs, t + kCmStages);
+      const TileGeom gi = cm_geom(a.segs, iss, t + kCmStages);
       if (lane == 0) cm_issue(gi, buf, &full[warp][s]);
     }
   }

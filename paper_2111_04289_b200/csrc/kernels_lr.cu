@@ -106,26 +106,17 @@ struct LrArgs {
   unsigned long long total_tiles;
 };
 
-__device__ __forceinline__ void seg_of_tile(const SegTable& s, unsigned long long tile, int& si,
-                                            unsigned long long& local) {
-  si = 0;
-  while (si + 1 < s.n && tile >= s.tile_prefix[si + 1]) si++;
-  local = tile - s.tile_prefix[si];
-}
-
-// Issue the bulk copy for global tile `tile` into stage buffer `dst`; returns bytes copied by
-// the TMA engine (the <16 B remainder of a segment's last tile is copied by threads later).
-__device__ __forceinline__ void lr_issue(const SegTable& segs, unsigned long long tile, uint8_t* dst,
-                                        uint64_t* bar) {
-  int si;
-  unsigned long long lt;
-  seg_of_tile(segs, tile, si, lt);
-  const unsigned long long off = lt * (unsigned long long)kLrTileBytes;
-  const unsigned long long rem = segs.s[si].nbytes - off;
+// Issue the bulk copy for global tile `tile` into stage buffer `dst` (the <16 B remainder of
+// a segment's last tile is copied by threads later).
+__device__ __forceinline__ void lr_issue(const SegTable& segs, SegCursor& c, unsigned long long tile,
+                                        uint8_t* dst, uint64_t* bar) {
+  c.seek(segs, tile);
+  const unsigned long long off = (tile - c.base) * (unsigned long long)kLrTileBytes;
+  const unsigned long long rem = segs.s[c.si].nbytes - off;
   const uint32_t bytes = (uint32_t)(rem < (unsigned long long)kLrTileBytes ? rem : kLrTileBytes);
   const uint32_t bulk = bytes & ~15u;
   mbar_arrive_expect_tx(bar, bulk);
-  if (bulk) bulk_g2s(dst, segs.s[si].ptr + off, bulk, bar);
+  if (bulk) bulk_g2s(dst, segs.s[c.si].ptr + off, bulk, bar);
 }
 
 template <int KIND>
@@ -154,9 +145,12 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
     mbar_fence_init();
   }
   __syncthreads();
+  SegCursor cur, iss;                          // consumer / producer cursors
+  cur.init(a.segs);
+  iss.init(a.segs);
   if (tid == 0) {
     for (int s = 0; s < kLrStages; s++)
-      if (t0 + s < t1) lr_issue(a.segs, t0 + s, stage + s * kLrTileBytes, &full[s]);
+      if (t0 + s < t1) lr_issue(a.segs, iss, t0 + s, stage + s * kLrTileBytes, &full[s]);
   }
 
   const unsigned long long wm_prev = q.state->wm_prev;
@@ -166,10 +160,9 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   for (unsigned long long t = t0; t < t1; t++) {
     const int s = (int)((t - t0) % kLrStages);
     const uint32_t ph = (uint32_t)(((t - t0) / kLrStages) & 1);
-    int si;
-    unsigned long long lt;
-    seg_of_tile(a.segs, t, si, lt);
-    const unsigned long long off = lt * (unsigned long long)kLrTileBytes;
+    cur.seek(a.segs, t);
+    const int si = cur.si;
+    const unsigned long long off = (t - cur.base) * (unsigned long long)kLrTileBytes;
     const unsigned long long rem = a.segs.s[si].nbytes - off;
     const uint32_t bytes = (uint32_t)(rem < (unsigned long long)kLrTileBytes ? rem : kLrTileBytes);
     const uint32_t nrec = bytes / kLrRecBytes;
@@ -244,7 +237,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
       }
     }
     __syncthreads();   // stage s fully consumed
-    if (tid == 0 && t + kLrStages < t1) lr_issue(a.segs, t + kLrStages, buf, &full[s]);
+    if (tid == 0 && t + kLrStages < t1) lr_issue(a.segs, iss, t + kLrStages, buf, &full[s]);
   }
 
   if (!kLR1) {

@@ -118,11 +118,14 @@ def test_device_and_host_segments_mixed():
     compare_run("LR2S", product_run("LR2S", batches, device_batches=devmask), oracle_rows("LR2S", batches))
 
 
-def test_many_segments_more_than_16():
-    data = stream("LR", "B(0.2)", 40)
-    batches = [data[:37], data[37:]]
-    devmask = [[True] * len(b) for b in batches]
-    compare_run("LR2S", product_run("LR2S", batches, device_batches=devmask), oracle_rows("LR2S", batches))
+def test_many_segments_more_than_one_launch():
+    """> 128 borrowed device segments in one batch: several aggregate launches per batch, and
+    segment cursors crossing many tiny segments inside one launch."""
+    for fam, qname in (("LR", "LR2S"), ("CM", "CM2S")):
+        data = stream(fam, "B(0.02)", 300)
+        batches = [data[:170], data[170:190], data[190:]]
+        devmask = [[True] * len(b) for b in batches]
+        compare_run(qname, product_run(qname, batches, device_batches=devmask), oracle_rows(qname, batches))
 
 
 def test_empty_flush_and_tiny_batches():

@@ -1,0 +1,240 @@
+#!/usr/bin/env python
+"""Stream-latency configurations C1, C2, C3, C5 of BASELINE.json on one B200.
+
+Every micro-batch runs through the C ABI on the GPU (`lms_poll` decides admission with
+Alg. 1 / CG(dN) / OS(tN)).  Arrivals follow a
+VIRTUAL clock (10 ms polls): a dataset becomes visible at its ingest time; an admitted
+batch runs for real and its measured Proc (device + result D2H) advances that query's clock.
+Datasets are generated on the GPU by lmsgen (byte-identical to the oracle's generator) one
+virtual second at a time, split at record boundaries into `parts` sub-datasets ingested at
+t + (j + 1) / parts (reading R4), and pushed as borrowed device segments.
+
+  python tools/latency_configs.py [--configs C1,C2,C3,C5] [--out profiles/r01b/latency_configs.json]
+
+Reported per config: batches, records, MaxLat (Eq. 5) p50/p99/max, Proc p50/p99, device time
+p50/p99, deadline-violation fraction (MaxLat > target), mean dataset latency (reading R17),
+and processing throughput = records / sum of device time.
+"""
+from __future__ import annotations
+
+import argparse
+import collections
+import json
+import math
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+POLL = 0.01
+
+
+def pct(v, p):
+    v = sorted(v)
+    if not v:
+        return None
+    return v[max(1, math.ceil(p * len(v) / 100)) - 1]
+
+
+class Source:
+    """One stream: lazily generated seconds, split into sub-datasets, pushed to a query."""
+
+    def __init__(self, q, family, traffic, seconds, parts, seed):
+        import lmsgen as g
+        self.q, self.family, self.parts, self.seed = q, family, parts, seed
+        self.tr = g.Traffic.parse(traffic)
+        self.seconds = seconds
+        self.next_sec = 0
+        self.queue = collections.deque()       # (ingest, ptr, nbytes, owner tensor)
+        self.live = collections.deque()        # (ingest, owner tensor) of pushed, unconsumed datasets
+        self.busy_until = 0.0
+        self.pending_records = 0
+        self.force_at = None                   # MANUAL sweep: force a batch at this many records
+        self.recs = []
+        self.lat = []                          # per-dataset completion - ingest
+
+    def _gen(self, t):
+        import torch
+        from lmsgen import cuda as gcu
+        n = self.tr.count(t, self.seed)
+        buf, nb = gcu.second_tensor(self.family, t, n, seed=self.seed)
+        if self.family == "LR":
+            cuts = [70 * (n * j // self.parts) for j in range(self.parts + 1)]
+            nrec = [n * (j + 1) // self.parts - n * j // self.parts for j in range(self.parts)]
+        else:
+            nl = (buf[:nb] == 10).nonzero().squeeze(1)
+            idx = [(len(nl) * j // self.parts) - 1 for j in range(1, self.parts + 1)]
+            cuts = [0] + [int(nl[i].item()) + 1 if i >= 0 else 0 for i in idx]
+            cuts[-1] = nb
+            ends = [i + 1 for i in idx]
+            nrec = [ends[0]] + [ends[j] - ends[j - 1] for j in range(1, self.parts)]
+        # lms_push_device borrows 16 B aligned segments: repack the sub-datasets
+        sizes = [cuts[j + 1] - cuts[j] for j in range(self.parts)]
+        offs, o = [], 0
+        for n_j in sizes:
+            offs.append(o)
+            o += (n_j + 15) & ~15
+        dst = torch.empty(o + 64, dtype=torch.uint8, device="cuda")
+        for j in range(self.parts):
+            if sizes[j]:
+                dst[offs[j]:offs[j] + sizes[j]].copy_(buf[cuts[j]:cuts[j + 1]])
+        torch.cuda.synchronize()
+        del buf
+        for j in range(self.parts):
+            if sizes[j]:
+                self.queue.append((t + (j + 1) / self.parts, dst.data_ptr() + offs[j], sizes[j], dst, nrec[j]))
+
+    def push_until(self, now):
+        while True:
+            if not self.queue:
+                if self.next_sec >= self.seconds:
+                    return
+                self._gen(self.next_sec)
+                self.next_sec += 1
+                continue
+            ing, ptr, nb, own, nr = self.queue[0]
+            if ing > now + 1e-12:
+                return
+            self.queue.popleft()
+            self.q.push_device(ptr, nb, ing)
+            self.live.append((ing, own))
+            self.pending_records += nr
+
+    def completed(self, rec):
+        self.recs.append(rec)
+        end = rec["admit_time_s"] + rec["proc_s"]
+        for _ in range(rec["num_datasets"]):
+            ing, _own = self.live.popleft()
+            self.lat.append(end - ing)
+        self.busy_until = end
+        self.pending_records -= rec["num_records"]
+
+
+def run_stream(sources, t_end):
+    """Virtual-clock loop over one or more sources; batches admitted at the same poll run
+    concurrently on their queries' streams (real contention), each query's next poll is the
+    first tick at or after its batch completed."""
+    for tick in range(int(round(t_end / POLL)) + 1):
+        now = tick * POLL
+        admitted = []
+        for s in sources:
+            if now + 1e-12 < s.busy_until:
+                continue
+            s.push_until(now)
+            if s.force_at is not None:
+                idx = s.q.force(now) if s.pending_records >= s.force_at else None
+            else:
+                idx, _ = s.q.poll(now)
+            if idx is not None:
+                admitted.append((s, idx))
+        for s, idx in admitted:
+            s.q.sync()
+            s.q.read_lr1() if s.q.kind in (0, 1) else s.q.read_agg()
+            s.completed(s.q.record(idx))
+    for s in sources:                              # the rest: one flush batch
+        s.push_until(float("inf"))
+        s.q.flush(t_end + POLL)
+        s.q.read_lr1() if s.q.kind in (0, 1) else s.q.read_agg()
+        s.completed(s.q.record(s.q.num_batches() - 1))
+
+
+def summarize(name, s, target=None, exclude_flush=True):
+    recs = s.recs[:-1] if exclude_flush and len(s.recs) > 1 else s.recs
+    ml = [r["max_lat_s"] for r in recs]
+    pr = [r["proc_s"] for r in recs]
+    dv = [r["device_s"] for r in recs]
+    nrec = sum(r["num_records"] for r in recs)
+    out = {"config": name, "batches": len(recs), "records": nrec,
+           "max_lat_s": {"p50": pct(ml, 50), "p99": pct(ml, 99), "max": max(ml) if ml else None},
+           "proc_ms": {"p50": 1e3 * pct(pr, 50), "p99": 1e3 * pct(pr, 99)} if pr else None,
+           "device_ms": {"p50": 1e3 * pct(dv, 50), "p99": 1e3 * pct(dv, 99)} if dv else None,
+           "mean_dataset_latency_s": sum(s.lat) / len(s.lat) if s.lat else None,
+           "records_per_batch_p50": pct([r["num_records"] for r in recs], 50),
+           "processing_records_per_s": nrec / sum(dv) if dv and sum(dv) > 0 else None,
+           "bad_records": sum(r["bad_records"] for r in s.recs),
+           "late_records": sum(r["late_records"] for r in s.recs)}
+    if target is not None:
+        out["target_s"] = target
+        out["violation_fraction"] = sum(1 for x in ml if x > target) / len(ml) if ml else None
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="C1,C2,C3,C5")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "latency_configs.json"))
+    ap.add_argument("--seed", type=int, default=211104289)
+    ap.add_argument("--c3-seconds", type=int, default=300)
+    ap.add_argument("--c5-seconds", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+    import paper_2111_04289_b200 as P
+    torch.cuda.set_device(0)
+    want = set(args.configs.split(","))
+    results = []
+    t0 = time.time()
+
+    def emit(d):
+        print(json.dumps(d), flush=True)
+        results.append(d)
+
+    if "C1" in want:   # CM1 on B(1), 10 s, one OS(t10) trigger
+        q = P.Query("CM1S", mode="trigger", trigger_s=10.0, max_batch_bytes=1 << 24)
+        s = Source(q, "CM", "B(1)", 10, 1, args.seed)
+        run_stream([s], 10.0)
+        emit(summarize("C1 CM1S B(1) 10 s, OS(t10) single trigger", s))
+        q.close()
+    if "C2" in want:   # LR1S on U(100), Alg. 1 (SlideTime 5 s)
+        q = P.Query("LR1S", mode="lmstream", max_batch_bytes=1 << 28)
+        s = Source(q, "LR", "U(100)", 120, 10, args.seed)
+        run_stream([s], 120.0)
+        emit(summarize("C2 LR1S U(100) 120 s, LMStream (SlideTime 5 s)", s, target=5.0))
+        q.close()
+    if "C3" in want:   # LR2S on R(50,500): Alg. 1, CG(d5), CG(d0), OS(t10)
+        for mode, kw, tgt in (("lmstream", {}, 10.0), ("deadline", {"deadline_s": 5.0}, 5.0),
+                              ("deadline", {"deadline_s": 0.0}, None), ("trigger", {"trigger_s": 10.0}, 10.0)):
+            q = P.Query("LR2S", mode=mode, max_batch_bytes=1 << 30, **kw)
+            s = Source(q, "LR", "R(50,500)", args.c3_seconds, 10, args.seed)
+            run_stream([s], float(args.c3_seconds))
+            label = {"lmstream": "LMStream (SlideTime 10 s)", "trigger": "OS(t10)"}.get(
+                mode, f"CG(d{kw.get('deadline_s', 0):g})")
+            emit(summarize(f"C3 LR2S R(50,500) {args.c3_seconds} s, {label}", s, target=tgt))
+            q.close()
+            torch.cuda.empty_cache()
+    if "C5" in want:   # mixed LR2 + CM2 on B(10000), CG(d1), two handles / streams
+        ql = P.Query("LR2S", mode="deadline", deadline_s=1.0, max_batch_bytes=3 << 30)
+        qc = P.Query("CM2S", mode="deadline", deadline_s=1.0, max_batch_bytes=5 << 30)
+        sl = Source(ql, "LR", "B(10000)", args.c5_seconds, 100, args.seed)
+        sc = Source(qc, "CM", "B(10000)", args.c5_seconds, 100, args.seed + 1)
+        run_stream([sl, sc], float(args.c5_seconds))
+        emit(summarize(f"C5 mixed: LR2S B(10000) {args.c5_seconds} s, CG(d1)", sl, target=1.0))
+        emit(summarize(f"C5 mixed: CM2S B(10000) {args.c5_seconds} s, CG(d1)", sc, target=1.0))
+        ql.close()
+        qc.close()
+        # MANUAL sweep: both streams forced at a fixed batch size (records per query)
+        for size in (100_000, 1_000_000, 3_000_000, 10_000_000, 30_000_000):
+            ql = P.Query("LR2S", mode="manual", max_batch_bytes=max(1 << 26, 80 * size))
+            qc = P.Query("CM2S", mode="manual", max_batch_bytes=max(1 << 26, 150 * size))
+            sl = Source(ql, "LR", "B(10000)", args.c5_seconds, 100, args.seed)
+            sc = Source(qc, "CM", "B(10000)", args.c5_seconds, 100, args.seed + 1)
+            sl.force_at = sc.force_at = size
+            run_stream([sl, sc], float(args.c5_seconds))
+            for nm, src in (("LR2S", sl), ("CM2S", sc)):
+                d = summarize(f"C5 sweep: {nm} B(10000) {args.c5_seconds} s, MANUAL batches of {size} records", src)
+                d["forced_batch_records"] = size
+                emit(d)
+            ql.close()
+            qc.close()
+            torch.cuda.empty_cache()
+    doc = {"device": torch.cuda.get_device_name(0), "seed": args.seed, "poll_s": POLL,
+           "wall_s": time.time() - t0, "results": results}
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    with open(args.out, "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
