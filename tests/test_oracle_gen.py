@@ -138,3 +138,28 @@ def test_golden_digests():
         for t, data in g.stream_datasets(fam, traffic, 3):
             h.update(data)
         assert h.hexdigest() == want, key
+
+
+def test_vectorised_columns_match_scalar_generator():
+    """lmsgen.vec (numpy column form, used by the full-size checks) == lmsgen.lr_fields /
+    cm_fields record by record, incl. the u() high-product at large n (jobId map)."""
+    import numpy as np
+    from lmsgen import vec
+    rng = np.random.default_rng(5)
+    assert [int(v) for v in vec.mix(np.array([0, 1, 2 ** 64 - 1], dtype=np.uint64))] == \
+        [g.mix(0), g.mix(1), g.mix(2 ** 64 - 1)]
+    xs = rng.integers(0, 2 ** 63, 1000, dtype=np.uint64) * np.uint64(2) + np.uint64(1)
+    for n in (2, 100, 500000, 9 * 10 ** 9, 2 ** 63 + 12345):
+        assert [int(v) for v in vec.u(xs, n)] == [g.u(int(x), n) for x in xs]
+    for t, p in ((0, g.LRParams()), (17, g.LRParams(num_xways=3, num_vehicles=77))):
+        cols = vec.lr_columns(g.SEED, t, 3000, p)
+        for i in rng.integers(0, 3000, 200):
+            f = g.lr_fields(g.SEED, t, int(i), p)
+            assert (f["vid"], f["xway"], f["dir"], f["seg"], f["lane"], f["spd"]) == tuple(
+                int(cols[k][i]) for k in ("vid", "xway", "dir", "seg", "lane", "spd"))
+    for t, p in ((0, g.CMParams()), (5, g.CMParams(num_jobs=300, sel_ppm=700000))):
+        cols = vec.cm_columns(g.SEED, t, 3000, p)
+        for i in rng.integers(0, 3000, 200):
+            f = g.cm_fields(g.SEED, t, int(i), p)
+            assert (f["job"], f["event"], f["cat"], f["cpu_m"]) == tuple(
+                int(cols[k][i]) for k in ("job", "event", "cat", "cpu_m"))
