@@ -137,11 +137,13 @@ def gen_inputs(wl, seconds, t0, seed, torch):
 
 
 def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
+    import numpy as np
     import paper_2111_04289_b200 as P
     dev = torch.cuda.current_device()
     inputs = gen_inputs(wl, warmup + steps, 0, seed, torch)
     q = P.Query(wl["kind"], mode="manual", device=dev, max_batch_bytes=1 << 20, rank=rank, world=world)
     out = {"agg_s": [], "close_s": [], "batch_s": [], "rows": 0}
+    rowbuf = np.zeros(1 << 16, P.AGG_DTYPE)             # caller-owned result buffer (pages touched)
     if world > 1:
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
         h, ex = RankHandle(q), TorchDistExchange()
@@ -153,8 +155,12 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
         else:
             q.force(float(t) + 1.0)
             q.sync()
-        rows = q.read_agg()
-        return len(rows)
+        n = 0
+        while True:                                   # results to host, into a reused buffer
+            rows = q.read_agg(out=rowbuf)
+            n += len(rows)
+            if len(rows) < len(rowbuf):
+                return n
 
     for i in range(warmup):
         step(*inputs[i])
@@ -209,6 +215,7 @@ def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None):
     torch.cuda.empty_cache()
     cap = max(n for _, n, _ in host) + 4096
     q = P.Query(wl["kind"], mode="manual", device=dev, max_batch_bytes=cap, rank=rank, world=world)
+    rowbuf = np.zeros(1 << 16, P.AGG_DTYPE)
     if world > 1:
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
         hd, ex = RankHandle(q), TorchDistExchange()
@@ -221,9 +228,13 @@ def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None):
         else:
             q.force(float(t) + 1.0)
             q.sync()
-        rows = q.read_agg()
-        d2h.append(rows.nbytes + 88)
-        return rows
+        nb = 0
+        while True:
+            rows = q.read_agg(out=rowbuf)
+            nb += rows.nbytes
+            if len(rows) < len(rowbuf):
+                break
+        d2h.append(nb + 88)
 
     for i in range(warmup):
         step(*host[i])

@@ -99,19 +99,32 @@ class Query:
         return check(L.lms_flush(self.h, now), "lms_flush", ok)
 
     # -- results
-    def _drain(self, fn, dtype, ctype, name):
+    def _drain(self, fn, dtype, ctype, name, out=None):
         n, rem = C.c_uint64(), C.c_uint64()
+        if out is not None:                     # caller-owned, reusable buffer: fill a prefix
+            if out.dtype != dtype or not out.flags.c_contiguous:
+                raise TypeError(f"out must be a C-contiguous {dtype} array")
+            check(fn(self.h, out.ctypes.data_as(C.POINTER(ctype)), len(out), C.byref(n), C.byref(rem)), name)
+            return out[:n.value]
         check(fn(self.h, None, 0, C.byref(n), C.byref(rem)), name)      # how many are queued
         arr = np.empty(rem.value, dtype)
         if rem.value:
             check(fn(self.h, arr.ctypes.data_as(C.POINTER(ctype)), rem.value, C.byref(n), C.byref(rem)), name)
         return arr[:n.value]
 
-    def read_agg(self) -> np.ndarray:
-        return self._drain(L.lms_read_agg, AGG_DTYPE, L.lms_agg_row, "lms_read_agg")
+    def read_agg(self, out=None) -> np.ndarray:
+        """Queued LR2 / CM1 / CM2 rows (FIFO).  out: optional reusable AGG_DTYPE buffer; then
+        at most len(out) rows are read into it and a view of them is returned."""
+        return self._drain(L.lms_read_agg, AGG_DTYPE, L.lms_agg_row, "lms_read_agg", out)
 
-    def read_lr1(self) -> np.ndarray:
-        return self._drain(L.lms_read_lr1, LR1_DTYPE, L.lms_lr1_row, "lms_read_lr1")
+    def read_lr1(self, out=None) -> np.ndarray:
+        return self._drain(L.lms_read_lr1, LR1_DTYPE, L.lms_lr1_row, "lms_read_lr1", out)
+
+    def queued_rows(self) -> int:
+        n, rem = C.c_uint64(), C.c_uint64()
+        fn = L.lms_read_lr1 if self.kind in (L.LMS_LR1S, L.LMS_LR1T) else L.lms_read_agg
+        check(fn(self.h, None, 0, C.byref(n), C.byref(rem)), "lms_read")
+        return rem.value
 
     def num_batches(self) -> int:
         n = C.c_uint64()

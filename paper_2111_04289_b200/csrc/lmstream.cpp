@@ -74,15 +74,39 @@ uint64_t next_pow2(uint64_t v) {
 // FIFO of result rows drained by lms_read_* (contiguous storage + read offset).
 template <typename T>
 struct RowFifo {
-  std::vector<T> v;
-  size_t off = 0;
-  void append(const T* p, uint64_t n) { v.insert(v.end(), p, p + n); }
-  uint64_t size() const { return v.size() - off; }
-  uint64_t read(T* dst, uint64_t cap) {
-    const uint64_t n = std::min<uint64_t>(cap, size());
-    if (n) std::memcpy(dst, v.data() + off, n * sizeof(T));
-    off += n;
-    if (off == v.size()) { v.clear(); off = 0; }
+  // Result rows waiting for lms_read_*: pinned host memory, so the device rows are copied by
+  // DMA straight into the FIFO's tail (one D2H, one copy into the caller's array).
+  T* buf = nullptr;
+  uint64_t cap = 0, head = 0, tail = 0;
+  ~RowFifo() { if (buf) cudaFreeHost(buf); }
+  cudaError_t reserve(uint64_t extra) {
+    if (tail + extra <= cap) return cudaSuccess;
+    const uint64_t live = tail - head;
+    if (live + extra <= cap && buf) {            // compact in place
+      std::memmove(buf, buf + head, live * sizeof(T));
+    } else {
+      const uint64_t ncap = std::max<uint64_t>(2 * cap, live + extra);
+      T* nb = nullptr;
+      cudaError_t e = cudaHostAlloc((void**)&nb, ncap * sizeof(T), cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+      std::memset(static_cast<void*>(nb), 0, ncap * sizeof(T));      // touch the pages now
+      if (live) std::memcpy(static_cast<void*>(nb), buf + head, live * sizeof(T));
+      if (buf) cudaFreeHost(buf);
+      buf = nb;
+      cap = ncap;
+    }
+    head = 0;
+    tail = live;
+    return cudaSuccess;
+  }
+  T* tail_ptr() { return buf + tail; }
+  void commit(uint64_t n) { tail += n; }
+  uint64_t size() const { return tail - head; }
+  uint64_t read(T* dst, uint64_t n_max) {
+    const uint64_t n = std::min<uint64_t>(n_max, size());
+    if (n) std::memcpy(static_cast<void*>(dst), buf + head, n * sizeof(T));
+    head += n;
+    if (head == tail) head = tail = 0;
     return n;
   }
 };
@@ -121,8 +145,7 @@ struct lms_query {
   std::vector<lms_batch_record> records;
   RowFifo<lms_agg_row> agg_rows;
   RowFifo<lms_lr1_row> lr1_rows;
-  void* h_rows = nullptr;          // pinned staging for result rows
-  uint64_t h_rows_cap = 0;         // rows it holds
+  unsigned long long* h_count = nullptr;   // pinned 8 B (merged row count)
   uint64_t launches = 0;
   double last_batch_s = 0, last_agg_s = 0, last_close_s = 0;
   lms_status last_completion = LMS_OK;
@@ -132,7 +155,7 @@ struct lms_query {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : dallocs) cudaFree(p);
     if (h_report) cudaFreeHost(h_report);
-    if (h_rows) cudaFreeHost(h_rows);
+    if (h_count) cudaFreeHost(h_count);
     for (cudaEvent_t e : {ev_start, ev_agg, ev_close, ev_end})
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
@@ -262,7 +285,7 @@ lms_status launch_close_stage(lms_query* q) {
     q->launches += 2;
   }
   CUDA_TRY(cudaEventRecord(q->ev_close, q->stream));
-  CUDA_TRY(cudaMemcpyAsync(q->h_report, q->qd.report, sizeof(BatchReport), cudaMemcpyDeviceToHost, q->stream));
+  // the batch report lives in mapped pinned memory: the close kernel writes it to the host
   CUDA_TRY(cudaEventRecord(q->ev_end, q->stream));
   q->awaiting_close = false;
   q->in_flight = true;
@@ -289,17 +312,18 @@ lms_status complete(lms_query* q) {
   double d2h = 0;
   if (nrows) {
     const double t0 = now_host();
-    // device rows -> pinned staging (chunks) -> host FIFO
-    const size_t rsz = is_lr1(q->kind) ? sizeof(lms_lr1_row) : sizeof(lms_agg_row);
+    // device rows -> (DMA) -> pinned host FIFO
     const uint8_t* src = static_cast<const uint8_t*>(q->qd.rows);
-    for (uint64_t done = 0; done < nrows;) {
-      const uint64_t n = std::min<uint64_t>(nrows - done, q->h_rows_cap);
-      CUDA_TRY(cudaMemcpyAsync(q->h_rows, src + done * rsz, n * rsz, cudaMemcpyDeviceToHost, q->stream));
-      CUDA_TRY(cudaStreamSynchronize(q->stream));
-      if (is_lr1(q->kind)) q->lr1_rows.append(static_cast<const lms_lr1_row*>(q->h_rows), n);
-      else q->agg_rows.append(static_cast<const lms_agg_row*>(q->h_rows), n);
-      done += n;
+    if (is_lr1(q->kind)) {
+      CUDA_TRY(q->lr1_rows.reserve(nrows));
+      CUDA_TRY(cudaMemcpyAsync(q->lr1_rows.tail_ptr(), src, nrows * sizeof(lms_lr1_row), cudaMemcpyDeviceToHost, q->stream));
+    } else {
+      CUDA_TRY(q->agg_rows.reserve(nrows));
+      CUDA_TRY(cudaMemcpyAsync(q->agg_rows.tail_ptr(), src, nrows * sizeof(lms_agg_row), cudaMemcpyDeviceToHost, q->stream));
     }
+    CUDA_TRY(cudaStreamSynchronize(q->stream));
+    if (is_lr1(q->kind)) q->lr1_rows.commit(nrows);
+    else q->agg_rows.commit(nrows);
     d2h = now_host() - t0;
   }
   q->in_used[q->in_flight_buf] = 0;
@@ -414,10 +438,12 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     QC_TRY(cudaStreamCreateWithFlags(&q->stream, cudaStreamNonBlocking));
     QC_TRY(cudaStreamCreateWithFlags(&q->copy_stream, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&q->ev_start, &q->ev_agg, &q->ev_close, &q->ev_end}) QC_TRY(cudaEventCreate(e));
-    QC_TRY(cudaHostAlloc((void**)&q->h_report, sizeof(BatchReport), cudaHostAllocDefault));
-    q->h_rows_cap = std::min<uint64_t>(cfg->max_result_rows, 1ull << 16);
-    QC_TRY(cudaHostAlloc(&q->h_rows, q->h_rows_cap * std::max(sizeof(lms_agg_row), sizeof(lms_lr1_row)),
-                         cudaHostAllocDefault));
+    QC_TRY(cudaHostAlloc((void**)&q->h_report, sizeof(BatchReport), cudaHostAllocMapped));
+    QC_TRY(cudaHostAlloc((void**)&q->h_count, sizeof(unsigned long long), cudaHostAllocDefault));
+    {   // pre-size the result FIFO (pinned, pages touched) for up to 64 K rows
+      const uint64_t pre = std::min<uint64_t>(cfg->max_result_rows, 1ull << 16);
+      QC_TRY(is_lr1(q->kind) ? q->lr1_rows.reserve(pre) : q->agg_rows.reserve(pre));
+    }
     std::memset(q->h_report, 0, sizeof(BatchReport));
 
     QueryDev& d = q->qd;
@@ -434,7 +460,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     d.rank = (uint32_t)cfg->rank;
     d.world = (uint32_t)cfg->world;
     Q_TRY(q->dalloc(&d.state, 1, 0));
-    Q_TRY(q->dalloc(&d.report, 1, 0));
+    QC_TRY(cudaHostGetDevicePointer((void**)&d.report, q->h_report, 0));   // zero-copy report
     if (d.world > 1) {                // owner-side merge of partial rows
       lms_agg_row* send;
       Q_TRY(q->dalloc(&send, cfg->max_result_rows, 0));
@@ -751,20 +777,18 @@ lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
       CUDA_TRY(launch_merge(q->qd, rows, n, k, nwin, q->stream));
       q->launches += 2;
     }
-    // final rows -> pinned staging -> host FIFO
+    // final rows -> (DMA) -> pinned host FIFO
     unsigned long long* d_rows = &q->qd.state->rows;
-    CUDA_TRY(cudaMemcpyAsync(q->h_rows, d_rows, sizeof(unsigned long long), cudaMemcpyDeviceToHost, q->stream));
+    CUDA_TRY(cudaMemcpyAsync(q->h_count, d_rows, sizeof(unsigned long long), cudaMemcpyDeviceToHost, q->stream));
     CUDA_TRY(cudaStreamSynchronize(q->stream));
-    const uint64_t total = *static_cast<unsigned long long*>(q->h_rows);
+    const uint64_t total = *q->h_count;
     const uint64_t nrows = std::min<uint64_t>(total, q->cfg.max_result_rows);
-    const uint8_t* src = static_cast<const uint8_t*>(q->qd.rows);
-    for (uint64_t done = 0; done < nrows;) {
-      const uint64_t m = std::min<uint64_t>(nrows - done, q->h_rows_cap);
-      CUDA_TRY(cudaMemcpyAsync(q->h_rows, src + done * sizeof(lms_agg_row), m * sizeof(lms_agg_row),
+    if (nrows) {
+      CUDA_TRY(q->agg_rows.reserve(nrows));
+      CUDA_TRY(cudaMemcpyAsync(q->agg_rows.tail_ptr(), q->qd.rows, nrows * sizeof(lms_agg_row),
                                cudaMemcpyDeviceToHost, q->stream));
       CUDA_TRY(cudaStreamSynchronize(q->stream));
-      q->agg_rows.append(static_cast<const lms_agg_row*>(q->h_rows), m);
-      done += m;
+      q->agg_rows.commit(nrows);
     }
     CUDA_TRY(cudaMemsetAsync(d_rows, 0, sizeof(unsigned long long), q->stream));
     if (!q->records.empty()) {
