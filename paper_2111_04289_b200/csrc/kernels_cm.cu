@@ -81,18 +81,34 @@ struct TileGeom {
   uint32_t payload;                  // tile payload bytes (<= kCmTile)
 };
 
-__device__ __forceinline__ TileGeom cm_geom(const SegTable& s, SegCursor& c, unsigned long long tile) {
-  c.seek(s, tile);
-  TileGeom g;
-  const unsigned long long lt = tile - c.base;
-  g.seg = s.s[c.si].ptr;
-  g.off = lt * (unsigned long long)kCmTile;
-  const unsigned long long rem = s.s[c.si].nbytes - g.off;
-  g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
-  g.lo = lt == 0 ? kCmHaloL : 0;
-  g.hi = kCmHaloL + (uint32_t)(rem < (unsigned long long)kCmWin ? rem : kCmWin);
-  return g;
-}
+// A warp's walk over its contiguous tile range: the current tile's segment and offset,
+// advanced one tile at a time (the segment changes only at segment ends).
+struct TileIter {
+  const uint8_t* seg;
+  unsigned long long off, nbytes;      // tile start within the segment, segment size
+  int si;
+  __device__ __forceinline__ void init(const SegTable& s, unsigned long long tile) {
+    si = 0;
+    while (si + 1 < s.n && tile >= s.tile_prefix[si + 1]) si++;
+    seg = s.s[si].ptr;
+    nbytes = s.s[si].nbytes;
+    off = (tile - s.tile_prefix[si]) * (unsigned long long)kCmTile;
+  }
+  __device__ __forceinline__ void next(const SegTable& s) {
+    off += kCmTile;
+    if (off >= nbytes && si + 1 < s.n) { si++; seg = s.s[si].ptr; nbytes = s.s[si].nbytes; off = 0; }
+  }
+  __device__ __forceinline__ TileGeom geom() const {
+    TileGeom g;
+    g.seg = seg;
+    g.off = off;
+    const unsigned long long rem = nbytes - off;
+    g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
+    g.lo = off == 0 ? kCmHaloL : 0;
+    g.hi = kCmHaloL + (uint32_t)(rem < (unsigned long long)kCmWin ? rem : kCmWin);
+    return g;
+  }
+};
 
 __device__ __forceinline__ void cm_issue(const TileGeom& g, uint8_t* dst, uint64_t* bar) {
   const uint32_t bulk = (g.hi - g.lo) & ~15u;
@@ -320,14 +336,14 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     mbar_fence_init();
   }
   __syncthreads();
-  SegCursor cur, iss;                          // consumer / producer (2 tiles ahead) cursors
-  cur.init(a.segs);
-  iss.init(a.segs);
-  for (int s = 0; s < kCmStages; s++)
-    if (t0 + s < t1) {
-      const TileGeom gi = cm_geom(a.segs, iss, t0 + s);
-      if (lane == 0) cm_issue(gi, wsmem + s * kCmStage, &full[warp][s]);
-    }
+  const uint32_t ntiles = (uint32_t)(t1 - t0);
+  TileIter cur, iss;                           // consumer / producer (2 tiles ahead)
+  cur.init(a.segs, t0);
+  iss.init(a.segs, t0);
+  for (uint32_t s = 0; s < (uint32_t)kCmStages && s < ntiles; s++) {
+    if (lane == 0) cm_issue(iss.geom(), wsmem + s * kCmStage, &full[warp][s]);
+    iss.next(a.segs);
+  }
 
   const unsigned long long wm_prev = q.state->wm_prev;
   CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
@@ -353,11 +369,12 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     __syncwarp();
   };
 
-  for (unsigned long long t = t0; t < t1; t++) {
-    const int s = (int)((t - t0) % kCmStages);
-    const uint32_t ph = (uint32_t)(((t - t0) / kCmStages) & 1);
+  for (uint32_t it = 0; it < ntiles; it++) {
+    const int s = (int)(it % kCmStages);
+    const uint32_t ph = (it / kCmStages) & 1u;
     uint8_t* buf = wsmem + s * kCmStage;
-    const TileGeom g = cm_geom(a.segs, cur, t);
+    const TileGeom g = cur.geom();
+    cur.next(a.segs);
     mbar_wait(&full[warp][s], ph);
     {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
       const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
@@ -412,10 +429,12 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const uint4 nw = lds128(nl_s + 16 * lane);
     const bool prev_nl = lane == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
                                    : (nl32[4 * lane - 1] >> 31) != 0;
+    uint32_t f_mine;                            // first newline of my chunk (0xFFFF: none)
     {
       const uint32_t w = nw.x ? nw.x : (nw.y ? nw.y : (nw.z ? nw.z : nw.w));
       const uint32_t k = nw.x ? 0u : (nw.y ? 32u : (nw.z ? 64u : 96u));
-      fnl[lane] = w ? (uint16_t)(cb + k + lsb32(w)) : (uint16_t)0xFFFFu;
+      f_mine = w ? cb + k + lsb32(w) : 0xFFFFu;
+      fnl[lane] = (uint16_t)f_mine;
       if (lane < 2) {                           // halo chunks kChunks, kChunks + 1
         const uint32_t hb = (kChunks + lane) * kChunk;
         const uint4 hw = lds128(nl_s + hb / 8);
@@ -430,12 +449,17 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const uint32_t e_after = fnl[lane + 1] != 0xFFFFu ? (uint32_t)fnl[lane + 1] : (uint32_t)fnl[lane + 2];
     const uint32_t limit = min(cb + (uint32_t)kChunk, g.payload);   // starts must lie below
     uint32_t n0 = nw.x, n1 = nw.y, n2 = nw.z, n3 = nw.w;             // my unconsumed newlines
+    uint32_t rem = __popc(n0) + __popc(n1) + __popc(n2) + __popc(n3);
     uint32_t prev = cb - 1u;                    // '\n' before the next record (cb - 1: wraps at 0)
     bool have = prev_nl;
-    if (!have) {
-      uint32_t b0;
-      have = pop_lowest(n0, n1, n2, n3, b0);
-      prev = cb + b0;
+    if (!have && rem) {                         // first record starts after my first newline
+      prev = f_mine;
+      have = true;
+      rem--;
+      if (rem) {                                // (short lines only) drop it from the words
+        uint32_t b0;
+        pop_lowest(n0, n1, n2, n3, b0);
+      }
     }
     have = have && prev + 1u < limit;
     // ---- Pass 3: decode my records; aggregate (one record per lane per round)
@@ -446,9 +470,13 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       bool next = false;
       if (have) {
         cnt.n++;
-        uint32_t bn;
-        const bool inchunk = pop_lowest(n0, n1, n2, n3, bn);
-        const uint32_t e = inchunk ? cb + bn : e_after;           // my record's '\n'
+        uint32_t bn = 0;
+        bool inchunk = false;
+        if (rem) {                              // another newline in my chunk (short lines)
+          inchunk = pop_lowest(n0, n1, n2, n3, bn);
+          rem--;
+        }
+        const uint32_t e = inchunk ? cb + bn : e_after;           // my record's newline
         prev = e;
         next = inchunk && e + 1u < limit;
         const int ok = e == 0xFFFFu ? (cm_parse_serial(buf, kCmHaloL + cb + b_cur, g.hi, r) ? 1 : 0)
@@ -518,9 +546,9 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       if (!__any_sync(0xffffffffu, have)) break;   // warp-local rounds
     }
     __syncwarp();      // stage s and the masks consumed by every lane
-    if (t + kCmStages < t1) {
-      const TileGeom gi = cm_geom(a.segs, iss, t + kCmStages);
-      if (lane == 0) cm_issue(gi, buf, &full[warp][s]);
+    if (it + kCmStages < ntiles) {
+      if (lane == 0) cm_issue(iss.geom(), buf, &full[warp][s]);
+      iss.next(a.segs);
     }
   }
 
