@@ -251,14 +251,20 @@ def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None):
         dist.barrier()
     el = e0.elapsed_time(e1) / 1e3
     if world > 1:
-        t = torch.tensor([el], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
+        el = max_over_ranks(el, torch, dist)
     recs = [q.record(i) for i in range(warmup, n_sec)]
     q.close()
     return {"elapsed_s": el, "h2d_bytes_per_step": float(np.mean([n for _, n, _ in host[warmup:]])),
             "d2h_bytes_per_step": float(np.mean(d2h[warmup:])),
             "proc_s": [r["proc_s"] for r in recs], "h2d_s": [r["h2d_s"] for r in recs]}
+
+
+def max_over_ranks(x, torch, dist):
+    """Max of a host scalar over ranks (NCCL: a device tensor; gloo: a host tensor)."""
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def pct(v, p):
@@ -334,19 +340,23 @@ def main():
 
     import torch
     dist = None
+    # one process per GPU; LMS_DIST_BACKEND=gloo (tests only) lets N ranks share fewer GPUs
+    backend = os.environ.get("LMS_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2111_04289_b200 import build  # noqa: F401  (library must already be built)
 
     seed = args.seed + 7919 * rank        # each rank: its own partition of the global batch
     res = device_run(wl, args.steps, args.warmup, seed, rank, world, torch, dist)
     el = res["elapsed_s"]
     if world > 1:
-        t = torch.tensor([el], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
+        el = max_over_ranks(el, torch, dist)
     recs = wl["records"] * world * args.steps
     value = recs / el
     pk = peaks()
@@ -356,6 +366,8 @@ def main():
     if args.secondary and args.secondary != args.workload:
         w2 = WORKLOADS[args.secondary]
         r2 = device_run(w2, max(5, args.steps // 2), args.warmup, seed, rank, world, torch, dist)
+        if world > 1:
+            r2["elapsed_s"] = max_over_ranks(r2["elapsed_s"], torch, dist)
         a2 = statistics.mean(r2["agg_s"])
         sec = {"workload": w2["desc"], "records_per_s": w2["records"] * world * len(r2["agg_s"]) / r2["elapsed_s"],
                "ms_per_step": 1e3 * r2["elapsed_s"] / len(r2["agg_s"]),

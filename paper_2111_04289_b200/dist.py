@@ -112,6 +112,33 @@ class TorchDistExchange:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo (CPU protocol tests, or ranks sharing one GPU in tests): stage device tensors
+        # through host memory; NCCL runs on the library's stream directly
+        self.host_staged = dist.get_backend(group) == "gloo"
+
+    def _all_reduce(self, t, op):
+        if self.host_staged and t.is_cuda:
+            import torch
+            torch.cuda.synchronize()
+            c = t.cpu()
+            self.dist.all_reduce(c, op=op, group=self.group)
+            t.copy_(c)
+            torch.cuda.synchronize()
+        else:
+            self.dist.all_reduce(t, op=op, group=self.group)
+
+    def _a2a(self, out, inp, out_splits=None, in_splits=None):
+        if self.host_staged and inp.is_cuda:
+            import torch
+            torch.cuda.synchronize()
+            co = torch.empty(out.shape, dtype=out.dtype)
+            self.dist.all_to_all_single(co, inp.cpu(), output_split_sizes=out_splits,
+                                        input_split_sizes=in_splits, group=self.group)
+            out.copy_(co)
+            torch.cuda.synchronize()
+        else:
+            self.dist.all_to_all_single(out, inp, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                                        group=self.group)
 
     def _on(self, h):
         import torch
@@ -123,8 +150,8 @@ class TorchDistExchange:
         (h,) = handles
         wm, tsmin = h.watermark_tensors()
         with self._on(h):
-            self.dist.all_reduce(wm, op=self.dist.ReduceOp.MAX, group=self.group)
-            self.dist.all_reduce(tsmin, op=self.dist.ReduceOp.MIN, group=self.group)
+            self._all_reduce(wm, self.dist.ReduceOp.MAX)
+            self._all_reduce(tsmin, self.dist.ReduceOp.MIN)
 
     def all_to_all(self, handles, sends):
         """sends[0] = (uint8 rows tensor grouped by owner, per-owner counts) -> received rows."""
@@ -134,11 +161,10 @@ class TorchDistExchange:
         send_c = torch.tensor(counts, dtype=torch.int64, device=dev)
         recv_c = torch.empty_like(send_c)
         with self._on(h):
-            self.dist.all_to_all_single(recv_c, send_c, group=self.group)
+            self._a2a(recv_c, send_c)
             rc = [int(x) for x in recv_c.tolist()]
             recv = torch.empty(sum(rc) * ROW_BYTES, dtype=torch.uint8, device=dev)
-            self.dist.all_to_all_single(recv, rows, output_split_sizes=[c * ROW_BYTES for c in rc],
-                                        input_split_sizes=[c * ROW_BYTES for c in counts], group=self.group)
+            self._a2a(recv, rows, [c * ROW_BYTES for c in rc], [c * ROW_BYTES for c in counts])
         return [recv]
 
 
