@@ -125,31 +125,25 @@ Dag query_dag(int32_t kind) {
 // ---------------------------------------------------------------- Eq. 10
 
 bool infpt_fit(const double* thput, const double* lat, const double* infpt, uint64_t n, double b[3]) {
-  // OLS via normal equations on regressors (1, thput[MB/s], lat[s]); long double,
-  // partial pivoting; singular -> insufficient history.
+  // Eq. 10 OLS on regressors (1, thput[MB/s], lat[s]) in long double.  The regressors
+  // are centred first (the normal equations of the intercept decouple: b0 = mean(y) - b1
+  // mean(t) - b2 mean(l)), which removes the cancellation of the raw normal equations when
+  // the cumulative AvgThPut (Eq. 4) settles; singular 2x2 -> insufficient history.
   if (n < 3) return false;
-  long double A[3][4] = {};
+  long double mt = 0, ml = 0, my = 0;
+  for (uint64_t r = 0; r < n; r++) { mt += thput[r] / 1e6L; ml += lat[r]; my += infpt[r]; }
+  mt /= n; ml /= n; my /= n;
+  long double stt = 0, sll = 0, stl = 0, sty = 0, sly = 0;
   for (uint64_t r = 0; r < n; r++) {
-    const long double x[3] = {1.0L, (long double)thput[r] / 1e6L, (long double)lat[r]};
-    for (int i = 0; i < 3; i++) {
-      for (int j = 0; j < 3; j++) A[i][j] += x[i] * x[j];
-      A[i][3] += x[i] * (long double)infpt[r];
-    }
+    const long double t = thput[r] / 1e6L - mt, l = lat[r] - ml, y = infpt[r] - my;
+    stt += t * t; sll += l * l; stl += t * l; sty += t * y; sly += l * y;
   }
-  long double scale = 0;
-  for (int i = 0; i < 3; i++) for (int j = 0; j < 3; j++) scale = std::max(scale, std::fabs(A[i][j]));
-  for (int c = 0; c < 3; c++) {
-    int p = c;
-    for (int r = c + 1; r < 3; r++) if (std::fabs(A[r][c]) > std::fabs(A[p][c])) p = r;
-    if (std::fabs(A[p][c]) <= scale * 1e-14L) return false;
-    if (p != c) for (int k = 0; k < 4; k++) std::swap(A[p][k], A[c][k]);
-    for (int r = 0; r < 3; r++) {
-      if (r == c) continue;
-      const long double f = A[r][c] / A[c][c];
-      for (int k = 0; k < 4; k++) A[r][k] -= f * A[c][k];
-    }
-  }
-  for (int i = 0; i < 3; i++) b[i] = (double)(A[i][3] / A[i][i]);
+  const long double det = stt * sll - stl * stl;
+  if (!(stt > 0) || !(sll > 0) || det <= stt * sll * 1e-15L) return false;
+  const long double b1 = (sty * sll - sly * stl) / det, b2 = (sly * stt - sty * stl) / det;
+  b[0] = (double)(my - b1 * mt - b2 * ml);
+  b[1] = (double)b1;
+  b[2] = (double)b2;
   return true;
 }
 

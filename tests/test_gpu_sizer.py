@@ -141,3 +141,43 @@ def test_percentiles_of_maxlat():
         out = C.c_double()
         L.check(L.lms_percentile(arr, len(lat), p, C.byref(out)), "lms_percentile")
         assert out.value == percentile_nearest_rank(lat, p)
+
+
+def test_online_infpt_regression_in_the_loop():
+    """LMS_FLAG_ONLINE_INFPT: after every completed batch the library refits Eq. 10 on the
+    (AvgThPut, MaxLat, InfPT) history and the next batch's Alg. 2 runs with the
+    predicted InfPT — the oracle's exact-rational OLS on the same history must agree."""
+    import paper_2111_04289_b200 as P
+    from oracle import regression as RG
+    from paper_2111_04289_b200 import _lib as L
+    from paper_2111_04289_b200 import sim
+    secs = list(g.stream_datasets("LR", "R(0.3,3)", 70, seed=9))
+    arr = sim.split_seconds("LR", secs, 5)
+    with P.Query("LR2S", mode="deadline", deadline_s=0.0, flags=L.LMS_FLAG_ONLINE_INFPT) as q:
+        res = sim.run(q, arr, 70.0)
+    recs = res.records
+    assert len(recs) > 20
+    hist, infpt, updates = [], 150e3, 0
+
+    def conditioning(rows):
+        """1 - corr^2 of the centred regressors (0: collinear)."""
+        import numpy as np
+        t = np.array([x[0] / 1e6 for x in rows]); lt = np.array([x[1] for x in rows])
+        t, lt = t - t.mean(), lt - lt.mean()
+        stt, sll, stl = (t * t).sum(), (lt * lt).sum(), (t * lt).sum()
+        return 0.0 if stt <= 0 or sll <= 0 else 1.0 - stl * stl / (stt * sll)
+
+    for r in recs:
+        if r["inf_pt_bytes"] != pytest.approx(infpt, rel=1e-6):
+            # fp vs exact-rational OLS may only part ways on a (near-)collinear history, where
+            # Eq. 10's prediction is ill-posed; the feedback makes the runs differ after that
+            assert len(hist) >= 3 and conditioning(hist[-256:]) < 1e-6, (len(hist), r["inf_pt_bytes"], infpt)
+            break
+        if r["num_datasets"] == 0:
+            continue
+        hist.append((r["avg_thput_Bps"], r["max_lat_s"], r["inf_pt_bytes"]))
+        b = RG.fit(hist[-256:])
+        if b is not None:
+            infpt = RG.predict(b, *RG.targets(hist[-256:], 10.0))   # LR2S: SlideTime 10 s
+            updates += 1
+    assert updates > 10
