@@ -274,18 +274,37 @@ def pct(v, p):
 
 # ----------------------------------------------------------------------------- CPU / reference arm
 
-def cpu_sample(kind, seconds=2, rate=6000, seed=211104289):
-    """The oracle as it stands (single-threaded Python) on a bounded sample of the same
-    workload: `seconds` datasets of `rate` records, parse + windows (Replay, flush)."""
+def _sample_datasets(fam, seconds, rate, seed, t0=0):
+    """Input bytes of the bounded CPU sample: the records of seconds t0.. of the same seeded
+    workload (the GPU generator when a GPU is present — byte-identical to the Python one —
+    so that generating the sample costs no CPU minutes; generation is not timed)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            from lmsgen import cuda as gcu
+            out = []
+            for t in range(t0, t0 + seconds):
+                buf, n = gcu.second_tensor(fam, t, rate, seed=seed)
+                out.append(bytes(buf[:n].cpu().numpy()))
+            return out
+    except Exception:
+        pass
     import lmsgen as g
+    return [d for _, d in g.stream_datasets(fam, f"B({rate / 1000})", seconds, seed=seed, t0=t0)]
+
+
+def cpu_sample(kind, seconds=2, rate=450_000, seed=211104289, t0=0):
+    """The oracle as it stands (single-threaded Python) on a bounded sample of the same
+    workload: `seconds` datasets of `rate` records (seconds t0..), parse + windows (Replay,
+    flush).  Default ~0.9M records: about 10 s of CPU."""
     from oracle import queries as Q
     fam = "CM" if kind.startswith("CM") else "LR"
-    data = [d for _, d in g.stream_datasets(fam, f"B({rate / 1000})", seconds, seed=seed)]
+    data = _sample_datasets(fam, seconds, rate, seed, t0)
     nbytes = sum(len(d) for d in data)
     q = Q.query_spec(kind)
-    t0 = time.perf_counter()
+    t0_ = time.perf_counter()
     outs = Q.replay(q, [[d] for d in data])
-    el = time.perf_counter() - t0
+    el = time.perf_counter() - t0_
     n = seconds * rate
     return {"records": n, "bytes": nbytes, "elapsed_s": el, "records_per_s": n / el,
             "rows": sum(len(o.rows) for o in outs)}
@@ -296,9 +315,9 @@ def reference_arm(args, wl, rank, world):
         return 0
     per = []
     for _ in range(args.warmup):
-        cpu_sample(wl["kind"], seconds=1, rate=3000)
-    for _ in range(args.steps):
-        per.append(cpu_sample(wl["kind"], seconds=2, rate=3000))
+        cpu_sample(wl["kind"], seconds=1, rate=10_000)
+    for i in range(args.steps):       # each step: 2 seconds x 30k records of the workload
+        per.append(cpu_sample(wl["kind"], seconds=2, rate=30_000, t0=2 * i))
     tot_r = sum(p["records"] for p in per)
     tot_t = sum(p["elapsed_s"] for p in per)
     v = tot_r / tot_t
@@ -306,10 +325,10 @@ def reference_arm(args, wl, rank, world):
             "value": v, "unit": "records/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64+f64 (Python)", "data": "synthetic (lmsgen, seeded)",
-            "config": {"workload": wl["desc"] + " -- bounded sample: 2 datasets x 3000 records per step",
-                       "global_batch": 6000, "parallelism": "none (1 host thread)"},
+            "config": {"workload": wl["desc"] + " -- bounded sample: 2 datasets x 30000 records per step",
+                       "global_batch": 60000, "parallelism": "none (1 host thread)"},
             "cpu_baseline": {"value": v, "unit": "records/s", "cores": 1, "kind": "oracle",
-                             "sample": "2 x 3000-record datasets of the same generator per step"},
+                             "sample": "2 x 30000-record datasets (seconds 2i, 2i+1) of the same generator per step"},
             "e2e": {"value": v, "unit": "records/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
     return 0
@@ -385,9 +404,9 @@ def main():
                "proc_ms_p99": 1e3 * pct(e["proc_s"], 99), "h2d_ms_mean": 1e3 * statistics.mean(e["h2d_s"])}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        s = cpu_sample(wl["kind"], seconds=2, rate=6000)
+        s = cpu_sample(wl["kind"], seconds=2, rate=450_000)
         cpu = {"value": s["records_per_s"], "unit": "records/s", "cores": 1, "kind": "oracle",
-               "sample": f"{s['records']} records (2 x 6000-record datasets of the same generator), "
+               "sample": f"{s['records']} records (2 x 450000-record datasets of the same generator), "
                          f"{s['elapsed_s']:.1f} s single-threaded Python"}
     if rank == 0:
         line = {
