@@ -342,16 +342,22 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   if (w.any) {
     const uint32_t kk0 = (q.kind == kCM1S || q.kind == kCM1T) ? 0 : k0;
     const uint32_t kk1 = (q.kind == kCM1S || q.kind == kCM1T) ? q.K : k1;
-    __shared__ uint32_t s_sp[1024];                            // slot -> pane (P <= 1024)
+    __shared__ uint32_t s_ev[1024];                            // evicted slots (P <= 1024)
+    __shared__ uint32_t s_nev;
     __syncthreads();
-    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x) s_sp[g] = q.slot_pane[g];
+    if (threadIdx.x == 0) s_nev = 0;
     __syncthreads();
-    for (uint32_t g = 0; g < P; g++) {
-      const uint32_t p = s_sp[g];
-      if (p == kEmpty32 || (long long)p > w.k_last) continue;
+    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x) {   // compact the evicted slots
+      const uint32_t p = q.slot_pane[g];
+      if (p != kEmpty32 && (long long)p <= w.k_last) s_ev[atomicAdd(&s_nev, 1u)] = g;
+    }
+    __syncthreads();
+    const uint32_t nev = s_nev;
+    for (uint32_t i = 0; i < nev; i++) {
+      const size_t g = s_ev[i];
       for (uint32_t k = kk0 + threadIdx.x; k < kk1; k += blockDim.x) {
-        q.acc_sum[(size_t)g * q.K + k] = 0;
-        q.acc_cnt[(size_t)g * q.K + k] = 0;
+        q.acc_sum[g * q.K + k] = 0;
+        q.acc_cnt[g * q.K + k] = 0;
       }
     }
   }
