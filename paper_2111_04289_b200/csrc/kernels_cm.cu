@@ -427,8 +427,9 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     // segment start) and belongs to the chunk holding its first byte.
     const uint32_t cb = lane * kChunk;
     const uint4 nw = lds128(nl_s + 16 * lane);
+    const uint32_t prev_w = __shfl_up_sync(0xffffffffu, nw.w, 1);   // chunk l-1's last word
     const bool prev_nl = lane == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
-                                   : (nl32[4 * lane - 1] >> 31) != 0;
+                                   : (prev_w >> 31) != 0;
     uint32_t f_mine;                            // first newline of my chunk (0xFFFF: none)
     {
       const uint32_t w = nw.x ? nw.x : (nw.y ? nw.y : (nw.z ? nw.z : nw.w));
