@@ -274,26 +274,68 @@ __device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32
   uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
   if (nh < 6u || __popc(t0) + __popc(t1) < 6u) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
   uint32_t c[10];
+  // ---- head: commas 0..5 = the 6 lowest bits of h1:h0.  c0 ends ts (1..9 digits), c1 = c0 + 1
+  // (empty field 1): anything else is malformed.  Usual shape: a 10-digit jobId, so c2 =
+  // c0 + 12 is read off the mask; taskIndex / machineId are free-form: two pops give c3, c4.
+  const uint32_t o0 = lsb32(h0 | 0x80000000u);               // h0 == 0: ts > 31 bytes
+  if (o0 - 1u > 8u || ((h0 >> (o0 + 1u)) & 1u) == 0) return 0;
+  const uint32_t j0 = __funnelshift_r(h0, h1, o0 + 2u), j1 = h1 >> (o0 + 2u);   // from the jobId
+  if ((j0 & 0x7FFu) == 0x400u) {
+    c[0] = S + o0;
+    c[1] = S + o0 + 1u;
+    c[2] = S + o0 + 12u;
+    uint32_t r0 = __funnelshift_r(j0, j1, 11u), r1 = j1 >> 11;   // bits after c2
+    const uint32_t base = S + o0 + 13u;
 #pragma unroll
-  for (int k = 0; k < 6; k++) {
-    const bool l = h0 != 0;
-    const uint32_t t = l ? h0 : h1;
-    const uint32_t bit = lsb32(t);
-    c[k] = S + bit + (l ? 0u : 32u);
-    const uint32_t tc = t & (t - 1u);
-    h0 = l ? tc : h0;
-    h1 = l ? h1 : tc;
+    for (int k = 3; k < 5; k++) {
+      const bool l = r0 != 0;
+      const uint32_t t = l ? r0 : r1;
+      const uint32_t bit = lsb32(t);
+      c[k] = base + bit + (l ? 0u : 32u);                    // r1 holds bits 32.. of r
+      const uint32_t tc = t & (t - 1u);
+      r0 = l ? tc : r0;
+      r1 = l ? r1 : tc;
+    }
+    // eventType must be 1 char: the next comma (c5) sits at c4 + 2
+    c[5] = base + (r0 ? lsb32(r0) : 32u + lsb32(r1));
+    if (c[5] != c[4] + 2u) return 0;
+  } else {
+#pragma unroll
+    for (int k = 0; k < 6; k++) {
+      const bool l = h0 != 0;
+      const uint32_t t = l ? h0 : h1;
+      const uint32_t bit = lsb32(t);
+      c[k] = S + bit + (l ? 0u : 32u);
+      const uint32_t tc = t & (t - 1u);
+      h0 = l ? tc : h0;
+      h1 = l ? h1 : tc;
+    }
   }
+  // ---- tail: commas 6..11 = the 6 highest bits of the window [e-64, e).  Usual shape:
+  // cpu, ram, disk 8 chars and a 1-char constraint, i.e. commas exactly at e-29, e-20, e-11,
+  // e-2 in [e-30, e); then c7 = the next comma below and c6 = c7 - 2 (1-char category).
   const uint32_t T0 = kCmHaloL + tp;
+  if ((t1 >> 2) == 0x10080402u) {
+    c[8] = T0 + 35u;
+    c[9] = T0 + 44u;
+    const uint32_t l7 = t1 & 7u;
+    const uint32_t q7 = l7 ? 32u + msb32(l7) : msb32(t0);     // window bit of c7 (t0 != 0)
+    c[7] = T0 + q7;
+    // the comma before c7 must be at c7 - 2: bit q7-1 clear, bit q7-2 set
+    const uint32_t w2 = __funnelshift_rc(t0, t1, q7 - 2u) & 3u;   // window bits q7-2, q7-1
+    if (q7 < 2u || w2 != 1u) return 0;
+    c[6] = c[7] - 2u;
+  } else {
 #pragma unroll
-  for (int k = 11; k >= 6; k--) {
-    const bool h = t1 != 0;
-    const uint32_t t = h ? t1 : t0;
-    const uint32_t bit = msb32(t);
-    if (k < 10) c[k] = T0 + bit + (h ? 32u : 0u);
-    const uint32_t tc = t ^ (1u << bit);
-    t1 = h ? tc : t1;
-    t0 = h ? t0 : tc;
+    for (int k = 11; k >= 6; k--) {
+      const bool h = t1 != 0;
+      const uint32_t t = h ? t1 : t0;
+      const uint32_t bit = msb32(t);
+      if (k < 10) c[k] = T0 + bit + (h ? 32u : 0u);
+      const uint32_t tc = t ^ (1u << bit);
+      t1 = h ? tc : t1;
+      t0 = h ? t0 : tc;
+    }
   }
   return cm_fields(buf, S, c, r) ? 1 : 0;
 }

@@ -142,3 +142,35 @@ def test_xways_domain_and_high_key_space():
     compare_run("LR2S", product_run("LR2S", batches, num_xways=16), oracle_rows("LR2S", batches, num_xways=16))
     # with the default domain (10 xways) records with xway >= 10 are malformed
     compare_run("LR2S", product_run("LR2S", batches), oracle_rows("LR2S", batches))
+
+
+def _cm_line(ts="7", miss="", job="1234567890", task="12", mach="345", ev="1", user="Ab+/Zz09",
+             cat="2", prio="3", cpu="0.123456", ram="0.000001", disk="0.999999", cons="1"):
+    return ",".join([ts, miss, job, task, mach, ev, user, cat, prio, cpu, ram, disk, cons]).encode() + b"\n"
+
+
+def test_cm_field_shape_variants():
+    """Every field-width variant of the CM grammar (reading R1) around the kernel's fast-path
+    shapes (10-digit jobId, 8-char cpu/ram/disk, 1-char constraint): valid ones must be
+    aggregated, invalid ones dropped — exactly as the oracle decides."""
+    variants = [
+        {}, {"job": "1"}, {"job": "123456789"}, {"job": "12345678901"}, {"job": "1234567890123456789"},
+        {"job": "12345678901234567890"}, {"job": ""}, {"job": "12345x7890"}, {"ts": ""}, {"ts": "000000006"},
+        {"ts": "0000000006"}, {"ts": "1a"}, {"miss": "x"}, {"task": ""}, {"task": "ab,c"}, {"task": "x y"},
+        {"mach": ""}, {"mach": "12345678901234"}, {"ev": ""}, {"ev": "11"}, {"ev": "x"}, {"cat": ""},
+        {"cat": "12"}, {"cat": "z"}, {"prio": ""}, {"prio": "123"}, {"cpu": "0.12345"}, {"cpu": "0.1234567"},
+        {"cpu": "01234567"}, {"cpu": "0.12345x"}, {"ram": "1"}, {"ram": "0.1234567890"}, {"disk": ""},
+        {"disk": "0.1"}, {"cons": ""}, {"cons": "10"}, {"cons": "xyz"}, {"user": ""}, {"user": "a" * 120},
+        {"user": "a,b"}, {"ram": "0.12,3456"}, {"cons": "1,"},
+    ]
+    lines = []
+    for i, v in enumerate(variants):
+        for t in range(3):
+            d = dict(ts=str(5 + t), job=f"{1000000000 + 7 * i}", ev="1")
+            d.update(v)
+            lines.append(_cm_line(**d))
+    data = b"".join(lines)
+    batches = [[data]]
+    for q in ("CM2S", "CM1S"):
+        prod = product_run(q, batches)
+        compare_run(q, prod, oracle_rows(q, batches))
