@@ -12,7 +12,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liblmstream.so")
 
 if not os.path.exists(LIB_PATH):
-    raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2111_04289_b200.build` "
+    raise ImportError(f"{LIB_PATH} is missing: run `python paper_2111_04289_b200/build.py` "
                       "(the LMStream hot path has no CPU fallback)")
 _lib = C.CDLL(LIB_PATH)
 

@@ -3,7 +3,7 @@
   paper_2111_04289_b200/liblmstream.so   the product (C ABI in include/lmstream.h)
   lmsgen/liblmsgen.so                    the CUDA input generator (test / bench input only)
 
-Usage: python -m paper_2111_04289_b200.build [--force]
+Usage: python paper_2111_04289_b200/build.py [--force]   (or __graft_entry__.build())
 """
 from __future__ import annotations
 

@@ -9,6 +9,10 @@ if ROOT not in sys.path:
 
 
 def pytest_configure(config):
+    # Build (or refresh) the in-tree libraries first: nvcc cross-compiles without a GPU, and
+    # the CPU suite checks the library's exported symbols.
+    import __graft_entry__
+    __graft_entry__._build_module().build()
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run via gpurun")
     config.addinivalue_line("markers", "slow: long-running CPU test")
 
