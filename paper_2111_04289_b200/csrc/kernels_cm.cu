@@ -198,7 +198,7 @@ __device__ __forceinline__ bool cm_fields(const uint8_t* buf, uint32_t s, const 
 }
 
 // Exact byte-serial path: any line the fast path does not cover (short / long / malformed).
-__device__ bool cm_parse_serial(const uint8_t* buf, uint32_t s, uint32_t limit, CmRec& r) {
+__device__ __forceinline__ bool cm_parse_serial(const uint8_t* buf, uint32_t s, uint32_t limit, CmRec& r) {
   uint32_t c[10];
   uint32_t nc = 0;
   const uint32_t stop = min(limit, s + kCmMaxLine + 1);
@@ -248,15 +248,15 @@ __device__ __forceinline__ bool pop_lowest(uint32_t& s0, uint32_t& s1, uint32_t&
 }
 
 // Parse the record starting at mask bit sb whose '\n' is at mask bit e (e > sb).
-// Returns 1 valid, 0 malformed.  Fast path (64 <= L = e - sb <= 191): the comma count of
-// [sb, e) from a 192-bit window at sb (must be 12: 13 fields); commas 0..5 are the 6 lowest
-// bits of its first 64 bits, commas 6..11 the 6 highest bits of the 64-bit window ending at
-// e.  Anything else takes the exact byte-serial path.
+// Returns 1 valid, 0 malformed, 2 undecided (the caller runs the exact byte-serial path).
+// Mask path (64 <= L = e - sb <= 191): the comma count of [sb, e) from a 192-bit window at sb
+// (must be 12: 13 fields); commas 0..5 are the 6 lowest bits of its first 64 bits, commas
+// 6..11 the 6 highest bits of the 64-bit window ending at e.
 __device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e,
                                         uint32_t hi_bits, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
-  if (L - 64u > 127u) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  if (L - 64u > 127u) return 2;
   const uint32_t* w = cm32 + (sb >> 5);
   const uint32_t sh = sb & 31u;
   const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4], v5 = w[5], v6 = w[6];
@@ -272,7 +272,7 @@ __device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32
   const uint32_t* u = cm32 + (tp >> 5);
   const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
   uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
-  if (nh < 6u || __popc(t0) + __popc(t1) < 6u) return cm_parse_serial(buf, S, kCmHaloL + hi_bits, r) ? 1 : 0;
+  if (nh < 6u || __popc(t0) + __popc(t1) < 6u) return 2;
   uint32_t c[10];
   // ---- head: commas 0..5 = the 6 lowest bits of h1:h0.  c0 ends ts (1..9 digits), c1 = c0 + 1
   // (empty field 1): anything else is malformed.  Usual shape: a 10-digit jobId, so c2 =
@@ -338,6 +338,88 @@ __device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32
     }
   }
   return cm_fields(buf, S, c, r) ? 1 : 0;
+}
+
+// Bytes [p, p+8) of smem as two little-endian words (p arbitrary; reads 12 aligned bytes).
+__device__ __forceinline__ void load8(const uint8_t* buf, uint32_t p, uint32_t& d0, uint32_t& d1) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(buf + (p & ~3u));
+  const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], sh = (p & 3u) * 8u;
+  d0 = __funnelshift_r(w0, w1, sh);
+  d1 = __funnelshift_r(w1, w2, sh);
+}
+
+// Straight-line (branch-free) decode of a record of the USUAL shape: 64 <= L <= 191, exactly
+// 12 commas, ts of 1..8 digits, empty field 1, a 10-digit jobId, a 1-character eventType,
+// category (1 char) / priority / cpu, ram, disk (8 chars each) / constraint (1 char) at the
+// tail.  Returns true iff the record matches that shape AND is valid under reading R1 (then r
+// holds its fields); false means "not decided here": the caller re-parses the record with the
+// exact general path (cm_parse), so the fast path never needs to reject anything itself.
+// sb / e: mask bits of the record start and of its '\n'.  Every smem address is clamped into
+// the stage so that predicated-off garbage positions cannot fault.
+__device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e, CmRec& r) {
+  const uint32_t S = kCmHaloL + sb;
+  const uint32_t L = e - sb;
+  bool ok = L - 64u <= 127u;
+  // ---- exactly 12 commas in [sb, e) (13 fields)
+  const uint32_t* w = cm32 + (sb >> 5);
+  const uint32_t sh = sb & 31u;
+  const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4], v5 = w[5], v6 = w[6];
+  const uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
+  const uint32_t x2 = __funnelshift_r(v2, v3, sh) & low_bits(clamp32((int)L - 64));
+  const uint32_t x3 = __funnelshift_r(v3, v4, sh) & low_bits(clamp32((int)L - 96));
+  const uint32_t x4 = __funnelshift_r(v4, v5, sh) & low_bits(clamp32((int)L - 128));
+  const uint32_t x5 = __funnelshift_r(v5, v6, sh) & low_bits(clamp32((int)L - 160));
+  ok &= __popc(h0) + __popc(h1) + __popc(x2) + __popc(x3) + __popc(x4) + __popc(x5) == 12u;
+  // ---- head: c0 = sb + o0 ends ts (1..8 digits); c1 = c0 + 1 (empty field 1); c2 = c0 + 12
+  // (10-digit jobId); then taskIndex, machineId free-form: c4 = the 2nd comma after c2, and
+  // eventType is 1 character: the next comma (c5) is at c4 + 2.
+  const uint32_t o0 = lsb32(h0 | 0x80000000u);
+  ok &= o0 - 1u <= 7u;
+  const uint32_t jw = __funnelshift_r(h0, h1, o0 + 1u);           // bit 0 <-> c1
+  ok &= (jw & 0xFFFu) == 0x801u;
+  const uint32_t rr = __funnelshift_r(h0, h1, o0 + 13u);          // bits after c2
+  const uint32_t x = rr & (rr - 1u);                              // c3 cleared
+  const uint32_t a4 = lsb32(x | 0x80000000u);                     // c4 = c2 + 1 + a4
+  ok &= x != 0u && a4 <= 29u && ((x >> a4) & 7u) == 5u;
+  // ---- tail: window [e-64, e): commas exactly at e-29, e-20, e-11, e-2 within [e-30, e)
+  // (cpu, ram, disk 8 chars, constraint 1 char); c7 = the next comma below; c6 = c7 - 2.
+  const uint32_t tp = min(max(e, 64u) - 64u, (uint32_t)(kMaskBits - 64));
+  const uint32_t* u = cm32 + (tp >> 5);
+  const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
+  const uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
+  ok &= (t1 >> 2) == 0x10080402u;
+  const uint32_t l7 = t1 & 7u;
+  const uint32_t q7 = l7 ? 32u + msb32(l7) : msb32(t0 | 1u);       // window bit of c7
+  ok &= q7 >= 2u && (__funnelshift_rc(t0, t1, q7 - 2u) & 3u) == 1u;
+  // ---- fields
+  const uint32_t lim = kCmStage - 12u;
+  // ts: the 8 bytes ending at c0; the (8 - o0) bytes before the digits are replaced by '0'
+  uint32_t a0, a1;
+  load8(buf, min(S + o0 - 8u, lim), a0, a1);
+  const uint32_t pad = 64u - 8u * o0;                              // bits of padding
+  const uint32_t m0 = low_bits(clamp32((int)pad)), m1 = low_bits(clamp32((int)pad - 32));
+  a0 = (a0 & ~m0) | (0x30303030u & m0);
+  a1 = (a1 & ~m1) | (0x30303030u & m1);
+  ok &= (nondigit(a0) | nondigit(a1)) == 0u;
+  r.ts = swar4(a0) * 10000u + swar4(a1);
+  // jobId: 10 digits at c1 + 1 = S + o0 + 2
+  uint32_t d0, d1, d2;
+  load12(buf, min(S + o0 + 2u, lim), d0, d1, d2);
+  ok &= (nondigit(d0) | nondigit(d1) | (nondigit(d2) & 0x8080u)) == 0u;
+  const uint32_t hi8 = swar4(d0) * 10000u + swar4(d1);
+  const uint32_t lo2 = ((d2 & 0xFFu) - 48u) * 10u + (((d2 >> 8) & 0xFFu) - 48u);
+  r.job = (unsigned long long)hi8 * 100ull + lo2;
+  // eventType at c4 + 1 = S + o0 + 14 + a4; category at c6 + 1 = c7 - 1
+  r.event = (uint32_t)buf[min(S + o0 + 14u + a4, lim)] - 48u;
+  r.cat = (uint32_t)buf[min(kCmHaloL + tp + q7 - 1u, lim)] - 48u;
+  ok &= r.event <= 9u && r.cat <= 9u;
+  // cpu = D.DDDDDD at c8 + 1 = e - 28
+  uint32_t p0, p1;
+  load8(buf, min(kCmHaloL + e - 28u, lim), p0, p1);
+  ok &= ((p0 >> 8) & 0xFFu) == '.' && ((nondigit(p0) & 0x80800080u) | nondigit(p1)) == 0u;
+  const uint32_t f2 = (((p0 >> 16) & 0xFFu) - 48u) * 10u + (((p0 >> 24) & 0xFFu) - 48u);
+  r.cpu_m = ((p0 & 0xFFu) - 48u) * 1000000u + f2 * 10000u + swar4(p1);
+  return ok;
 }
 
 template <int KIND>
@@ -507,10 +589,11 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     have = have && prev + 1u < limit;
     // ---- Pass 3: decode my records; aggregate (one record per lane per round)
     while (true) {
-      CmRec r{0, 0, 0, 0, 0};
+      CmRec r;
       bool surv = false;
       const uint32_t b_cur = prev + 1u - cb;
       bool next = false;
+      uint32_t e = 0u;
       if (have) {
         cnt.n++;
         uint32_t bn = 0;
@@ -519,11 +602,22 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           inchunk = pop_lowest(n0, n1, n2, n3, bn);
           rem--;
         }
-        const uint32_t e = inchunk ? cb + bn : e_after;           // my record's newline
+        e = inchunk ? cb + bn : e_after;        // my record's newline (0xFFFF: none in reach)
         prev = e;
         next = inchunk && e + 1u < limit;
-        const int ok = e == 0xFFFFu ? (cm_parse_serial(buf, kCmHaloL + cb + b_cur, g.hi, r) ? 1 : 0)
-                                    : cm_parse(buf, cm32, cb + b_cur, e, hi_bits, r);
+      }
+      const uint32_t sb = have ? cb + b_cur : 0u;
+      // usual-shape records: branch-free fast path; anything else: the exact general path
+      const bool fast = cm_fast(buf, cm32, sb, e, r) & have;
+      const bool slow = have & !fast;
+      bool ok = fast;
+      if (__any_sync(0xffffffffu, slow)) {
+        if (slow) {
+          const int st = e == 0xFFFFu ? 2 : cm_parse(buf, cm32, sb, e, hi_bits, r);
+          ok = st == 2 ? cm_parse_serial(buf, kCmHaloL + sb, g.hi, r) : st != 0;
+        }
+      }
+      if (have) {
         if (!ok) cnt.bad++;
         else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;
         else {

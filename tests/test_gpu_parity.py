@@ -174,3 +174,37 @@ def test_cm_field_shape_variants():
     for q in ("CM2S", "CM1S"):
         prod = product_run(q, batches)
         compare_run(q, prod, oracle_rows(q, batches))
+
+
+def test_cm_fast_path_fuzz():
+    """Randomised lines around every boundary of the kernel's branch-free usual-shape decode
+    (ts of 1..10 digits, line lengths 40..250 B, taskIndex/machineId widths, user lengths) plus
+    single-byte mutations at and next to the separators the fast path reads off the masks:
+    every line must be aggregated or dropped exactly as the oracle decides."""
+    rng = random.Random(2111)
+    digits = lambda n: "".join(rng.choice("0123456789") for _ in range(n))
+    lines = []
+    for i in range(6000):
+        ts = str(5 + i * 8 // 6000).zfill(rng.randint(1, 10))     # widths 1..10, in-order seconds
+        d = dict(ts=ts, job=digits(10) if rng.random() < 0.85 else digits(rng.randint(1, 20)),
+                 task=digits(rng.randint(0, 5)), mach=digits(rng.randint(0, 11)),
+                 ev=str(rng.choice([1, 1, 1, 0, 4, 5])) if rng.random() < 0.95 else digits(rng.randint(0, 2)),
+                 user="".join(rng.choice("ABCdef+/019") for _ in range(rng.choice([0, 1, 5, 40, 70, 90, 150]))),
+                 cat=str(rng.randrange(4)) if rng.random() < 0.95 else digits(rng.randint(0, 2)),
+                 prio=digits(rng.randint(0, 3)),
+                 cpu="0." + digits(6) if rng.random() < 0.9 else digits(rng.randint(0, 9)),
+                 ram="0." + digits(6) if rng.random() < 0.9 else digits(rng.randint(0, 9)),
+                 disk="0." + digits(6), cons=str(rng.randrange(2)) if rng.random() < 0.95 else digits(2))
+        line = bytearray(_cm_line(**d))
+        if rng.random() < 0.25:            # mutate a byte at / next to a separator
+            seps = [k for k, c in enumerate(line) if c in b",."]
+            k = min(max(rng.choice(seps) + rng.choice([-1, 0, 1]), 0), len(line) - 2)
+            line[k] = rng.choice(b",.x05\n")
+        lines.append(bytes(line))
+    data = b"".join(lines)
+    batches = [[data[:len(data) // 2].rsplit(b"\n", 1)[0] + b"\n"]]
+    rest = data[len(batches[0][0]):]
+    batches.append([rest])
+    for q in ("CM2S", "CM1S"):
+        prod = product_run(q, batches)
+        compare_run(q, prod, oracle_rows(q, batches))
