@@ -45,18 +45,28 @@ static_assert(kPieces % 64 == 16, "4 piece pairs + a half row per lane");
 constexpr int kSurvCap = 64;                                 // per-warp survivor list
 constexpr int kSmemPad = 16;                                 // SWAR loads may read 12 B past a stage
 
-// Exact byte-equality flags of one 4-byte word (c < 0x80 per byte): bit 7 of byte k set iff
-// byte k == c.  Low 7 bits equal <=> ((w & 0x7F..) ^ c) + 0x7F.. leaves bit 7 clear, and the
-// byte's own bit 7 must be clear.
-__device__ __forceinline__ uint32_t eq_flags(uint32_t m7, uint32_t w, uint32_t c4) {
-  const uint32_t t = (m7 ^ c4) + 0x7F7F7F7Fu;
+// Pass-1 byte classification, balanced between the ALU pipe (LOP3, SHF: half rate on B200)
+// and the FMA pipe (VIADD / IMAD / IDP): per word and class one LOP3 (w & 0x7F..) ^ c, one add,
+// one LOP3 for the flags; per 16 B piece and class an IDP.4A chain and one IMAD + SHF.
+// Exact byte-equality flags: bit 7 of byte k set iff byte k == c (c < 0x80): the low 7 bits
+// equal <=> ((w & 0x7F..) ^ c) + 0x7F.. leaves bit 7 clear, and the byte's own bit 7 is clear.
+__device__ __forceinline__ uint32_t lop3_and_xor(uint32_t a, uint32_t b, uint32_t c) {   // (a & b) ^ c
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0x6A;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t eq_flags(uint32_t w, uint32_t k7f, uint32_t c4) {
+  const uint32_t t = lop3_and_xor(w, k7f, c4) + 0x7F7F7F7Fu;
   return ~(t | w) & 0x80808080u;
 }
-// 16-bit mask of a 16 B piece from four flag words (IDP.4A gathers bytes {0,0x80} -> bits).
-__device__ __forceinline__ uint32_t gather16(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3) {
-  const uint32_t lo = __dp4a(f1, 0x80402010u, __dp4a(f0, 0x08040201u, 0u));   // 128 * bits 0..7
+// 16-bit mask of a 16 B piece from four flag words: IDP.4A gathers bytes {0, 0x80} to
+// 128 * bits 0..7 per word pair; (hi * 256 + lo) >> 7 joins the halves.
+__device__ __forceinline__ uint32_t gather16(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3, uint32_t k256) {
+  const uint32_t lo = __dp4a(f1, 0x80402010u, __dp4a(f0, 0x08040201u, 0u));
   const uint32_t hi = __dp4a(f3, 0x80402010u, __dp4a(f2, 0x08040201u, 0u));
-  return (lo >> 7) | (hi << 1);
+  uint32_t x;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(hi), "r"(k256), "r"(lo));   // stays an IMAD
+  return x >> 7;
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
@@ -72,6 +82,7 @@ struct CmArgs {
   QueryDev q;
   SegTable segs;
   unsigned long long total_tiles;
+  uint32_t k7f, k256;                // 0x7F7F7F7F, 256: kernel arguments, so they stay in registers
 };
 
 struct TileGeom {
@@ -348,28 +359,45 @@ __device__ __forceinline__ void load8(const uint8_t* buf, uint32_t p, uint32_t& 
   d1 = __funnelshift_r(w1, w2, sh);
 }
 
-// Straight-line (branch-free) decode of a record of the USUAL shape: 64 <= L <= 191, exactly
+// SWAR digit helpers on d = x - 0x30303030 (x: 4 ASCII bytes, first character in the low byte).
+// dbad(d): bit 7 of some byte is set iff some byte of x is not an ASCII digit.  Proof: let k be
+// the lowest non-digit byte (no borrow reaches it); x_k < '0' wraps d_k to >= 0xD0, and
+// x_k > '9' gives d_k >= 0x0A, so d_k has bit 7 set or d_k + 0x76 does (the digit bytes below
+// k add at most 0x7F: no carry into byte k).  All digits: d_k <= 9, d_k + 0x76 <= 0x7F.
+__device__ __forceinline__ uint32_t dbad(uint32_t d) { return d | (d + 0x76767676u); }
+// value of 4 digit values (first = most significant): pairs 10*d0+d1, 10*d2+d3 land in bytes
+// 1 and 3 of d * 0xA01 (each <= 99: no carries), PRMT moves them to bytes 0 and 2, and
+// (p * (100 << 16 | 1)) >> 16 = 100 * pair0 + pair1.
+__device__ __forceinline__ uint32_t swar4d(uint32_t d) {
+  const uint32_t p = __byte_perm(d * 0xA01u, 0u, 0x4341u);
+  return (p * 0x640001u) >> 16;
+}
+
+// Straight-line (branch-free) decode of a record of the USUAL shape: 128 <= L <= 191, exactly
 // 12 commas, ts of 1..8 digits, empty field 1, a 10-digit jobId, a 1-character eventType,
-// category (1 char) / priority / cpu, ram, disk (8 chars each) / constraint (1 char) at the
-// tail.  Returns true iff the record matches that shape AND is valid under reading R1 (then r
-// holds its fields); false means "not decided here": the caller re-parses the record with the
-// exact general path (cm_parse), so the fast path never needs to reject anything itself.
-// sb / e: mask bits of the record start and of its '\n'.  Every smem address is clamped into
-// the stage so that predicated-off garbage positions cannot fault.
+// then (user free-form) a 1-character category, a 1..2-character priority and, at the tail,
+// cpu, ram, disk (8 characters each) and a 1-character constraint.  Returns true iff the
+// record has that shape AND is valid under reading R1 (then r holds its fields); false means
+// "not decided here": the caller re-parses the record with the exact general path (cm_parse),
+// so the fast path never rejects anything itself.  sb / e: mask bits of the record start and
+// of its '\n'.  Every smem address is clamped into the stage so that predicated-off garbage
+// positions cannot fault.
 __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
-  bool ok = L - 64u <= 127u;
-  // ---- exactly 12 commas in [sb, e) (13 fields)
+  bool ok = L - 128u <= 63u;
+  // ---- exactly 12 commas in [sb, e): head [sb, sb+64) + middle [sb+64, e-64) + tail [e-64, e)
   const uint32_t* w = cm32 + (sb >> 5);
   const uint32_t sh = sb & 31u;
-  const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4], v5 = w[5], v6 = w[6];
+  const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4];
   const uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
-  const uint32_t x2 = __funnelshift_r(v2, v3, sh) & low_bits(clamp32((int)L - 64));
-  const uint32_t x3 = __funnelshift_r(v3, v4, sh) & low_bits(clamp32((int)L - 96));
-  const uint32_t x4 = __funnelshift_r(v4, v5, sh) & low_bits(clamp32((int)L - 128));
-  const uint32_t x5 = __funnelshift_r(v5, v6, sh) & low_bits(clamp32((int)L - 160));
-  ok &= __popc(h0) + __popc(h1) + __popc(x2) + __popc(x3) + __popc(x4) + __popc(x5) == 12u;
+  const uint32_t m0 = __funnelshift_r(v2, v3, sh) & low_bits(min(L - 128u, 32u));
+  const uint32_t m1 = __funnelshift_r(v3, v4, sh) & low_bits(clamp32((int)L - 160));
+  const uint32_t tp = min(max(e, 64u) - 64u, (uint32_t)(kMaskBits - 64));
+  const uint32_t* u = cm32 + (tp >> 5);
+  const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
+  const uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
+  ok &= __popc(h0) + __popc(h1) + __popc(m0) + __popc(m1) + __popc(t0) + __popc(t1) == 12u;
   // ---- head: c0 = sb + o0 ends ts (1..8 digits); c1 = c0 + 1 (empty field 1); c2 = c0 + 12
   // (10-digit jobId); then taskIndex, machineId free-form: c4 = the 2nd comma after c2, and
   // eventType is 1 character: the next comma (c5) is at c4 + 2.
@@ -381,45 +409,46 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   const uint32_t x = rr & (rr - 1u);                              // c3 cleared
   const uint32_t a4 = lsb32(x | 0x80000000u);                     // c4 = c2 + 1 + a4
   ok &= x != 0u && a4 <= 29u && ((x >> a4) & 7u) == 5u;
-  // ---- tail: window [e-64, e): commas exactly at e-29, e-20, e-11, e-2 within [e-30, e)
-  // (cpu, ram, disk 8 chars, constraint 1 char); c7 = the next comma below; c6 = c7 - 2.
-  const uint32_t tp = min(max(e, 64u) - 64u, (uint32_t)(kMaskBits - 64));
-  const uint32_t* u = cm32 + (tp >> 5);
-  const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
-  const uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
+  // ---- tail, window [e-64, e): commas exactly at e-29, e-20, e-11, e-2 within [e-30, e)
+  // (cpu, ram, disk 8 chars, constraint 1 char); c7 (priority end) at e-31 or e-32 and
+  // c6 = c7 - 2 (1-char category): window bits 30..34 = 0b01010 or 0b00101.
   ok &= (t1 >> 2) == 0x10080402u;
-  const uint32_t l7 = t1 & 7u;
-  const uint32_t q7 = l7 ? 32u + msb32(l7) : msb32(t0 | 1u);       // window bit of c7
-  ok &= q7 >= 2u && (__funnelshift_rc(t0, t1, q7 - 2u) & 3u) == 1u;
-  // ---- fields
+  const uint32_t pc = __funnelshift_r(t0, t1, 30u) & 0x1Fu;
+  ok &= pc == 0x0Au || pc == 0x05u;
+  const uint32_t cat_at = kCmHaloL + e - (pc == 0x0Au ? 32u : 33u);  // c6 + 1
+  // ---- fields (digit checks accumulate into bad; bit 7 of a byte = not a digit)
   const uint32_t lim = kCmStage - 12u;
-  // ts: the 8 bytes ending at c0; the (8 - o0) bytes before the digits are replaced by '0'
+  // ts: the 8 bytes ending at c0; the (8 - o0) bytes before the digits become '0'
   uint32_t a0, a1;
   load8(buf, min(S + o0 - 8u, lim), a0, a1);
-  const uint32_t pad = 64u - 8u * o0;                              // bits of padding
-  const uint32_t m0 = low_bits(clamp32((int)pad)), m1 = low_bits(clamp32((int)pad - 32));
-  a0 = (a0 & ~m0) | (0x30303030u & m0);
-  a1 = (a1 & ~m1) | (0x30303030u & m1);
-  ok &= (nondigit(a0) | nondigit(a1)) == 0u;
-  r.ts = swar4(a0) * 10000u + swar4(a1);
+  const unsigned long long pm = (~0ull >> (min(max(8u * o0, 8u), 64u) - 1u)) >> 1;   // ~0 >> 8*o0
+  const uint32_t pm0 = (uint32_t)pm, pm1 = (uint32_t)(pm >> 32);
+  const uint32_t da0 = ((a0 & ~pm0) | (0x30303030u & pm0)) - 0x30303030u;
+  const uint32_t da1 = ((a1 & ~pm1) | (0x30303030u & pm1)) - 0x30303030u;
+  uint32_t bad = dbad(da0) | dbad(da1);
+  r.ts = swar4d(da0) * 10000u + swar4d(da1);
   // jobId: 10 digits at c1 + 1 = S + o0 + 2
   uint32_t d0, d1, d2;
   load12(buf, min(S + o0 + 2u, lim), d0, d1, d2);
-  ok &= (nondigit(d0) | nondigit(d1) | (nondigit(d2) & 0x8080u)) == 0u;
-  const uint32_t hi8 = swar4(d0) * 10000u + swar4(d1);
-  const uint32_t lo2 = ((d2 & 0xFFu) - 48u) * 10u + (((d2 >> 8) & 0xFFu) - 48u);
-  r.job = (unsigned long long)hi8 * 100ull + lo2;
-  // eventType at c4 + 1 = S + o0 + 14 + a4; category at c6 + 1 = c7 - 1
+  d0 -= 0x30303030u;
+  d1 -= 0x30303030u;
+  d2 -= 0x30303030u;
+  bad |= dbad(d0) | dbad(d1) | (dbad(d2) & 0x8080u);
+  const uint32_t lo2 = __byte_perm(d2 * 0xA01u, 0u, 0x4441u);     // 10 * d2_0 + d2_1
+  r.job = (unsigned long long)(swar4d(d0) * 10000u + swar4d(d1)) * 100ull + lo2;
+  // eventType at c4 + 1 = S + o0 + 14 + a4; category at c6 + 1
   r.event = (uint32_t)buf[min(S + o0 + 14u + a4, lim)] - 48u;
-  r.cat = (uint32_t)buf[min(kCmHaloL + tp + q7 - 1u, lim)] - 48u;
+  r.cat = (uint32_t)buf[min(cat_at, lim)] - 48u;
   ok &= r.event <= 9u && r.cat <= 9u;
-  // cpu = D.DDDDDD at c8 + 1 = e - 28
+  // cpu = D.DDDDDD at c8 + 1 = e - 28: the '.' is swapped for '0' for the digit check and
+  // SWAR value (D0DD DDDD), and the integer digit's weight is fixed up (10^7 -> 10^6)
   uint32_t p0, p1;
   load8(buf, min(kCmHaloL + e - 28u, lim), p0, p1);
-  ok &= ((p0 >> 8) & 0xFFu) == '.' && ((nondigit(p0) & 0x80800080u) | nondigit(p1)) == 0u;
-  const uint32_t f2 = (((p0 >> 16) & 0xFFu) - 48u) * 10u + (((p0 >> 24) & 0xFFu) - 48u);
-  r.cpu_m = ((p0 & 0xFFu) - 48u) * 1000000u + f2 * 10000u + swar4(p1);
-  return ok;
+  ok &= ((p0 >> 8) & 0xFFu) == '.';
+  const uint32_t dp0 = (p0 ^ 0x1E00u) - 0x30303030u, dp1 = p1 - 0x30303030u;
+  bad |= dbad(dp0) | dbad(dp1);
+  r.cpu_m = swar4d(dp0) * 10000u + swar4d(dp1) - 9000000u * (dp0 & 0xFFu);
+  return ok && (bad & 0x80808080u) == 0u;
 }
 
 template <int KIND>
@@ -470,6 +499,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   }
 
   const unsigned long long wm_prev = q.state->wm_prev;
+  const uint32_t k7f = a.k7f, k256 = a.k256;                    // runtime constants (see eq_flags)
   CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
   uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
@@ -512,11 +542,10 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const uint32_t buf_s = smem_addr(buf) + kCmHaloL;
     auto piece = [&](int p, uint32_t& nl, uint32_t& cm) {
       const uint4 v = lds128(buf_s + 16 * p);
-      const uint32_t m0 = v.x & 0x7F7F7F7Fu, m1 = v.y & 0x7F7F7F7Fu, m2 = v.z & 0x7F7F7F7Fu, m3 = v.w & 0x7F7F7F7Fu;
-      nl = gather16(eq_flags(m0, v.x, 0x0A0A0A0Au), eq_flags(m1, v.y, 0x0A0A0A0Au),
-                    eq_flags(m2, v.z, 0x0A0A0A0Au), eq_flags(m3, v.w, 0x0A0A0A0Au));
-      cm = gather16(eq_flags(m0, v.x, 0x2C2C2C2Cu), eq_flags(m1, v.y, 0x2C2C2C2Cu),
-                    eq_flags(m2, v.z, 0x2C2C2C2Cu), eq_flags(m3, v.w, 0x2C2C2C2Cu));
+      nl = gather16(eq_flags(v.x, k7f, 0x0A0A0A0Au), eq_flags(v.y, k7f, 0x0A0A0A0Au),
+                    eq_flags(v.z, k7f, 0x0A0A0A0Au), eq_flags(v.w, k7f, 0x0A0A0A0Au), k256);
+      cm = gather16(eq_flags(v.x, k7f, 0x2C2C2C2Cu), eq_flags(v.y, k7f, 0x2C2C2C2Cu),
+                    eq_flags(v.z, k7f, 0x2C2C2C2Cu), eq_flags(v.w, k7f, 0x2C2C2C2Cu), k256);
     };
     // piece p's 16 bits live at byte offset 2p of the mask arrays
 #pragma unroll
@@ -728,6 +757,8 @@ cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   a.q = q;
   a.segs = segs;
   a.total_tiles = segs.tile_prefix[segs.n];
+  a.k7f = 0x7F7F7F7Fu;
+  a.k256 = 256u;
   if (a.total_tiles == 0) return cudaSuccess;
   const size_t smem = (size_t)kWarps * kCmStages * kCmStage + kSmemPad;
   const int grid = (int)q.n_agg_ctas;
