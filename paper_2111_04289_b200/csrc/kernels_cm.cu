@@ -59,19 +59,41 @@ __device__ __forceinline__ uint32_t eq_flags(uint32_t w, uint32_t k7f, uint32_t 
   const uint32_t t = lop3_and_xor(w, k7f, c4) + 0x7F7F7F7Fu;
   return ~(t | w) & 0x80808080u;
 }
-// 16-bit mask of a 16 B piece from four flag words: IDP.4A gathers bytes {0, 0x80} to
-// 128 * bits 0..7 per word pair; (hi * 256 + lo) >> 7 joins the halves.
-__device__ __forceinline__ uint32_t gather16(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3, uint32_t k256) {
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {   // a * b + c, kept an IMAD
+  uint32_t x;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(a), "r"(b), "r"(c));
+  return x;
+}
+// 128 * (16-bit mask) of a 16 B piece from four flag words: IDP.4A gathers bytes {0, 0x80}
+// to 128 * bits 0..7 per word pair, hi * 256 + lo joins the halves.
+__device__ __forceinline__ uint32_t gather16x128(uint32_t f0, uint32_t f1, uint32_t f2, uint32_t f3, uint32_t k256) {
   const uint32_t lo = __dp4a(f1, 0x80402010u, __dp4a(f0, 0x08040201u, 0u));
   const uint32_t hi = __dp4a(f3, 0x80402010u, __dp4a(f2, 0x08040201u, 0u));
-  uint32_t x;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(x) : "r"(hi), "r"(k256), "r"(lo));   // stays an IMAD
-  return x >> 7;
+  return imad(hi, k256, lo);
+}
+__device__ __forceinline__ uint32_t sel(bool c, uint32_t a, uint32_t b) {   // c ? a : b, never a branch
+  uint32_t d;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+      : "=r"(d) : "r"((uint32_t)c), "r"(a), "r"(b));
+  return d;
+}
+// first set bit of a 128-bit chunk mask (chunk base cb), 0xFFFF if none (branch-free)
+__device__ __forceinline__ uint32_t first_bit128(uint32_t m0, uint32_t m1, uint32_t m2, uint32_t m3, uint32_t cb) {
+  const uint32_t a = sel(m0 != 0u, m0, m1), ka = sel(m0 != 0u, 0u, 32u);
+  const uint32_t b = sel(m2 != 0u, m2, m3), kb = sel(m2 != 0u, 64u, 96u);
+  const bool lo = (m0 | m1) != 0u;
+  const uint32_t w = sel(lo, a, b), k = sel(lo, ka, kb);
+  return sel(w != 0u, cb + k + (uint32_t)(__ffs(w) - 1), 0xFFFFu);
 }
 
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
@@ -82,7 +104,7 @@ struct CmArgs {
   QueryDev q;
   SegTable segs;
   unsigned long long total_tiles;
-  uint32_t k7f, k256;                // 0x7F7F7F7F, 256: kernel arguments, so they stay in registers
+  uint32_t k7f, k256, k512;          // 0x7F7F7F7F, 256, 512: kernel arguments, so they stay in registers
 };
 
 struct TileGeom {
@@ -90,6 +112,7 @@ struct TileGeom {
   unsigned long long off;            // tile starts at seg + off
   uint32_t lo, hi;                   // valid smem bytes [lo, hi) (relative to stage start)
   uint32_t payload;                  // tile payload bytes (<= kCmTile)
+  bool cont;                         // the next tile continues this segment (its first 256 B = our halo)
 };
 
 // A warp's walk over its contiguous tile range: the current tile's segment and offset,
@@ -117,6 +140,7 @@ struct TileIter {
     g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
     g.lo = off == 0 ? kCmHaloL : 0;
     g.hi = kCmHaloL + (uint32_t)(rem < (unsigned long long)kCmWin ? rem : kCmWin);
+    g.cont = rem > (unsigned long long)kCmTile;
     return g;
   }
 };
@@ -459,7 +483,6 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   __shared__ unsigned long long slot_tag[2];
   // per-warp '\n' / ',' masks of the warp's current window (+ zero words for reads past it)
   __shared__ __align__(16) uint32_t nlm[kWarps][kMaskW32 + 8], cmm[kWarps][kMaskW32 + 8];
-  __shared__ uint16_t fnl_s[kWarps][kChunks + 4];              // first newline of each chunk
   // CM2: per-warp survivor lists; CM1: per-warp accumulators [warp][slot][cat]
   __shared__ unsigned long long sv_job[kCM2 ? kWarps : 1][kSurvCap];
   __shared__ uint32_t sv_m[kCM2 ? kWarps : 1][kSurvCap], sv_p[kCM2 ? kWarps : 1][kSurvCap];
@@ -474,7 +497,6 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   uint8_t* const wsmem = smem + warp * (kCmStages * kCmStage);
   uint32_t* const nl32 = nlm[warp];
   uint32_t* const cm32 = cmm[warp];
-  uint16_t* const fnl = fnl_s[warp];
 
   if (!kCM2)
     for (int i = tid; i < kWarps * 20; i += blockDim.x) {
@@ -483,7 +505,6 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     }
   if (tid < 2) slot_tag[tid] = kEmpty64;
   if (lane < 8) { nl32[kMaskW32 + lane] = 0; cm32[kMaskW32 + lane] = 0; }   // reads past the end
-  if (lane < 2) fnl[kChunks + 2 + lane] = 0xFFFFu;                        // no chunk beyond
   if (lane == 0) {
     for (int s = 0; s < kCmStages; s++) mbar_init(&full[warp][s], 1);
     mbar_fence_init();
@@ -499,8 +520,9 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   }
 
   const unsigned long long wm_prev = q.state->wm_prev;
-  const uint32_t k7f = a.k7f, k256 = a.k256;                    // runtime constants (see eq_flags)
-  CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
+  const uint32_t k7f = a.k7f, k256 = a.k256, k512 = a.k512;    // runtime constants (see eq_flags)
+  const uint32_t wm32 = (uint32_t)min(wm_prev, 0xFFFFFFFFull);  // late iff ts + 1 < wm_prev (ts < 1e9)
+  uint32_t n_rec = 0, n_bad = 0, n_late = 0, n_ovf = 0, ts_min = kEmpty32, ts_max1 = 0;
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
   uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
   const uint32_t nl_s = smem_addr(nl32), cm_s = smem_addr(cm32);
@@ -513,7 +535,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       const uint32_t pp = sv_p[kCM2 ? warp : 0][lane];
       if (pp != c_pane) { c_pane = pp; c_gslot = claim_slot(q, pp); }
       const uint32_t idx = c_gslot != kFail32 ? dict_get(q.dict, sv_job[kCM2 ? warp : 0][lane], q.state) : kEmpty32;
-      if (idx == kEmpty32) cnt.overflow++;
+      if (idx == kEmpty32) n_ovf++;
       else {
         const size_t gi = (size_t)c_gslot * q.K + idx;
         atomicAdd(&q.acc_sum[gi], (unsigned long long)sv_m[kCM2 ? warp : 0][lane]);
@@ -523,13 +545,16 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     __syncwarp();
   };
 
+  bool fresh = true;              // window bits [0, 256) not inherited from the previous tile
+  uint32_t carry_nl = 0;          // the previous tile's last payload byte is a '\n' (when !fresh)
   for (uint32_t it = 0; it < ntiles; it++) {
     const int s = (int)(it % kCmStages);
     const uint32_t ph = (it / kCmStages) & 1u;
     uint8_t* buf = wsmem + s * kCmStage;
     const TileGeom g = cur.geom();
     cur.next(a.segs);
-    mbar_wait(&full[warp][s], ph);
+    if (lane == 0) mbar_wait(&full[warp][s], ph);
+    __syncwarp();
     {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
       const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
       if (bulk_end < g.hi) {
@@ -538,34 +563,27 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
     }
     const uint32_t hi_bits = g.hi - kCmHaloL;                  // mask bits beyond are invalid
-    // ---- Pass 1: exact '\n' / ',' masks of every 16 B piece (round robin: conflict-free LDS.128)
+    // ---- Pass 1: exact '\n' / ',' masks, one 32-bit mask word (32 B) per lane per step.
+    // Window bits [0, 256) are the previous tile's halo masks when the tile continues the
+    // segment (carried below), so a tile classifies 4096 new bytes: 4 words per lane.
     const uint32_t buf_s = smem_addr(buf) + kCmHaloL;
-    auto piece = [&](int p, uint32_t& nl, uint32_t& cm) {
-      const uint4 v = lds128(buf_s + 16 * p);
-      nl = gather16(eq_flags(v.x, k7f, 0x0A0A0A0Au), eq_flags(v.y, k7f, 0x0A0A0A0Au),
-                    eq_flags(v.z, k7f, 0x0A0A0A0Au), eq_flags(v.w, k7f, 0x0A0A0A0Au), k256);
-      cm = gather16(eq_flags(v.x, k7f, 0x2C2C2C2Cu), eq_flags(v.y, k7f, 0x2C2C2C2Cu),
-                    eq_flags(v.z, k7f, 0x2C2C2C2Cu), eq_flags(v.w, k7f, 0x2C2C2C2Cu), k256);
+    auto mword = [&](int wi) {
+      const uint4 va = lds128(buf_s + 32 * wi), vb = lds128(buf_s + 32 * wi + 16);
+      const uint32_t na = gather16x128(eq_flags(va.x, k7f, 0x0A0A0A0Au), eq_flags(va.y, k7f, 0x0A0A0A0Au),
+                                       eq_flags(va.z, k7f, 0x0A0A0A0Au), eq_flags(va.w, k7f, 0x0A0A0A0Au), k256);
+      const uint32_t nb = gather16x128(eq_flags(vb.x, k7f, 0x0A0A0A0Au), eq_flags(vb.y, k7f, 0x0A0A0A0Au),
+                                       eq_flags(vb.z, k7f, 0x0A0A0A0Au), eq_flags(vb.w, k7f, 0x0A0A0A0Au), k256);
+      const uint32_t ca = gather16x128(eq_flags(va.x, k7f, 0x2C2C2C2Cu), eq_flags(va.y, k7f, 0x2C2C2C2Cu),
+                                       eq_flags(va.z, k7f, 0x2C2C2C2Cu), eq_flags(va.w, k7f, 0x2C2C2C2Cu), k256);
+      const uint32_t cb2 = gather16x128(eq_flags(vb.x, k7f, 0x2C2C2C2Cu), eq_flags(vb.y, k7f, 0x2C2C2C2Cu),
+                                        eq_flags(vb.z, k7f, 0x2C2C2C2Cu), eq_flags(vb.w, k7f, 0x2C2C2C2Cu), k256);
+      sts32(nl_s + 4 * wi, imad(nb, k512, na >> 7));       // (128 mb) * 512 = mb << 16
+      sts32(cm_s + 4 * wi, imad(cb2, k512, ca >> 7));
     };
-    // piece p's 16 bits live at byte offset 2p of the mask arrays
 #pragma unroll
-    for (int k = 0; k < kPieces - 32; k += 64) {
-      const int p0 = lane + k, p1 = p0 + 32;
-      uint32_t n0, c0, n1, c1;
-      piece(p0, n0, c0);
-      piece(p1, n1, c1);
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)n0));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p1), "h"((uint16_t)n1));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p0), "h"((uint16_t)c0));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p1), "h"((uint16_t)c1));
-    }
-    if (lane < kPieces % 64) {                  // the last 16 pieces (halo end)
-      const int p0 = lane + (kPieces / 64) * 64;
-      uint32_t n0, c0;
-      piece(p0, n0, c0);
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(nl_s + 2 * p0), "h"((uint16_t)n0));
-      asm volatile("st.shared.u16 [%0], %1;" ::"r"(cm_s + 2 * p0), "h"((uint16_t)c0));
-    }
+    for (int k = 0; k < 4; k++) mword(8 + lane + 32 * k);
+    fresh = fresh || g.lo != 0;
+    if (fresh && lane < 8) mword(lane);
     __syncwarp();
     if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (warp-uniform): clear stale bits
       for (uint32_t wi = lane; wi < (uint32_t)kMaskW32; wi += 32) {
@@ -575,67 +593,39 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
       __syncwarp();
     }
-    // ---- Pass 2: lane l owns payload chunk l (128 B, mask words 4l..4l+3); fnl[] = first
-    // newline of each chunk (+ the 2 halo chunks).  A record starts after a '\n' (or at a
-    // segment start) and belongs to the chunk holding its first byte.
+    // ---- Pass 2: lane l owns payload chunk l (128 B, mask words 4l..4l+3).  A record starts
+    // after a '\n' (or at a segment start) and belongs to the chunk holding its first byte;
+    // its '\n' is the first newline of chunk l+1, else of chunk l+2 (else the line is longer
+    // than 256 B: serial path).  Chunks 32, 33 are the right halo.
     const uint32_t cb = lane * kChunk;
     const uint4 nw = lds128(nl_s + 16 * lane);
-    const uint32_t prev_w = __shfl_up_sync(0xffffffffu, nw.w, 1);   // chunk l-1's last word
-    const bool prev_nl = lane == 0 ? ((g.lo == kCmHaloL) || buf[kCmHaloL - 1] == '\n')
-                                   : (prev_w >> 31) != 0;
-    uint32_t f_mine;                            // first newline of my chunk (0xFFFF: none)
-    {
-      const uint32_t w = nw.x ? nw.x : (nw.y ? nw.y : (nw.z ? nw.z : nw.w));
-      const uint32_t k = nw.x ? 0u : (nw.y ? 32u : (nw.z ? 64u : 96u));
-      f_mine = w ? cb + k + lsb32(w) : 0xFFFFu;
-      fnl[lane] = (uint16_t)f_mine;
-      if (lane < 2) {                           // halo chunks kChunks, kChunks + 1
-        const uint32_t hb = (kChunks + lane) * kChunk;
-        const uint4 hw = lds128(nl_s + hb / 8);
-        const uint32_t w2 = hw.x ? hw.x : (hw.y ? hw.y : (hw.z ? hw.z : hw.w));
-        const uint32_t k2 = hw.x ? 0u : (hw.y ? 32u : (hw.z ? 64u : 96u));
-        fnl[kChunks + lane] = w2 ? (uint16_t)(hb + k2 + lsb32(w2)) : (uint16_t)0xFFFFu;
-      }
-    }
-    __syncwarp();      // fnl[] complete
-    // '\n' of the last record starting in my chunk: first newline of chunk l+1, else l+2
-    // (else the line is > 256 B: serial path)
-    const uint32_t e_after = fnl[lane + 1] != 0xFFFFu ? (uint32_t)fnl[lane + 1] : (uint32_t)fnl[lane + 2];
-    const uint32_t limit = min(cb + (uint32_t)kChunk, g.payload);   // starts must lie below
-    uint32_t n0 = nw.x, n1 = nw.y, n2 = nw.z, n3 = nw.w;             // my unconsumed newlines
-    uint32_t rem = __popc(n0) + __popc(n1) + __popc(n2) + __popc(n3);
-    uint32_t prev = cb - 1u;                    // '\n' before the next record (cb - 1: wraps at 0)
-    bool have = prev_nl;
-    if (!have && rem) {                         // first record starts after my first newline
-      prev = f_mine;
-      have = true;
-      rem--;
-      if (rem) {                                // (short lines only) drop it from the words
-        uint32_t b0;
-        pop_lowest(n0, n1, n2, n3, b0);
-      }
-    }
-    have = have && prev + 1u < limit;
+    const uint4 nx = lds128(nl_s + 16 * (lane + 2));
+    const uint32_t f_mine = first_bit128(nw.x, nw.y, nw.z, nw.w, cb);           // my first '\n'
+    const uint32_t f2 = first_bit128(nx.x, nx.y, nx.z, nx.w, cb + 2 * kChunk);  // chunk l+2's
+    const uint32_t f1s = __shfl_down_sync(0xffffffffu, f_mine, 1);
+    const uint32_t f32 = __shfl_sync(0xffffffffu, f2, 30);      // chunk 32
+    const uint32_t f1 = sel(lane == 31, f32, f1s);
+    const uint32_t e_after = sel(f1 != 0xFFFFu, f1, f2);       // first '\n' past my chunk
+    // Records are owned by the '\n' before them: lane l takes the record after each '\n' of
+    // its chunk (if it starts inside the payload); lane 0 also takes the record at payload byte
+    // 0 when the tile starts a segment or the byte before it is a '\n'.
+    const bool start0 = lane == 0 && (g.lo != 0 || (fresh ? buf[kCmHaloL - 1] == '\n' : carry_nl != 0));
+    carry_nl = __shfl_sync(0xffffffffu, nw.w, 31) >> 31;       // last payload byte, for the next tile
+    const uint32_t pay = g.payload;
+    uint32_t n0 = nw.x, n1 = nw.y, n2 = nw.z, n3 = nw.w;             // unconsumed newlines (generic lanes)
+    const uint32_t cnt_nl = __popc(n0) + __popc(n1) + __popc(n2) + __popc(n3);
+    // round 0 serves the usual lane: at most one '\n' in the chunk, no record at byte 0 (records
+    // are >= 130 B > a chunk); every other lane walks its records in the generic rounds 1, 2, ...
+    const bool simple = cnt_nl <= 1u && !start0;
+    bool have = simple && cnt_nl == 1u && f_mine + 1u < pay;
+    uint32_t sb = f_mine + 1u, e = e_after;
+    bool more = !simple, pend0 = start0;
     // ---- Pass 3: decode my records; aggregate (one record per lane per round)
     while (true) {
       CmRec r;
       bool surv = false;
-      const uint32_t b_cur = prev + 1u - cb;
-      bool next = false;
-      uint32_t e = 0u;
-      if (have) {
-        cnt.n++;
-        uint32_t bn = 0;
-        bool inchunk = false;
-        if (rem) {                              // another newline in my chunk (short lines)
-          inchunk = pop_lowest(n0, n1, n2, n3, bn);
-          rem--;
-        }
-        e = inchunk ? cb + bn : e_after;        // my record's newline (0xFFFF: none in reach)
-        prev = e;
-        next = inchunk && e + 1u < limit;
-      }
-      const uint32_t sb = have ? cb + b_cur : 0u;
+      n_rec += have ? 1u : 0u;
+      sb = sel(have, sb, 0u);
       // usual-shape records: branch-free fast path; anything else: the exact general path
       const bool fast = cm_fast(buf, cm32, sb, e, r) & have;
       const bool slow = have & !fast;
@@ -647,15 +637,14 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
         }
       }
       if (have) {
-        if (!ok) cnt.bad++;
-        else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;
+        if (!ok) n_bad++;
+        else if (r.ts + 1u < wm32) n_late++;
         else {
-          cnt.ts_min = min(cnt.ts_min, r.ts);
-          cnt.ts_max1 = max(cnt.ts_max1, r.ts + 1u);
+          ts_min = min(ts_min, r.ts);
+          ts_max1 = max(ts_max1, r.ts + 1u);
           surv = kCM2 ? (r.event == 1u) : true;                   // WHERE (eventType == 1)
         }
       }
-      have = next;
       if (surv && r.ts - pc_lo >= q.S) {         // pane = floor(ts / S), cached per thread
         pc_p = pane_of(r.ts, q.S, q.div_magic);
         pc_lo = pc_p * q.S;
@@ -694,7 +683,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           const uint32_t sm = __reduce_add_sync(0xffffffffu, me ? r.cpu_m : 0u);   // < 32 * 1e7
           if (lane == leader) {
             if (lp != c_pane) { c_pane = lp; local_slot(slot_tag, q, lp, c_slot, c_gslot); }
-            if (c_gslot == kFail32) cnt.overflow += __popc(mm);
+            if (c_gslot == kFail32) n_ovf += __popc(mm);
             else if (c_slot < 2) {
               w_sum[warp][c_slot][lc] += sm;
               w_cnt[warp][c_slot][lc] += __popc(mm);
@@ -709,9 +698,33 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           __syncwarp();   // order the leader's smem accumulator update before the next leader's
         }
       }
-      if (!__any_sync(0xffffffffu, have)) break;   // warp-local rounds
+      if (!__any_sync(0xffffffffu, more)) break;   // warp-local rounds
+      // next record of a generic lane: at byte 0 (lane 0), then after each '\n' of the chunk;
+      // it ends at the next '\n' of the chunk, else at the first one past the chunk
+      have = false;
+      if (more) {
+        if (pend0) {
+          pend0 = false;
+          sb = 0u;
+          have = pay != 0u;
+        } else {
+          uint32_t bn;
+          if (pop_lowest(n0, n1, n2, n3, bn)) {
+            sb = cb + bn + 1u;
+            have = sb < pay;
+          }
+        }
+        const uint32_t nn = first_bit128(n0, n1, n2, n3, cb);
+        e = sel(nn != 0xFFFFu, nn, e_after);
+        more = pend0 || (n0 | n1 | n2 | n3) != 0u;
+      }
     }
     __syncwarp();      // stage s and the masks consumed by every lane
+    fresh = !g.cont;
+    if (g.cont && lane < 8) {                   // halo masks = the next tile's window bits [0, 256)
+      sts32(nl_s + 4 * lane, lds32(nl_s + 4 * (kChunks * 4 + lane)));
+      sts32(cm_s + 4 * lane, lds32(cm_s + 4 * (kChunks * 4 + lane)));
+    }
     if (it + kCmStages < ntiles) {
       if (lane == 0) cm_issue(iss.geom(), buf, &full[warp][s]);
       iss.next(a.segs);
@@ -736,7 +749,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
     }
   }
-  flush_counters(cnt, q.state);
+  flush_counters(CtaCounters{n_rec, n_bad, n_late, n_ovf, ts_min, ts_max1}, q.state);
 }
 
 }  // namespace
@@ -759,6 +772,7 @@ cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   a.total_tiles = segs.tile_prefix[segs.n];
   a.k7f = 0x7F7F7F7Fu;
   a.k256 = 256u;
+  a.k512 = 512u;
   if (a.total_tiles == 0) return cudaSuccess;
   const size_t smem = (size_t)kWarps * kCmStages * kCmStage + kSmemPad;
   const int grid = (int)q.n_agg_ctas;
