@@ -116,26 +116,44 @@ struct TileGeom {
 };
 
 // A warp's walk over its contiguous tile range: the current tile's segment and offset,
-// advanced one tile at a time (the segment changes only at segment ends).
+// advanced one tile at a time (the segment changes only at segment ends).  j = tile index in
+// the segment; tiles 1..jfull are FULL (left halo, 4096 B payload, whole right halo), the
+// common case, whose geometry is constant.
 struct TileIter {
   const uint8_t* seg;
   unsigned long long off, nbytes;      // tile start within the segment, segment size
   int si;
+  uint32_t j, jend, jfull;             // tile index in the segment, segment tiles, last full tile
+  __device__ __forceinline__ void seg_init(const SegTable& s) {
+    seg = s.s[si].ptr;
+    nbytes = s.s[si].nbytes;
+    jend = (uint32_t)(s.tile_prefix[si + 1] - s.tile_prefix[si]);
+    jfull = nbytes >= (unsigned long long)kCmWin ? (uint32_t)((nbytes - kCmWin) / kCmTile) : 0u;
+  }
   __device__ __forceinline__ void init(const SegTable& s, unsigned long long tile) {
     si = 0;
     while (si + 1 < s.n && tile >= s.tile_prefix[si + 1]) si++;
-    seg = s.s[si].ptr;
-    nbytes = s.s[si].nbytes;
-    off = (tile - s.tile_prefix[si]) * (unsigned long long)kCmTile;
+    seg_init(s);
+    j = (uint32_t)(tile - s.tile_prefix[si]);
+    off = (unsigned long long)j * kCmTile;
   }
   __device__ __forceinline__ void next(const SegTable& s) {
     off += kCmTile;
-    if (off >= nbytes && si + 1 < s.n) { si++; seg = s.s[si].ptr; nbytes = s.s[si].nbytes; off = 0; }
+    j++;
+    while (j >= jend && si + 1 < s.n) { si++; seg_init(s); off = 0; j = 0; }
   }
+  __device__ __forceinline__ bool full() const { return j - 1u < jfull; }
   __device__ __forceinline__ TileGeom geom() const {
     TileGeom g;
     g.seg = seg;
     g.off = off;
+    if (full()) {
+      g.payload = kCmTile;
+      g.lo = 0;
+      g.hi = kCmStage;
+      g.cont = true;
+      return g;
+    }
     const unsigned long long rem = nbytes - off;
     g.payload = (uint32_t)(rem < (unsigned long long)kCmTile ? rem : kCmTile);
     g.lo = off == 0 ? kCmHaloL : 0;
@@ -636,14 +654,13 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           ok = st == 2 ? cm_parse_serial(buf, kCmHaloL + sb, g.hi, r) : st != 0;
         }
       }
-      if (have) {
-        if (!ok) n_bad++;
-        else if (r.ts + 1u < wm32) n_late++;
-        else {
-          ts_min = min(ts_min, r.ts);
-          ts_max1 = max(ts_max1, r.ts + 1u);
-          surv = kCM2 ? (r.event == 1u) : true;                   // WHERE (eventType == 1)
-        }
+      {   // drop malformed (counted) and late (ts < W_prev, counted) records
+        const bool good = have & ok, late = r.ts + 1u < wm32, kept = good & !late;
+        n_bad += (have & !ok) ? 1u : 0u;
+        n_late += (good & late) ? 1u : 0u;
+        ts_min = sel(kept, min(ts_min, r.ts), ts_min);
+        ts_max1 = sel(kept, max(ts_max1, r.ts + 1u), ts_max1);
+        surv = kCM2 ? (kept & (r.event == 1u)) : kept;          // WHERE (eventType == 1)
       }
       if (surv && r.ts - pc_lo >= q.S) {         // pane = floor(ts / S), cached per thread
         pc_p = pane_of(r.ts, q.S, q.div_magic);
