@@ -105,7 +105,9 @@ typedef struct {
                                 rank aggregates its own rows; windows close per rank as
                                 PARTIAL rows that are exchanged by key owner
                                 (hash(key) % world) and merged on the owner — see
-                                lms_run_close / lms_partials / lms_merge.               */
+                                lms_run_close / lms_partials / lms_merge.  world > 1
+                                (LR1S, LR1T): vehicle-indexed counts, window counts
+                                all-reduced per closing instance — lms_lr1_close_range. */
 } lms_config;
 
 #define LMS_FLAG_ONLINE_INFPT 0x1u  /* Eq. 10 online regression of InfPT */
@@ -244,6 +246,24 @@ lms_status  lms_watermark_ptrs(lms_query* q, void** wm_dptr, void** tsmin_dptr, 
 lms_status  lms_run_close(lms_query* q);
 lms_status  lms_partials(lms_query* q, const void** rows_dptr, uint64_t* counts /*[world]*/);
 lms_status  lms_merge(lms_query* q, const void* rows_dptr, uint64_t n_rows);
+
+/* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
+ * index the per-pane counts directly (VID < max_keys; larger VIDs count as overflow), every
+ * rank keeps and probes its own rows, and the multiplicity m of a probed row counts the
+ * vehicle in the whole window over ALL ranks.  Per micro-batch, after the watermark
+ * all-reduce and before lms_run_close:
+ *   lms_lr1_close_range   instances [k_first, k_last] this batch closes (syncs the stream;
+ *                         empty when k_last < k_first); identical on every rank
+ *   for each k:  lms_lr1_window_counts(k) -> device uint32[n_counts] of this rank's counts
+ *                of instance k per vehicle; the caller all-reduces it (SUM) on `stream`;
+ *                lms_lr1_probe(k) emits the rows of instance k (newest slide) with the
+ *                all-reduced m
+ *   lms_run_close, lms_sync: state update / eviction; rows are final -> lms_read_lr1.
+ * The counts buffer is library-owned and reused by the next call.  EINVAL: null arguments;
+ * ESTATE: not a multi-GPU LR1 handle, or no aggregate pass awaiting its close.          */
+lms_status  lms_lr1_close_range(lms_query* q, int64_t* k_first, int64_t* k_last);
+lms_status  lms_lr1_window_counts(lms_query* q, int64_t k, void** counts_dptr, uint64_t* n_counts);
+lms_status  lms_lr1_probe(lms_query* q, int64_t k);
 
 /* ------------------------------------------------------------------ timing hooks */
 /* Device time of the last completed batch's kernels, and of its dominant

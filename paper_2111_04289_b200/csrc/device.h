@@ -129,6 +129,10 @@ struct QueryDev {
   unsigned long long* macc_sum; // [Wmerge][K]
   unsigned long long* macc_cnt; // [Wmerge][K]
   uint32_t Wmerge;              // instances merged per merge pass
+  // multi-GPU LR1: vehicles index the counts directly (VID < K), and each closing instance's
+  // window counts are summed into lr1_w and all-reduced before the probe
+  uint32_t lr1_dense;
+  uint32_t* lr1_w;              // [K]
 };
 
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
@@ -139,6 +143,8 @@ cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
 cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st);
 cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st);
+cudaError_t launch_lr1_wsum(const QueryDev& q, long long k, cudaStream_t st);
+cudaError_t launch_lr1_probe(const QueryDev& q, long long k, cudaStream_t st);
 cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st);

@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
       if (pos < q.row_cap) {
         lms_lr1_row o;
         o.win_start_s = k * (long long)q.S;
-        o.vehicle = q.dict.key_by_idx[r.vidx];
+        o.vehicle = q.lr1_dense ? r.vidx : q.dict.key_by_idx[r.vidx];
         o.ts = r.ts; o.multiplicity = m; o.speed = r.speed; o.xway = r.xway; o.segment = r.seg;
         o.lane = r.lane; o.dir = r.dir;
         rows[pos] = o;
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
 __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   DevState* st = q.state;
   const long long upto = st->evict_upto;
-  const uint32_t nk = min(st->n_keys, q.K);
+  const uint32_t nk = q.lr1_dense ? q.K : min(st->n_keys, q.K);
   for (uint32_t g = 0; g < q.P; g++) {
     const uint32_t p = q.slot_pane[g];
     if (p == kEmpty32 || (long long)p > upto) continue;
@@ -433,6 +433,70 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   if (ticket(st)) {
     evict_rebuild_cta(q, upto);
     if (threadIdx.x == 0) { st->close_ticket = 0; __threadfence(); }
+  }
+}
+
+// Multi-GPU LR1 (reading R8 on row-partitioned batches): every rank probes its own newest-pane
+// rows, but the multiplicity m counts the vehicle over ALL ranks' records of the window.
+// k_lr1_wsum writes this rank's counts of instance k's panes into lr1_w (vehicle-indexed,
+// lr1_dense), the caller all-reduces lr1_w (SUM), and k_lr1_probe emits the rows of instance k
+// with m = lr1_w[vehicle].  The union over ranks equals the single-GPU rows.
+__global__ void __launch_bounds__(kCloseThreads) k_lr1_wsum(const QueryDev q, long long k) {
+  __shared__ uint32_t wslots[256];   // R/S <= 256
+  window_slots(q, k, wslots);
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < q.K; v += gridDim.x * blockDim.x) {
+    uint32_t m = 0;
+    for (uint32_t j = 0; j < q.ppw; j++) {
+      const uint32_t g = wslots[j];
+      if (g != kEmpty32) m += q.acc_cnt32[(size_t)g * q.K + v];
+    }
+    q.lr1_w[v] = m;
+  }
+}
+
+__global__ void __launch_bounds__(kCloseThreads) k_lr1_probe(const QueryDev q, long long k) {
+  DevState* st = q.state;
+  const uint32_t cur = st->fifo_cur;
+  const uint32_t n = min((unsigned long long)st->fifo_count[cur], q.fifo_cap);
+  const Lr1Retained* src = q.fifo[cur];
+  Lr1Retained* dst = q.fifo[cur ^ 1u];
+  lms_lr1_row* rows = reinterpret_cast<lms_lr1_row*>(q.rows);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t iters = (n + stride - 1) / stride;
+  for (uint32_t it = 0; it < iters; it++) {
+    const uint32_t i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
+    bool emit = false, keep = false;
+    Lr1Retained r{};
+    if (i < n) {
+      r = src[i];
+      const long long p = (long long)pane_of(r.ts, q.S, q.div_magic);
+      emit = p - (long long)q.ppw + 1 == k;      // instance whose newest slide is pane p
+      keep = !emit;
+    }
+    const unsigned long long pos = row_slot(st, emit);
+    if (emit) {
+      if (pos < q.row_cap) {
+        lms_lr1_row o;
+        o.win_start_s = k * (long long)q.S;
+        o.vehicle = r.vidx;
+        o.ts = r.ts; o.multiplicity = q.lr1_w[r.vidx]; o.speed = r.speed; o.xway = r.xway;
+        o.segment = r.seg; o.lane = r.lane; o.dir = r.dir;
+        rows[pos] = o;
+      } else {
+        atomicExch(&st->row_overflow, 1u);
+      }
+    }
+    const uint32_t km = __ballot_sync(0xffffffffu, keep);
+    uint32_t base = 0;
+    if ((threadIdx.x & 31) == 0 && km) base = atomicAdd(&st->fifo_count[cur ^ 1u], __popc(km));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) dst[base + __popc(km & ((1u << (threadIdx.x & 31)) - 1u))] = r;
+  }
+  if (ticket(st) && threadIdx.x == 0) {          // the kept rows become the live FIFO
+    st->fifo_count[cur] = 0;
+    st->fifo_cur = cur ^ 1u;
+    st->close_ticket = 0;
+    __threadfence();
   }
 }
 
@@ -455,6 +519,16 @@ cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {
   CloseArgs a{q, flush};
   if (q.kind == kLR1S || q.kind == kLR1T) k_close_lr1<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
   else k_close_agg<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lr1_wsum(const QueryDev& q, long long k, cudaStream_t st) {
+  k_lr1_wsum<<<close_ctas(q), kCloseThreads, 0, st>>>(q, k);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lr1_probe(const QueryDev& q, long long k, cudaStream_t st) {
+  k_lr1_probe<<<close_ctas(q), kCloseThreads, 0, st>>>(q, k);
   return cudaGetLastError();
 }
 

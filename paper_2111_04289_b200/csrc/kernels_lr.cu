@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
           }
         } else {
           if (p != c_pane) { c_pane = p; c_gslot = claim_slot(q, p); }
-          uint32_t vidx = c_gslot != kFail32 ? dict_get(q.dict, r.vid, q.state) : kEmpty32;
+          // multi-GPU (lr1_dense): the vehicle id is the index, identical on every rank
+          uint32_t vidx = c_gslot == kFail32 ? kEmpty32
+                        : q.lr1_dense ? (r.vid < K ? (uint32_t)r.vid : kEmpty32)
+                                      : dict_get(q.dict, r.vid, q.state);
           if (vidx == kEmpty32) { cnt.overflow++; continue; }
           atomicAdd(&q.acc_cnt32[(size_t)c_gslot * K + vidx], 1u);
           // projection into the retained FIFO (one atomic per warp)

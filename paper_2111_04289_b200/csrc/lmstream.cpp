@@ -197,7 +197,6 @@ lms_status validate_config(const lms_config* c) {
   if (c->max_result_rows == 0 || c->max_result_rows > (1ull << 32)) return fail(LMS_EINVAL, "max_result_rows");
   if (c->world < 1 || c->world > kMaxWorld || c->rank < 0 || c->rank >= c->world)
     return fail(LMS_EINVAL, "need 0 <= rank < world <= 64");
-  if (c->world > 1 && is_lr1(c->kind)) return fail(LMS_EINVAL, "LR1 runs on one GPU (world must be 1)");
   if (c->world > 1 && c->mode != LMS_MODE_MANUAL)
     return fail(LMS_EINVAL, "multi-GPU handles use LMS_MODE_MANUAL (the caller forms batches in lockstep)");
   return LMS_OK;
@@ -280,7 +279,7 @@ lms_status launch_close_stage(lms_query* q) {
     CUDA_TRY(launch_lr1_evict(q->qd, q->stream));
     q->launches++;
   }
-  if (q->qd.world > 1) {
+  if (q->qd.world > 1 && !is_lr1(q->kind)) {
     CUDA_TRY(launch_bucket(q->qd, q->stream));
     q->launches += 2;
   }
@@ -308,7 +307,8 @@ lms_status complete(lms_query* q) {
   q->last_close_s = ms_close * 1e-3;
   // result rows -> host FIFO (multi-GPU: partial rows stay on the device for lms_merge)
   q->last_report = rep;
-  const uint64_t nrows = q->qd.world > 1 ? 0 : std::min<uint64_t>(rep.rows, q->cfg.max_result_rows);
+  // (LR1 rows are final on every rank: multi-GPU LR1 probes against all-reduced counts)
+  const uint64_t nrows = (q->qd.world > 1 && !is_lr1(q->kind)) ? 0 : std::min<uint64_t>(rep.rows, q->cfg.max_result_rows);
   double d2h = 0;
   if (nrows) {
     const double t0 = now_host();
@@ -461,7 +461,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     d.world = (uint32_t)cfg->world;
     Q_TRY(q->dalloc(&d.state, 1, 0));
     QC_TRY(cudaHostGetDevicePointer((void**)&d.report, q->h_report, 0));   // zero-copy report
-    if (d.world > 1) {                // owner-side merge of partial rows
+    if (d.world > 1 && !is_lr1(q->kind)) {   // owner-side merge of partial rows
       lms_agg_row* send;
       Q_TRY(q->dalloc(&send, cfg->max_result_rows, 0));
       d.send_rows = send;
@@ -482,6 +482,10 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     }
     if (is_lr1(q->kind)) {
       Q_TRY(q->dalloc(&d.acc_cnt32, (size_t)q->P * d.K, 0));
+      if (d.world > 1) {              // vehicle-indexed counts + the all-reduced window counts
+        d.lr1_dense = 1;
+        Q_TRY(q->dalloc(&d.lr1_w, d.K, 0));
+      }
     } else {
       Q_TRY(q->dalloc(&d.acc_sum, (size_t)q->P * d.K, 0));
       Q_TRY(q->dalloc(&d.acc_cnt, (size_t)q->P * d.K, 0));
@@ -755,9 +759,63 @@ lms_status lms_run_close(lms_query* q) {
   }
 }
 
+lms_status lms_lr1_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) {
+  try {
+    if (!q || !k_first || !k_last) return fail(LMS_EINVAL, "null argument");
+    if (!is_lr1(q->kind) || q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU LR1 handle");
+    if (!q->awaiting_close) return fail(LMS_ESTATE, "no aggregate pass awaiting its close");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    CUDA_TRY(cudaStreamSynchronize(q->stream));   // the caller's watermark all-reduce is on it
+    DevState s{};
+    CUDA_TRY(cudaMemcpy(&s, q->qd.state, sizeof(DevState), cudaMemcpyDeviceToHost));
+    // the close kernel's instance range (win_range, reading R7), computed from the same state
+    *k_first = 0;
+    *k_last = -1;
+    if (s.wm != 0) {
+      const long long W = (long long)s.wm - 1, R = q->qd.R, S = q->qd.S;
+      auto fdiv = [](long long a, long long b) { long long d = a / b; return (a % b != 0 && ((a < 0) != (b < 0))) ? d - 1 : d; };
+      *k_first = s.next_k_valid ? s.next_k : fdiv((long long)s.ts_min - R, S) + 1;
+      *k_last = q->in_flight_flush ? fdiv(W, S) : fdiv(W - R, S);
+    }
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in lr1_close_range");
+  }
+}
+
+lms_status lms_lr1_window_counts(lms_query* q, int64_t k, void** counts_dptr, uint64_t* n_counts) {
+  try {
+    if (!q || !counts_dptr || !n_counts) return fail(LMS_EINVAL, "null argument");
+    if (!is_lr1(q->kind) || q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU LR1 handle");
+    if (!q->awaiting_close) return fail(LMS_ESTATE, "no aggregate pass awaiting its close");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    CUDA_TRY(launch_lr1_wsum(q->qd, (long long)k, q->stream));
+    q->launches++;
+    *counts_dptr = q->qd.lr1_w;
+    *n_counts = q->qd.K;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in lr1_window_counts");
+  }
+}
+
+lms_status lms_lr1_probe(lms_query* q, int64_t k) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    if (!is_lr1(q->kind) || q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU LR1 handle");
+    if (!q->awaiting_close) return fail(LMS_ESTATE, "no aggregate pass awaiting its close");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    CUDA_TRY(launch_lr1_probe(q->qd, (long long)k, q->stream));
+    q->launches++;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in lr1_probe");
+  }
+}
+
 lms_status lms_partials(lms_query* q, const void** rows, uint64_t* counts) {
   if (!q || !rows || !counts) return fail(LMS_EINVAL, "null argument");
-  if (q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU handle");
+  if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");
   if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
   *rows = q->qd.send_rows;
   for (uint32_t r = 0; r < q->qd.world; r++) counts[r] = q->last_report.owner_count[r];
@@ -767,7 +825,7 @@ lms_status lms_partials(lms_query* q, const void** rows, uint64_t* counts) {
 lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
   try {
     if (!q || (n && !rows)) return fail(LMS_EINVAL, "null argument");
-    if (q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU handle");
+    if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");
     if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     const double t0 = now_host();

@@ -15,6 +15,10 @@ lms_query (lms_config.rank/world) and processes its own rows of each micro-batch
   5. all-to-all                partial rows to their owners (NCCL, bytes of lms_agg_row)
   6. lms_merge                 owner-side merge + AVG / HAVING / ORDER BY rank (kernels)
 
+LR1 (self-join, no owner exchange): after step 2, for every instance the batch closes the
+ranks' vehicle-indexed window counts are all-reduced (SUM, 4 B per vehicle) and each rank
+probes its own newest-slide rows against the global counts (lms_lr1_* calls).
+
 `Exchange` implementations: TorchDistExchange (one handle per process, any torch.distributed
 backend: NCCL on GPUs, gloo for the CPU protocol tests) and LocalExchange (several handles on
 one GPU in one process — "virtual shards", used to test the kernels of the protocol on a
@@ -43,9 +47,9 @@ class _CudaPtr:
 
 def device_view(ptr: int, nbytes: int, dtype="u1"):
     import torch
-    typestr, size = {"u1": ("|u1", 1), "i8": ("<i8", 8)}[dtype]
+    typestr, size = {"u1": ("|u1", 1), "i4": ("<i4", 4), "i8": ("<i8", 8)}[dtype]
     if nbytes == 0:
-        return torch.empty(0, dtype=torch.uint8 if dtype == "u1" else torch.int64, device="cuda")
+        return torch.empty(0, dtype={"u1": torch.uint8, "i4": torch.int32, "i8": torch.int64}[dtype], device="cuda")
     return torch.as_tensor(_CudaPtr(ptr, nbytes, typestr, size), device="cuda")
 
 
@@ -94,6 +98,27 @@ class RankHandle:
         check(L.lms_partials(self.q.h, C.byref(ptr), counts), "lms_partials")
         cnt = [int(c) for c in counts]
         return device_view(ptr.value or 0, sum(cnt) * ROW_BYTES), cnt
+
+    # ---- multi-GPU LR1
+    def lr1_close_range(self):
+        k0, k1 = C.c_int64(), C.c_int64()
+        check(L.lms_lr1_close_range(self.q.h, C.byref(k0), C.byref(k1)), "lms_lr1_close_range")
+        return k0.value, k1.value
+
+    def lr1_window_counts(self, k: int):
+        """int32 device view of this rank's vehicle counts of instance k (all-reduce it: SUM)."""
+        ptr, n = C.c_void_p(), C.c_uint64()
+        check(L.lms_lr1_window_counts(self.q.h, k, C.byref(ptr), C.byref(n)), "lms_lr1_window_counts")
+        return device_view(ptr.value, n.value * 4, "i4")
+
+    def lr1_probe(self, k: int):
+        check(L.lms_lr1_probe(self.q.h, k), "lms_lr1_probe")
+
+    def run_close(self):
+        check(L.lms_run_close(self.q.h), "lms_run_close")
+
+    def sync(self) -> int:
+        return self.q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW))
 
     def merge(self, rows_u8):
         n = rows_u8.numel() // ROW_BYTES
@@ -153,6 +178,12 @@ class TorchDistExchange:
             self._all_reduce(wm, self.dist.ReduceOp.MAX)
             self._all_reduce(tsmin, self.dist.ReduceOp.MIN)
 
+    def allreduce_sum(self, handles, tensors):
+        """In-place SUM all-reduce of tensors[0] (LR1 window counts) on the handle's stream."""
+        (h,), (t,) = handles, tensors
+        with self._on(h):
+            self._all_reduce(t, self.dist.ReduceOp.SUM)
+
     def all_to_all(self, handles, sends):
         """sends[0] = (uint8 rows tensor grouped by owner, per-owner counts) -> received rows."""
         import torch
@@ -182,6 +213,14 @@ class LocalExchange:
             b.copy_(ts)
         torch.cuda.synchronize()
 
+    def allreduce_sum(self, handles, tensors):
+        import torch
+        torch.cuda.synchronize()
+        tot = torch.stack(list(tensors)).sum(0, dtype=tensors[0].dtype)
+        for t in tensors:
+            t.copy_(tot)
+        torch.cuda.synchronize()
+
     def all_to_all(self, handles, sends):
         import torch
         world = len(handles)
@@ -207,11 +246,14 @@ class _Null:
 # ----------------------------------------------------------------------------- protocol
 
 def run_batch(handles, exchange, now: float, flush: bool = False) -> list[int]:
-    """One micro-batch on every local handle (steps 1-6 above).  Returns the sync statuses."""
+    """One micro-batch on every local handle (steps 1-6 above; LR1: run_batch_lr1's steps).
+    Returns the sync statuses."""
     for h in handles:
         st = L.lms_flush(h.q.h, now) if flush else L.lms_force_batch(h.q.h, now, None)
         check(st, "lms_flush" if flush else "lms_force_batch", (L.LMS_OK, L.LMS_EFORMAT))
     exchange.allreduce_watermarks(handles)
+    if handles[0].q.kind in (L.LMS_LR1S, L.LMS_LR1T):
+        return close_lr1(handles, exchange)
     for h in handles:
         check(L.lms_run_close(h.q.h), "lms_run_close")
     sts = [h.q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW)) for h in handles]
@@ -219,3 +261,20 @@ def run_batch(handles, exchange, now: float, flush: bool = False) -> list[int]:
     for h, rows in zip(handles, recvs):
         h.merge(rows)
     return sts
+
+
+def close_lr1(handles, exchange) -> list[int]:
+    """LR1 (window self-join, reading R8) on row-partitioned batches: for every instance the
+    batch closes, each rank's vehicle counts of the window are all-reduced (SUM) and every rank
+    probes its own newest-slide rows against them; the union of the ranks' rows is the
+    single-GPU result.  No rows move between ranks."""
+    k0, k1 = handles[0].lr1_close_range()
+    for h in handles[1:]:
+        assert h.lr1_close_range() == (k0, k1), "ranks disagree on the closing instances"
+    for k in range(k0, k1 + 1):
+        exchange.allreduce_sum(handles, [h.lr1_window_counts(k) for h in handles])
+        for h in handles:
+            h.lr1_probe(k)
+    for h in handles:
+        h.run_close()
+    return [h.sync() for h in handles]

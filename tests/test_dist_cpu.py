@@ -109,3 +109,63 @@ def test_split_points_record_boundaries(world):
     parts = split_points("LR", lr, world)
     assert all(o % 70 == 0 and n % 70 == 0 for o, n in parts)
     assert sum(n for _, n in parts) == len(lr)
+
+
+class FakeLr1Handle:
+    """CPU stand-in for an LR1 RankHandle: per-instance vehicle counts, records the all-reduced
+    counts each probe saw."""
+
+    def __init__(self, rank, k_range, nveh=64):
+        rng = np.random.default_rng(100 + rank)
+        self.stream_ptr, self.k_range = 0, k_range
+        self.local = {k: torch.from_numpy(rng.integers(0, 5, nveh).astype(np.int32)) for k in range(k_range[0], k_range[1] + 1)}
+        self.sent = {k: v.clone() for k, v in self.local.items()}
+        self.seen, self.closed = {}, False
+
+    def lr1_close_range(self):
+        return self.k_range
+
+    def lr1_window_counts(self, k):
+        return self.local[k]
+
+    def lr1_probe(self, k):
+        self.seen[k] = self.local[k].clone()
+
+    def run_close(self):
+        self.closed = True
+
+    def sync(self):
+        return 0
+
+
+def _lr1_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2111_04289_b200.dist import TorchDistExchange, close_lr1
+        h = FakeLr1Handle(rank, (3, 5))
+        sts = close_lr1([h], TorchDistExchange())
+        q.put((rank, {k: v.numpy().tobytes() for k, v in h.sent.items()},
+               {k: v.numpy().tobytes() for k, v in h.seen.items()}, h.closed, sts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_lr1_window_counts():
+    """Multi-GPU LR1 protocol (dist.close_lr1) over world-size-2 gloo: every closing instance's
+    vehicle counts are SUM-all-reduced before that instance's probe, on every rank."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_lr1_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for k in (3, 4, 5):
+        want = sum(np.frombuffer(r[1][k], np.int32).astype(np.int64) for r in res)
+        for r in res:
+            assert np.array_equal(np.frombuffer(r[2][k], np.int32), want)
+    assert all(r[3] and r[4] == [0] for r in res)

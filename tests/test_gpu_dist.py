@@ -6,7 +6,7 @@ single-GPU parity tests)."""
 import pytest
 
 import lmsgen as g
-from tests.helpers import compare_agg, oracle_rows
+from tests.helpers import compare_agg, compare_lr1, oracle_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -26,7 +26,7 @@ def sharded_run(qname, batches, world, **cfg):
                         h.q.push(d[o:o + n], t)
                 t += 1.0
         run_batch(hs, ex, t, flush=b is None)
-        rows = [h.q.read_agg() for h in hs]
+        rows = [h.q.read_lr1() if qname.startswith("LR1") else h.q.read_agg() for h in hs]
         recs = [h.q.record(h.q.num_batches() - 1) for h in hs]
         outs.append((rows, recs))
     for h in hs:
@@ -57,3 +57,27 @@ def test_virtual_shards_match_oracle(qname, traffic, world):
         assert sum(r["late_records"] for r in recs) == o.late
         assert all(r["windows_closed"] == o.windows_closed for r in recs)
         assert all(r["watermark"] == (-1 if o.watermark is None else o.watermark) for r in recs)
+
+
+@pytest.mark.parametrize("qname,traffic,world", [("LR1S", "B(0.4)", 2), ("LR1S", "U(0.3)", 3), ("LR1T", "B(0.3)", 2)])
+def test_virtual_shards_lr1_match_oracle(qname, traffic, world):
+    """Multi-GPU LR1: every shard probes its own newest-slide rows against the all-reduced
+    vehicle counts of the window; the union of the shards' rows (with multiplicities) equals
+    the single-stream oracle's self-join."""
+    import numpy as np
+    params = g.LRParams(num_vehicles=150)          # many repeat vehicles: m > 1 is common
+    secs = [d for _, d in g.stream_datasets("LR", traffic, 75, seed=23, params=params)]
+    sizes = [4, 9, 1, 13, 6, 20]
+    batches, i = [], 0
+    for s in sizes:
+        batches.append(secs[i:i + s])
+        i += s
+    batches.append(secs[i:])
+    ora = oracle_rows(qname, batches)
+    prod = sharded_run(qname, batches, world)
+    assert len(prod) == len(ora)
+    for (rows, recs), o in zip(prod, ora):
+        compare_lr1(np.concatenate(rows), o.rows)
+        assert sum(r["num_records"] for r in recs) == o.n_records
+        assert all(r["windows_closed"] == o.windows_closed for r in recs)
+        assert all(r["overflow_records"] == 0 for r in recs)
