@@ -310,6 +310,9 @@ def cpu_sample(kind, seconds=2, rate=450_000, seed=211104289, t0=0):
             "rows": sum(len(o.rows) for o in outs)}
 
 
+METRIC = "records/s per micro-batch (CM2 10M-record batches); HBM GB/s; p99 batch latency"
+
+
 def reference_arm(args, wl, rank, world):
     if rank != 0:
         return 0
@@ -321,12 +324,13 @@ def reference_arm(args, wl, rank, world):
     tot_r = sum(p["records"] for p in per)
     tot_t = sum(p["elapsed_s"] for p in per)
     v = tot_r / tot_t
-    line = {"impl": "reference", "metric": "records/s per micro-batch (CM2/LR2), oracle on host CPU",
+    line = {"impl": "reference", "metric": METRIC,
             "value": v, "unit": "records/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64+f64 (Python)", "data": "synthetic (lmsgen, seeded)",
-            "config": {"workload": wl["desc"] + " -- bounded sample: 2 datasets x 30000 records per step",
-                       "global_batch": 60000, "parallelism": "none (1 host thread)"},
+            "config": {"workload": wl["desc"], "records_per_batch_per_gpu": wl["records"],
+                       "global_batch": wl["records"] * world, "parallelism": "oracle, 1 host thread",
+                       "sample": "bounded sample of the workload: 2 datasets x 30000 records per step"},
             "cpu_baseline": {"value": v, "unit": "records/s", "cores": 1, "kind": "oracle",
                              "sample": "2 x 30000-record datasets (seconds 2i, 2i+1) of the same generator per step"},
             "e2e": {"value": v, "unit": "records/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -410,7 +414,7 @@ def main():
                          f"{s['elapsed_s']:.1f} s single-threaded Python"}
     if rank == 0:
         line = {
-            "metric": "records/s per micro-batch (CM2 10M-record batches); HBM GB/s; p99 batch latency",
+            "metric": METRIC,
             "value": value, "unit": "records/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64 fixed-point sums + f64 AVG", "data": "synthetic (lmsgen, seeded)",

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import lmsgen as g
-from tests.helpers import compare_agg, oracle_rows
+from tests.helpers import compare_agg, compare_lr1, oracle_rows
 
 pytestmark = pytest.mark.gpu
 
@@ -43,19 +43,21 @@ def _rank_main(rank, world, port, qname, batches, out_q):
                     t += 1.0
             run_batch([h], ex, t, flush=b is None)
             rec = h.q.record(h.q.num_batches() - 1)
-            outs.append((h.q.read_agg().tobytes(), rec["num_records"], rec["windows_closed"]))
+            rows = h.q.read_lr1() if qname.startswith("LR1") else h.q.read_agg()
+            outs.append((rows.tobytes(), rec["num_records"], rec["windows_closed"]))
         h.q.close()
         out_q.put((rank, outs))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("qname,traffic", [("CM2S", "B(1.5)"), ("LR2S", "R(0.5,2)"), ("CM1S", "B(0.8)")])
+@pytest.mark.parametrize("qname,traffic", [("CM2S", "B(1.5)"), ("LR2S", "R(0.5,2)"), ("CM1S", "B(0.8)"),
+                                           ("LR1S", "B(0.4)")])
 def test_two_processes_match_oracle(qname, traffic):
     import torch.multiprocessing as mp
-    from paper_2111_04289_b200 import AGG_DTYPE
+    from paper_2111_04289_b200 import AGG_DTYPE, LR1_DTYPE
     fam = qname[:2]
-    params = g.CMParams(num_jobs=200) if fam == "CM" else None
+    params = g.CMParams(num_jobs=200) if fam == "CM" else (g.LRParams(num_vehicles=150) if qname == "LR1S" else None)
     secs = [d for _, d in g.stream_datasets(fam, traffic, 75, seed=5, params=params)]
     batches = [secs[i:i + 7] for i in range(0, len(secs), 7)]
     ora = oracle_rows(qname, batches)
@@ -71,7 +73,11 @@ def test_two_processes_match_oracle(qname, traffic):
         assert p.exitcode == 0
     assert len(res[0]) == len(res[1]) == len(ora)
     for i, o in enumerate(ora):
-        rows = np.concatenate([np.frombuffer(res[r][i][0], AGG_DTYPE) for r in range(2)])
-        compare_agg(qname, rows, o.rows)
+        dt = LR1_DTYPE if qname.startswith("LR1") else AGG_DTYPE
+        rows = np.concatenate([np.frombuffer(res[r][i][0], dt) for r in range(2)])
+        if qname.startswith("LR1"):
+            compare_lr1(rows, o.rows)
+        else:
+            compare_agg(qname, rows, o.rows)
         assert res[0][i][1] + res[1][i][1] == o.n_records
         assert res[0][i][2] == res[1][i][2] == o.windows_closed
