@@ -107,7 +107,7 @@ typedef struct {
                                 (hash(key) % world) and merged on the owner — see
                                 lms_run_close / lms_partials / lms_merge.  world > 1
                                 (LR1S, LR1T): vehicle-indexed counts, window counts
-                                all-reduced per closing instance — lms_lr1_close_range. */
+                                all-reduced per closing instance — lms_lr1_window_counts. */
 } lms_config;
 
 #define LMS_FLAG_ONLINE_INFPT 0x1u  /* Eq. 10 online regression of InfPT */
@@ -233,6 +233,9 @@ lms_status  lms_get_batch_record(lms_query* q, uint64_t batch_index, lms_batch_r
  *   lms_force_batch / lms_poll   admit + launch the aggregate pass only (rank-local rows)
  *   all-reduce MAX of *wm, MIN of *ts_min on `stream` (lms_watermark_ptrs): one global
  *                                watermark (reading R7) on every rank
+ *   lms_close_range (optional)   the instances this batch closes, identical on every rank
+ *                                (syncs the stream); when none closes the caller may skip
+ *                                the exchange: lms_run_close + lms_sync finish the batch
  *   lms_run_close                close windows as PARTIAL rows (count, exact sum, no HAVING /
  *                                rank) bucketed by owner rank = fmix64(key) % world
  *   lms_sync                     wait; partial rows stay on the device
@@ -243,6 +246,10 @@ lms_status  lms_get_batch_record(lms_query* q, uint64_t batch_index, lms_batch_r
 /* Device pointers of the live watermark (max kept ts + 1, 0 = none; u64) and of the batch's
  * minimum kept ts (u64, 0xFFFFFFFF = none), and the handle's cudaStream_t.               */
 lms_status  lms_watermark_ptrs(lms_query* q, void** wm_dptr, void** tsmin_dptr, void** stream);
+/* [k_first, k_last]: window instances [k*S, k*S + R) the pending close emits (empty when
+ * k_last < k_first), from the all-reduced watermark (reading R7); call after the watermark
+ * all-reduce, before lms_run_close.  ESTATE: single-GPU handle or no pending close.      */
+lms_status  lms_close_range(lms_query* q, int64_t* k_first, int64_t* k_last);
 lms_status  lms_run_close(lms_query* q);
 lms_status  lms_partials(lms_query* q, const void** rows_dptr, uint64_t* counts /*[world]*/);
 lms_status  lms_merge(lms_query* q, const void* rows_dptr, uint64_t n_rows);
@@ -252,8 +259,7 @@ lms_status  lms_merge(lms_query* q, const void* rows_dptr, uint64_t n_rows);
  * rank keeps and probes its own rows, and the multiplicity m of a probed row counts the
  * vehicle in the whole window over ALL ranks.  Per micro-batch, after the watermark
  * all-reduce and before lms_run_close:
- *   lms_lr1_close_range   instances [k_first, k_last] this batch closes (syncs the stream;
- *                         empty when k_last < k_first); identical on every rank
+ *   lms_close_range       instances [k_first, k_last] this batch closes (above)
  *   for each k:  lms_lr1_window_counts(k) -> device uint32[n_counts] of this rank's counts
  *                of instance k per vehicle; the caller all-reduces it (SUM) on `stream`;
  *                lms_lr1_probe(k) emits the rows of instance k (newest slide) with the
@@ -261,7 +267,6 @@ lms_status  lms_merge(lms_query* q, const void* rows_dptr, uint64_t n_rows);
  *   lms_run_close, lms_sync: state update / eviction; rows are final -> lms_read_lr1.
  * The counts buffer is library-owned and reused by the next call.  EINVAL: null arguments;
  * ESTATE: not a multi-GPU LR1 handle, or no aggregate pass awaiting its close.          */
-lms_status  lms_lr1_close_range(lms_query* q, int64_t* k_first, int64_t* k_last);
 lms_status  lms_lr1_window_counts(lms_query* q, int64_t k, void** counts_dptr, uint64_t* n_counts);
 lms_status  lms_lr1_probe(lms_query* q, int64_t k);
 

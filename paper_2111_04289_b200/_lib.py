@@ -100,7 +100,7 @@ _PROTOS = {
     "lms_run_close": (C.c_int32, [_Q]),
     "lms_partials": (C.c_int32, [_Q, _P(C.c_void_p), _P(C.c_uint64)]),
     "lms_merge": (C.c_int32, [_Q, C.c_void_p, C.c_uint64]),
-    "lms_lr1_close_range": (C.c_int32, [_Q, _P(C.c_int64), _P(C.c_int64)]),
+    "lms_close_range": (C.c_int32, [_Q, _P(C.c_int64), _P(C.c_int64)]),
     "lms_lr1_window_counts": (C.c_int32, [_Q, C.c_int64, _P(C.c_void_p), _P(C.c_uint64)]),
     "lms_lr1_probe": (C.c_int32, [_Q, C.c_int64]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),

@@ -759,10 +759,10 @@ lms_status lms_run_close(lms_query* q) {
   }
 }
 
-lms_status lms_lr1_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) {
+lms_status lms_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) {
   try {
     if (!q || !k_first || !k_last) return fail(LMS_EINVAL, "null argument");
-    if (!is_lr1(q->kind) || q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU LR1 handle");
+    if (q->qd.world < 2) return fail(LMS_ESTATE, "not a multi-GPU handle");
     if (!q->awaiting_close) return fail(LMS_ESTATE, "no aggregate pass awaiting its close");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     CUDA_TRY(cudaStreamSynchronize(q->stream));   // the caller's watermark all-reduce is on it
@@ -779,7 +779,7 @@ lms_status lms_lr1_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) 
     }
     return LMS_OK;
   } catch (...) {
-    return fail(LMS_EINTERNAL, "exception in lr1_close_range");
+    return fail(LMS_EINTERNAL, "exception in close_range");
   }
 }
 

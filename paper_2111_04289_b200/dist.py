@@ -99,12 +99,17 @@ class RankHandle:
         cnt = [int(c) for c in counts]
         return device_view(ptr.value or 0, sum(cnt) * ROW_BYTES), cnt
 
-    # ---- multi-GPU LR1
-    def lr1_close_range(self):
+    def windows_closed(self) -> int:
+        """Window instances the last completed batch closed (identical on every rank)."""
+        return self.q.record(self.q.num_batches() - 1)["windows_closed"]
+
+    def close_range(self):
+        """Window instances [k0, k1] the pending close emits (k1 < k0: none)."""
         k0, k1 = C.c_int64(), C.c_int64()
-        check(L.lms_lr1_close_range(self.q.h, C.byref(k0), C.byref(k1)), "lms_lr1_close_range")
+        check(L.lms_close_range(self.q.h, C.byref(k0), C.byref(k1)), "lms_close_range")
         return k0.value, k1.value
 
+    # ---- multi-GPU LR1
     def lr1_window_counts(self, k: int):
         """int32 device view of this rank's vehicle counts of instance k (all-reduce it: SUM)."""
         ptr, n = C.c_void_p(), C.c_uint64()
@@ -172,11 +177,15 @@ class TorchDistExchange:
         return torch.cuda.stream(torch.cuda.ExternalStream(h.stream_ptr))
 
     def allreduce_watermarks(self, handles):
+        """One MAX all-reduce of [wm, -ts_min] (global watermark and first-batch ts_min)."""
+        import torch
         (h,) = handles
         wm, tsmin = h.watermark_tensors()
         with self._on(h):
-            self._all_reduce(wm, self.dist.ReduceOp.MAX)
-            self._all_reduce(tsmin, self.dist.ReduceOp.MIN)
+            both = torch.cat([wm, -tsmin])
+            self._all_reduce(both, self.dist.ReduceOp.MAX)
+            wm.copy_(both[:1])
+            tsmin.copy_(-both[1:])
 
     def allreduce_sum(self, handles, tensors):
         """In-place SUM all-reduce of tensors[0] (LR1 window counts) on the handle's stream."""
@@ -255,12 +264,21 @@ def run_batch(handles, exchange, now: float, flush: bool = False) -> list[int]:
     if handles[0].q.kind in (L.LMS_LR1S, L.LMS_LR1T):
         return close_lr1(handles, exchange)
     for h in handles:
-        check(L.lms_run_close(h.q.h), "lms_run_close")
-    sts = [h.q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW)) for h in handles]
+        h.run_close()
+    sts = [h.sync() for h in handles]
+    if handles[0].windows_closed() == 0:   # same on every rank: nothing to exchange (most batches)
+        return sts
     recvs = exchange.all_to_all(handles, [h.partials() for h in handles])
     for h, rows in zip(handles, recvs):
         h.merge(rows)
     return sts
+
+
+def _close_range(handles):
+    k0, k1 = handles[0].close_range()
+    for h in handles[1:]:
+        assert h.close_range() == (k0, k1), "ranks disagree on the closing instances"
+    return k0, k1
 
 
 def close_lr1(handles, exchange) -> list[int]:
@@ -268,9 +286,7 @@ def close_lr1(handles, exchange) -> list[int]:
     batch closes, each rank's vehicle counts of the window are all-reduced (SUM) and every rank
     probes its own newest-slide rows against them; the union of the ranks' rows is the
     single-GPU result.  No rows move between ranks."""
-    k0, k1 = handles[0].lr1_close_range()
-    for h in handles[1:]:
-        assert h.lr1_close_range() == (k0, k1), "ranks disagree on the closing instances"
+    k0, k1 = _close_range(handles)
     for k in range(k0, k1 + 1):
         exchange.allreduce_sum(handles, [h.lr1_window_counts(k) for h in handles])
         for h in handles:

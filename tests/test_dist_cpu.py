@@ -52,6 +52,9 @@ class FakeHandle:
     def partials(self):
         return torch.from_numpy(self.rows.view(np.uint8).copy()), self.counts
 
+    def windows_closed(self):
+        return 1
+
 
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
@@ -122,7 +125,7 @@ class FakeLr1Handle:
         self.sent = {k: v.clone() for k, v in self.local.items()}
         self.seen, self.closed = {}, False
 
-    def lr1_close_range(self):
+    def close_range(self):
         return self.k_range
 
     def lr1_window_counts(self, k):
