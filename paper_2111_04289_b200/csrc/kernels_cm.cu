@@ -163,6 +163,29 @@ struct TileIter {
   }
 };
 
+// mbarrier / bulk copy on precomputed shared-window addresses (no per-tile cvta)
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n CM_WAIT:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra CM_WAIT;\n}" ::"r"(bar), "r"(phase) : "memory");
+}
+__device__ __forceinline__ void issue_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+// Issue the copy of the producer iterator's tile into stage `dst` (full tiles: constant size).
+__device__ __forceinline__ void cm_issue_it(const TileIter& it, uint32_t dst, uint32_t bar) {
+  if (it.full()) {
+    issue_s(dst, it.seg + it.off - kCmHaloL, kCmStage, bar);
+    return;
+  }
+  const TileGeom g = it.geom();
+  const uint32_t bulk = (g.hi - g.lo) & ~15u;
+  if (bulk) issue_s(dst + g.lo, g.seg + g.off - kCmHaloL + g.lo, bulk, bar);
+  else asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(0u) : "memory");
+}
 __device__ __forceinline__ void cm_issue(const TileGeom& g, uint8_t* dst, uint64_t* bar) {
   const uint32_t bulk = (g.hi - g.lo) & ~15u;
   mbar_arrive_expect_tx(bar, bulk);
@@ -533,7 +556,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   cur.init(a.segs, t0);
   iss.init(a.segs, t0);
   for (uint32_t s = 0; s < (uint32_t)kCmStages && s < ntiles; s++) {
-    if (lane == 0) cm_issue(iss.geom(), wsmem + s * kCmStage, &full[warp][s]);
+    if (lane == 0) cm_issue_it(iss, smem_addr(wsmem + s * kCmStage), smem_addr(&full[warp][s]));
     iss.next(a.segs);
   }
 
@@ -544,6 +567,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
   uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
   const uint32_t nl_s = smem_addr(nl32), cm_s = smem_addr(cm32);
+  const uint32_t full_s = smem_addr(&full[warp][0]), stage_s = smem_addr(wsmem);
   uint32_t pc_lo = 0, pc_p = 0;                                 // cached pane [pc_lo, pc_lo + S)
 
   // CM2: process entries [0, n) of the warp's survivor list with the warp's lanes
@@ -571,7 +595,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     uint8_t* buf = wsmem + s * kCmStage;
     const TileGeom g = cur.geom();
     cur.next(a.segs);
-    if (lane == 0) mbar_wait(&full[warp][s], ph);
+    if (lane == 0) mbar_wait_s(full_s + 8u * s, ph);
     __syncwarp();
     {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
       const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
@@ -584,7 +608,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     // ---- Pass 1: exact '\n' / ',' masks, one 32-bit mask word (32 B) per lane per step.
     // Window bits [0, 256) are the previous tile's halo masks when the tile continues the
     // segment (carried below), so a tile classifies 4096 new bytes: 4 words per lane.
-    const uint32_t buf_s = smem_addr(buf) + kCmHaloL;
+    const uint32_t buf_s = stage_s + s * kCmStage + kCmHaloL;
     auto mword = [&](int wi) {
       const uint4 va = lds128(buf_s + 32 * wi), vb = lds128(buf_s + 32 * wi + 16);
       const uint32_t na = gather16x128(eq_flags(va.x, k7f, 0x0A0A0A0Au), eq_flags(va.y, k7f, 0x0A0A0A0Au),
@@ -743,7 +767,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       sts32(cm_s + 4 * lane, lds32(cm_s + 4 * (kChunks * 4 + lane)));
     }
     if (it + kCmStages < ntiles) {
-      if (lane == 0) cm_issue(iss.geom(), buf, &full[warp][s]);
+      if (lane == 0) cm_issue_it(iss, stage_s + s * kCmStage, full_s + 8u * s);
       iss.next(a.segs);
     }
   }
