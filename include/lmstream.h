@@ -254,6 +254,40 @@ lms_status  lms_run_close(lms_query* q);
 lms_status  lms_partials(lms_query* q, const void** rows_dptr, uint64_t* counts /*[world]*/);
 lms_status  lms_merge(lms_query* q, const void* rows_dptr, uint64_t n_rows);
 
+/* Fused exchange (PAPER.md "Shuffling" Table III): replaces the
+ * all-to-all + lms_merge steps for LR2S / CM1* / CM2S.  Every rank maps every other rank's
+ * owner-side merge accumulators, key dictionary and state into its address space (CUDA IPC:
+ * peer memory over NVLink/NVSwitch on a multi-GPU node; the same device works too), and a
+ * kernel adds the rank's partial (exact sum, count) of each (instance, key) straight into the
+ * owner's accumulators with remote RED.64 (CM2 keys: remote CAS in the owner's dictionary).
+ * Setup once: lms_p2p_export -> exchange the handles (e.g. all_gather) -> lms_p2p_import of
+ * every rank's handle (including the own one); in one process, lms_p2p_import_local(q, peer).
+ * Per batch that closes windows, after lms_run_close + lms_sync, for each pass of at most
+ * lms_merge_window instances [k_lo, k_lo + nwin) of [close k_first, k_last]:
+ *   lms_p2p_push(k_lo, nwin) on every rank (returns when the pushes are complete)
+ *   barrier across ranks
+ *   lms_p2p_finalize(k_lo, nwin) on every rank: AVG / HAVING / ORDER BY rank of the keys it
+ *                     owns -> host row FIFO (lms_read_agg)
+ *   barrier across ranks (before the next pass or batch pushes again)
+ * The handle is plain bytes (safe to send between processes).  EINVAL: null arguments, a peer
+ * of another query shape; ESTATE: not a multi-GPU aggregate handle, peers not imported, batch
+ * not complete; ECUDA: IPC failure (e.g. no peer access between the devices).            */
+typedef struct {
+  uint32_t rank, world, K, kind;
+  uint64_t dict_cap_mask;
+  uint32_t dict_max_keys, present;   /* present: bit i = ipc[i] is valid                  */
+  uint8_t  ipc[6][64];               /* cudaIpcMemHandle_t of: merge sums, merge counts,
+                                        dictionary keys, values, keys by index, state      */
+} lms_p2p_handle;
+lms_status  lms_p2p_export(lms_query* q, lms_p2p_handle* out);
+lms_status  lms_p2p_import(lms_query* q, const lms_p2p_handle* peer);
+lms_status  lms_p2p_import_local(lms_query* q, lms_query* peer);
+lms_status  lms_merge_window(lms_query* q, uint32_t* wmerge);
+/* Instances [k_first, k_last] the last completed batch closed (k_last < k_first: none).     */
+lms_status  lms_last_close_range(lms_query* q, int64_t* k_first, int64_t* k_last);
+lms_status  lms_p2p_push(lms_query* q, int64_t k_lo, uint32_t nwin);
+lms_status  lms_p2p_finalize(lms_query* q, int64_t k_lo, uint32_t nwin);
+
 /* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
  * index the per-pane counts directly (VID < max_keys; larger VIDs count as overflow), every
  * rank keeps and probes its own rows, and the multiplicity m of a probed row counts the

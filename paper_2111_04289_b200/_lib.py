@@ -70,6 +70,12 @@ class lms_batch_record(C.Structure):
                 ("bad_records", C.c_uint64), ("overflow_records", C.c_uint64), ("watermark", C.c_int64)]
 
 
+class lms_p2p_handle(C.Structure):
+    _fields_ = [("rank", C.c_uint32), ("world", C.c_uint32), ("K", C.c_uint32), ("kind", C.c_uint32),
+                ("dict_cap_mask", C.c_uint64), ("dict_max_keys", C.c_uint32), ("present", C.c_uint32),
+                ("ipc", (C.c_uint8 * 64) * 6)]
+
+
 class lms_dag(C.Structure):
     _fields_ = [("n", C.c_uint32), ("op_kind", C.POINTER(C.c_uint8)), ("pred_off", C.POINTER(C.c_int32)),
                 ("preds", C.POINTER(C.c_int32))]
@@ -103,6 +109,13 @@ _PROTOS = {
     "lms_close_range": (C.c_int32, [_Q, _P(C.c_int64), _P(C.c_int64)]),
     "lms_lr1_window_counts": (C.c_int32, [_Q, C.c_int64, _P(C.c_void_p), _P(C.c_uint64)]),
     "lms_lr1_probe": (C.c_int32, [_Q, C.c_int64]),
+    "lms_p2p_export": (C.c_int32, [_Q, _P(lms_p2p_handle)]),
+    "lms_p2p_import": (C.c_int32, [_Q, _P(lms_p2p_handle)]),
+    "lms_p2p_import_local": (C.c_int32, [_Q, _Q]),
+    "lms_merge_window": (C.c_int32, [_Q, _P(C.c_uint32)]),
+    "lms_last_close_range": (C.c_int32, [_Q, _P(C.c_int64), _P(C.c_int64)]),
+    "lms_p2p_push": (C.c_int32, [_Q, C.c_int64, C.c_uint32]),
+    "lms_p2p_finalize": (C.c_int32, [_Q, C.c_int64, C.c_uint32]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "lms_kernel_launches": (C.c_int32, [_Q, _P(C.c_uint64)]),
     "lms_est_max_lat": (C.c_int32, [_P(C.c_double), _P(C.c_uint64), C.c_uint64, C.c_double, _P(C.c_double)]),

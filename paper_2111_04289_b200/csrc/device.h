@@ -98,6 +98,17 @@ struct Dict {
   uint32_t max_keys;
 };
 
+// A rank's owner-side merge state as seen from any rank (multi-GPU fused exchange): its merge
+// accumulators, its key dictionary (CM2) and its DevState (dictionary counters).  Pointers are
+// local for the own rank and peer-mapped (CUDA IPC over NVLink, or another handle in the same
+// process) for the others.
+struct PeerView {
+  unsigned long long* macc_sum;
+  unsigned long long* macc_cnt;
+  Dict dict;
+  DevState* state;
+};
+
 struct QueryDev {
   int kind;
   uint32_t S, R, ppw, P;        // slide, range (s), panes per window, ring slots
@@ -133,6 +144,7 @@ struct QueryDev {
   // window counts are summed into lr1_w and all-reduced before the probe
   uint32_t lr1_dense;
   uint32_t* lr1_w;              // [K]
+  PeerView* peers;              // [world] (fused exchange; null until lms_p2p_import)
 };
 
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
@@ -148,6 +160,7 @@ cudaError_t launch_lr1_probe(const QueryDev& q, long long k, cudaStream_t st);
 cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st);
+cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cudaStream_t st);
 int close_ctas(const QueryDev& q);
 
 }  // namespace lms

@@ -186,11 +186,6 @@ __device__ __forceinline__ void cm_issue_it(const TileIter& it, uint32_t dst, ui
   if (bulk) issue_s(dst + g.lo, g.seg + g.off - kCmHaloL + g.lo, bulk, bar);
   else asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(0u) : "memory");
 }
-__device__ __forceinline__ void cm_issue(const TileGeom& g, uint8_t* dst, uint64_t* bar) {
-  const uint32_t bulk = (g.hi - g.lo) & ~15u;
-  mbar_arrive_expect_tx(bar, bulk);
-  if (bulk) bulk_g2s(dst + g.lo, g.seg + g.off - kCmHaloL + g.lo, bulk, bar);
-}
 
 struct CmRec {
   uint32_t ts;

@@ -80,6 +80,62 @@ __global__ void __launch_bounds__(kThreads) k_merge(const QueryDev q, const lms_
   }
 }
 
+// Fused exchange: instead of all-to-all of partial rows + owner merge, every
+// rank adds its partial (exact sum, count) of each (instance, key) straight into the OWNER's
+// merge accumulators through peer-mapped memory (remote RED.64 over NVLink); CM2 keys are
+// resolved in the owner's dictionary with remote CAS.  The caller then barriers the ranks
+// and each owner finalizes (k_finalize / k_finalize_cm1, unchanged).
+__device__ __forceinline__ uint32_t dict_get_sys(const Dict& d, unsigned long long key, DevState* st) {
+  unsigned long long h = fmix64(key) & d.cap_mask;
+  while (true) {
+    unsigned long long k = *(volatile unsigned long long*)&d.keys[h];
+    if (k == key || k == kEmpty64) {
+      if (k == kEmpty64) {
+        k = atomicCAS(&d.keys[h], kEmpty64, key);
+        if (k == kEmpty64) {
+          uint32_t idx = atomicAdd(&st->n_keys, 1u);
+          if (idx >= d.max_keys) {
+            atomicExch(&st->key_overflow, 1u);
+            idx = kEmpty32 - 1;
+          } else {
+            d.key_by_idx[idx] = key;
+          }
+          __threadfence_system();                  // key_by_idx before the index is published
+          atomicExch(&d.vals[h], idx);
+          return idx >= d.max_keys ? kEmpty32 : idx;
+        }
+      }
+      if (k == key) {
+        uint32_t v;
+        while ((v = *(volatile uint32_t*)&d.vals[h]) == kEmpty32) { }
+        return v >= d.max_keys ? kEmpty32 : v;
+      }
+    }
+    h = (h + 1) & d.cap_mask;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_p2p_push(const QueryDev q, long long k_lo, uint32_t nwin) {
+  DevState* st = q.state;
+  const unsigned long long n = st->part_rows;
+  const lms_agg_row* rows = reinterpret_cast<const lms_agg_row*>(q.send_rows);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const lms_agg_row r = rows[i];
+    const long long w = floor_div(r.win_start_s, (long long)q.S) - k_lo;
+    if (w < 0 || w >= (long long)nwin) continue;
+    const PeerView P = q.peers[owner_of(q, r)];
+    uint32_t idx;
+    if (q.kind == kCM2S) idx = dict_get_sys(P.dict, r.key, P.state);
+    else idx = (uint32_t)r.key;
+    if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
+    const size_t g = (size_t)w * q.K + idx;
+    atomicAdd(&P.macc_sum[g], r.sum_fixed);
+    atomicAdd(&P.macc_cnt[g], r.count);
+  }
+  __threadfence_system();
+}
+
 __device__ __forceinline__ unsigned long long append_row(DevState* st, bool want) {
   const uint32_t act = __activemask();
   const uint32_t m = __ballot_sync(act, want);
@@ -195,6 +251,11 @@ int sm_count() {
 cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st) {
   k_bucket_count<<<sm_count(), kThreads, 0, st>>>(q);
   k_bucket_scatter<<<sm_count(), kThreads, 0, st>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cudaStream_t st) {
+  k_p2p_push<<<sm_count(), kThreads, 0, st>>>(q, k_lo, nwin);
   return cudaGetLastError();
 }
 

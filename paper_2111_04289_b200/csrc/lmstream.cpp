@@ -146,6 +146,8 @@ struct lms_query {
   RowFifo<lms_agg_row> agg_rows;
   RowFifo<lms_lr1_row> lr1_rows;
   unsigned long long* h_count = nullptr;   // pinned 8 B (merged row count)
+  std::vector<PeerView> peers_h;           // fused exchange: every rank's owner state
+  std::vector<void*> ipc_opened;           // peer buffers opened with cudaIpcOpenMemHandle
   uint64_t launches = 0;
   double last_batch_s = 0, last_agg_s = 0, last_close_s = 0;
   lms_status last_completion = LMS_OK;
@@ -153,6 +155,7 @@ struct lms_query {
   ~lms_query() {
     cudaSetDevice(cfg.device);
     if (stream) cudaStreamSynchronize(stream);
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (void* p : dallocs) cudaFree(p);
     if (h_report) cudaFreeHost(h_report);
     if (h_count) cudaFreeHost(h_count);
@@ -813,6 +816,150 @@ lms_status lms_lr1_probe(lms_query* q, int64_t k) {
   }
 }
 
+lms_status merge_pass(lms_query* q, const void* rows, uint64_t n, long long k_lo, uint32_t nwin);
+
+// ---- fused exchange (peer-mapped owner accumulators)
+namespace {
+lms_status p2p_check(lms_query* q) {
+  if (!q) return fail(LMS_EINVAL, "null query");
+  if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");
+  return LMS_OK;
+}
+lms_status p2p_publish(lms_query* q) {
+  if (!q->qd.peers) {
+    PeerView* d = nullptr;
+    if (lms_status e = q->dalloc(&d, q->qd.world, 0)) return e;
+    q->qd.peers = d;
+  }
+  CUDA_TRY(cudaMemcpy(q->qd.peers, q->peers_h.data(), q->peers_h.size() * sizeof(PeerView), cudaMemcpyHostToDevice));
+  return LMS_OK;
+}
+}  // namespace
+
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "lms_p2p_handle.ipc slots are 64 B");
+static_assert(sizeof(lms_p2p_handle) == 416, "lms_p2p_handle layout is part of the ABI");
+
+lms_status lms_p2p_export(lms_query* q, lms_p2p_handle* out) {
+  try {
+    if (lms_status e = p2p_check(q)) return e;
+    if (!out) return fail(LMS_EINVAL, "null argument");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    *out = lms_p2p_handle{};
+    out->rank = q->qd.rank;
+    out->world = q->qd.world;
+    out->K = q->qd.K;
+    out->kind = q->kind;
+    out->dict_cap_mask = q->qd.dict.cap_mask;
+    out->dict_max_keys = q->qd.dict.max_keys;
+    void* bufs[6] = {q->qd.macc_sum, q->qd.macc_cnt, q->qd.dict.keys, q->qd.dict.vals, q->qd.dict.key_by_idx,
+                     q->qd.state};
+    for (int i = 0; i < 6; i++) {
+      if (!bufs[i]) continue;                     // no dictionary for LR2 / CM1
+      cudaIpcMemHandle_t h;
+      CUDA_TRY(cudaIpcGetMemHandle(&h, bufs[i]));
+      std::memcpy(out->ipc[i], &h, sizeof(h));
+      out->present |= 1u << i;
+    }
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in p2p_export");
+  }
+}
+
+lms_status lms_p2p_import(lms_query* q, const lms_p2p_handle* peer) {
+  try {
+    if (lms_status e = p2p_check(q)) return e;
+    if (!peer) return fail(LMS_EINVAL, "null argument");
+    if (peer->world != q->qd.world || peer->rank >= q->qd.world || peer->K != q->qd.K || peer->kind != q->kind)
+      return fail(LMS_EINVAL, "peer handle of another query shape");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    if (q->peers_h.empty()) q->peers_h.assign(q->qd.world, PeerView{});
+    PeerView v{};
+    if (peer->rank == q->qd.rank) {               // own rank: local pointers
+      v.macc_sum = q->qd.macc_sum; v.macc_cnt = q->qd.macc_cnt; v.dict = q->qd.dict; v.state = q->qd.state;
+    } else {
+      void* ptr[6] = {};
+      for (int i = 0; i < 6; i++) {
+        if (!(peer->present & (1u << i))) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, peer->ipc[i], sizeof(h));
+        CUDA_TRY(cudaIpcOpenMemHandle(&ptr[i], h, cudaIpcMemLazyEnablePeerAccess));
+        q->ipc_opened.push_back(ptr[i]);
+      }
+      v.macc_sum = static_cast<unsigned long long*>(ptr[0]);
+      v.macc_cnt = static_cast<unsigned long long*>(ptr[1]);
+      v.dict.keys = static_cast<unsigned long long*>(ptr[2]);
+      v.dict.vals = static_cast<uint32_t*>(ptr[3]);
+      v.dict.key_by_idx = static_cast<unsigned long long*>(ptr[4]);
+      v.dict.cap_mask = peer->dict_cap_mask;
+      v.dict.max_keys = peer->dict_max_keys;
+      v.state = static_cast<DevState*>(ptr[5]);
+    }
+    q->peers_h[peer->rank] = v;
+    return p2p_publish(q);
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in p2p_import");
+  }
+}
+
+lms_status lms_p2p_import_local(lms_query* q, lms_query* peer) {
+  try {
+    if (lms_status e = p2p_check(q)) return e;
+    if (!peer || peer->qd.world != q->qd.world || peer->qd.K != q->qd.K || peer->kind != q->kind)
+      return fail(LMS_EINVAL, "peer handle of another query shape");
+    if (peer->cfg.device != q->cfg.device) return fail(LMS_EINVAL, "in-process peers must share the device");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    if (q->peers_h.empty()) q->peers_h.assign(q->qd.world, PeerView{});
+    PeerView v{};
+    v.macc_sum = peer->qd.macc_sum; v.macc_cnt = peer->qd.macc_cnt; v.dict = peer->qd.dict; v.state = peer->qd.state;
+    q->peers_h[peer->qd.rank] = v;
+    return p2p_publish(q);
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in p2p_import_local");
+  }
+}
+
+lms_status lms_last_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) {
+  if (!q || !k_first || !k_last) return fail(LMS_EINVAL, "null argument");
+  if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
+  *k_first = q->last_report.close_k_first;
+  *k_last = q->last_report.close_k_last;
+  return LMS_OK;
+}
+
+lms_status lms_merge_window(lms_query* q, uint32_t* wmerge) {
+  if (lms_status e = p2p_check(q)) return e;
+  if (!wmerge) return fail(LMS_EINVAL, "null argument");
+  *wmerge = q->qd.Wmerge;
+  return LMS_OK;
+}
+
+lms_status lms_p2p_push(lms_query* q, int64_t k_lo, uint32_t nwin) {
+  try {
+    if (lms_status e = p2p_check(q)) return e;
+    if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
+    if (nwin == 0 || nwin > q->qd.Wmerge) return fail(LMS_EINVAL, "nwin must be in [1, merge window]");
+    for (const PeerView& v : q->peers_h)
+      if (!v.macc_sum) return fail(LMS_ESTATE, "peers not imported (lms_p2p_import for every rank)");
+    if (q->peers_h.size() != q->qd.world) return fail(LMS_ESTATE, "peers not imported");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    const double t0 = now_host();
+    CUDA_TRY(launch_p2p_push(q->qd, (long long)k_lo, nwin, q->stream));
+    q->launches++;
+    CUDA_TRY(cudaStreamSynchronize(q->stream));
+    if (!q->records.empty()) q->records.back().d2h_s += now_host() - t0;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in p2p_push");
+  }
+}
+
+lms_status lms_p2p_finalize(lms_query* q, int64_t k_lo, uint32_t nwin) {
+  if (lms_status e = p2p_check(q)) return e;
+  if (nwin == 0 || nwin > q->qd.Wmerge) return fail(LMS_EINVAL, "nwin must be in [1, merge window]");
+  return merge_pass(q, nullptr, 0, (long long)k_lo, nwin);
+}
+
 lms_status lms_partials(lms_query* q, const void** rows, uint64_t* counts) {
   if (!q || !rows || !counts) return fail(LMS_EINVAL, "null argument");
   if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");
@@ -822,20 +969,15 @@ lms_status lms_partials(lms_query* q, const void** rows, uint64_t* counts) {
   return LMS_OK;
 }
 
-lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
+// Owner merge of received rows for instances [k_lo, k_lo + nwin) (rows may be null: finalize
+// only, fused exchange), then final rows -> (DMA) -> pinned host FIFO.
+lms_status merge_pass(lms_query* q, const void* rows, uint64_t n, long long k_lo, uint32_t nwin) {
   try {
-    if (!q || (n && !rows)) return fail(LMS_EINVAL, "null argument");
-    if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");
     if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     const double t0 = now_host();
-    const BatchReport& rep = q->last_report;
-    for (long long k = rep.close_k_first; k <= rep.close_k_last; k += q->qd.Wmerge) {
-      const uint32_t nwin = (uint32_t)std::min<long long>(q->qd.Wmerge, rep.close_k_last - k + 1);
-      CUDA_TRY(launch_merge(q->qd, rows, n, k, nwin, q->stream));
-      q->launches += 2;
-    }
-    // final rows -> (DMA) -> pinned host FIFO
+    CUDA_TRY(launch_merge(q->qd, rows, n, k_lo, nwin, q->stream));
+    q->launches += n ? 2 : 1;
     unsigned long long* d_rows = &q->qd.state->rows;
     CUDA_TRY(cudaMemcpyAsync(q->h_count, d_rows, sizeof(unsigned long long), cudaMemcpyDeviceToHost, q->stream));
     CUDA_TRY(cudaStreamSynchronize(q->stream));
@@ -851,7 +993,7 @@ lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
     CUDA_TRY(cudaMemsetAsync(d_rows, 0, sizeof(unsigned long long), q->stream));
     if (!q->records.empty()) {
       lms_batch_record& r = q->records.back();
-      r.rows_emitted = nrows;
+      r.rows_emitted += nrows;
       r.d2h_s += now_host() - t0;
     }
     if (total > nrows) return fail(LMS_EOVERFLOW, "merged rows exceed max_result_rows");
@@ -859,6 +1001,19 @@ lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in merge");
   }
+}
+
+lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
+  if (!q || (n && !rows)) return fail(LMS_EINVAL, "null argument");
+  if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");
+  if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
+  const BatchReport& rep = q->last_report;
+  if (!q->records.empty()) q->records.back().rows_emitted = 0;
+  for (long long k = rep.close_k_first; k <= rep.close_k_last; k += q->qd.Wmerge) {
+    const uint32_t nwin = (uint32_t)std::min<long long>(q->qd.Wmerge, rep.close_k_last - k + 1);
+    if (lms_status e = merge_pass(q, rows, n, k, nwin)) return e;
+  }
+  return LMS_OK;
 }
 
 // ------------------------------------------------------------------ pure functions

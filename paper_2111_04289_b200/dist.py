@@ -22,8 +22,9 @@ probes its own newest-slide rows against the global counts (lms_lr1_* calls).
 `Exchange` implementations: TorchDistExchange (one handle per process, any torch.distributed
 backend: NCCL on GPUs, gloo for the CPU protocol tests) and LocalExchange (several handles on
 one GPU in one process — "virtual shards", used to test the kernels of the protocol on a
-single GPU).  The fused device-initiated exchange (NCCL device API / NVLS) is the next step
-(SURVEY §8f f1), not this module.
+single GPU).  run_batch(p2p=True) uses the fused exchange instead: each rank
+adds its partials straight into the owners' accumulators through peer-mapped memory (CUDA IPC
+over NVLink; lms_p2p_*), then barrier + owner finalize — no all-to-all, no merge copy.
 """
 from __future__ import annotations
 
@@ -102,6 +103,35 @@ class RankHandle:
     def windows_closed(self) -> int:
         """Window instances the last completed batch closed (identical on every rank)."""
         return self.q.record(self.q.num_batches() - 1)["windows_closed"]
+
+    # ---- fused exchange (peer-mapped owner accumulators)
+    def p2p_export(self) -> bytes:
+        h = L.lms_p2p_handle()
+        check(L.lms_p2p_export(self.q.h, C.byref(h)), "lms_p2p_export")
+        return bytes(h)
+
+    def p2p_import(self, blob: bytes):
+        h = L.lms_p2p_handle.from_buffer_copy(blob)
+        check(L.lms_p2p_import(self.q.h, C.byref(h)), "lms_p2p_import")
+
+    def p2p_import_local(self, other: "RankHandle"):
+        check(L.lms_p2p_import_local(self.q.h, other.q.h), "lms_p2p_import_local")
+
+    def merge_window(self) -> int:
+        w = C.c_uint32()
+        check(L.lms_merge_window(self.q.h, C.byref(w)), "lms_merge_window")
+        return w.value
+
+    def last_close_range(self):
+        k0, k1 = C.c_int64(), C.c_int64()
+        check(L.lms_last_close_range(self.q.h, C.byref(k0), C.byref(k1)), "lms_last_close_range")
+        return k0.value, k1.value
+
+    def p2p_push(self, k_lo: int, nwin: int):
+        check(L.lms_p2p_push(self.q.h, k_lo, nwin), "lms_p2p_push")
+
+    def p2p_finalize(self, k_lo: int, nwin: int):
+        return check(L.lms_p2p_finalize(self.q.h, k_lo, nwin), "lms_p2p_finalize", (L.LMS_OK, L.LMS_EOVERFLOW))
 
     def close_range(self):
         """Window instances [k0, k1] the pending close emits (k1 < k0: none)."""
@@ -187,6 +217,18 @@ class TorchDistExchange:
             wm.copy_(both[:1])
             tsmin.copy_(-both[1:])
 
+    def setup_p2p(self, handles):
+        """Fused exchange: every rank maps every rank's owner state (CUDA IPC handles sent with
+        all_gather_object)."""
+        (h,) = handles
+        blobs = [None] * self.world
+        self.dist.all_gather_object(blobs, h.p2p_export(), group=self.group)
+        for b in blobs:
+            h.p2p_import(b)
+
+    def barrier(self, handles):
+        self.dist.barrier(group=self.group)
+
     def allreduce_sum(self, handles, tensors):
         """In-place SUM all-reduce of tensors[0] (LR1 window counts) on the handle's stream."""
         (h,), (t,) = handles, tensors
@@ -210,6 +252,14 @@ class TorchDistExchange:
 
 class LocalExchange:
     """All ranks' handles in one process (virtual shards on one GPU)."""
+
+    def setup_p2p(self, handles):
+        for h in handles:
+            for o in handles:
+                h.p2p_import_local(o)
+
+    def barrier(self, handles):
+        pass                        # pushes are synchronous: nothing in flight
 
     def allreduce_watermarks(self, handles):
         import torch
@@ -254,8 +304,9 @@ class _Null:
 
 # ----------------------------------------------------------------------------- protocol
 
-def run_batch(handles, exchange, now: float, flush: bool = False) -> list[int]:
-    """One micro-batch on every local handle (steps 1-6 above; LR1: run_batch_lr1's steps).
+def run_batch(handles, exchange, now: float, flush: bool = False, p2p: bool = False) -> list[int]:
+    """One micro-batch on every local handle (steps 1-6 above; LR1: close_lr1's steps).
+    p2p: fused exchange (exchange.setup_p2p done once) instead of all-to-all + lms_merge.
     Returns the sync statuses."""
     for h in handles:
         st = L.lms_flush(h.q.h, now) if flush else L.lms_force_batch(h.q.h, now, None)
@@ -267,6 +318,18 @@ def run_batch(handles, exchange, now: float, flush: bool = False) -> list[int]:
         h.run_close()
     sts = [h.sync() for h in handles]
     if handles[0].windows_closed() == 0:   # same on every rank: nothing to exchange (most batches)
+        return sts
+    if p2p:
+        k0, k1 = handles[0].last_close_range()
+        wmerge = handles[0].merge_window()
+        for k in range(k0, k1 + 1, wmerge):
+            nwin = min(wmerge, k1 - k + 1)
+            for h in handles:
+                h.p2p_push(k, nwin)            # partials -> owners' accumulators (peer memory)
+            exchange.barrier(handles)
+            for h in handles:
+                h.p2p_finalize(k, nwin)        # owners: AVG / HAVING / rank -> host rows
+            exchange.barrier(handles)
         return sts
     recvs = exchange.all_to_all(handles, [h.partials() for h in handles])
     for h, rows in zip(handles, recvs):

@@ -172,3 +172,71 @@ def test_gloo_world2_lr1_window_counts():
         for r in res:
             assert np.array_equal(np.frombuffer(r[2][k], np.int32), want)
     assert all(r[3] and r[4] == [0] for r in res)
+
+
+class FakeP2PHandle:
+    """CPU stand-in for the fused-exchange side of a RankHandle: records the protocol calls."""
+
+    def __init__(self, rank):
+        self.rank, self.stream_ptr, self.calls, self.imported = rank, 0, [], []
+
+    def p2p_export(self):
+        return bytes([self.rank]) * 416
+
+    def p2p_import(self, blob):
+        self.imported.append(blob[0])
+
+    def windows_closed(self):
+        return 3
+
+    def last_close_range(self):
+        return (10, 12)
+
+    def merge_window(self):
+        return 2
+
+    def p2p_push(self, k, n):
+        self.calls.append(("push", k, n))
+
+    def p2p_finalize(self, k, n):
+        self.calls.append(("fin", k, n))
+
+
+def _p2p_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2111_04289_b200.dist as D
+        h = FakeP2PHandle(rank)
+        ex = D.TorchDistExchange()
+        ex.setup_p2p([h])
+        # the close / exchange tail of run_batch(p2p=True) on an already-synced batch
+        k0, k1 = h.last_close_range()
+        w = h.merge_window()
+        for k in range(k0, k1 + 1, w):
+            n = min(w, k1 - k + 1)
+            h.p2p_push(k, n)
+            ex.barrier([h])
+            h.p2p_finalize(k, n)
+            ex.barrier([h])
+        q.put((rank, h.imported, h.calls))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_p2p_setup_and_passes():
+    """Fused exchange host protocol over world-size-2 gloo: every rank imports every rank's
+    handle (in rank order) and pushes / finalizes the closed instances in merge-window passes."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, imported, calls in res:
+        assert imported == [0, 1]
+        assert calls == [("push", 10, 2), ("fin", 10, 2), ("push", 12, 1), ("fin", 12, 1)]

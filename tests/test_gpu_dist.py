@@ -11,12 +11,14 @@ from tests.helpers import compare_agg, compare_lr1, oracle_rows
 pytestmark = pytest.mark.gpu
 
 
-def sharded_run(qname, batches, world, **cfg):
+def sharded_run(qname, batches, world, p2p=False, **cfg):
     import paper_2111_04289_b200 as P
     from paper_2111_04289_b200.dist import LocalExchange, RankHandle, run_batch, split_points
     fam = qname[:2]
     hs = [RankHandle(P.Query(qname, mode="manual", rank=r, world=world, **cfg)) for r in range(world)]
     ex = LocalExchange()
+    if p2p:
+        ex.setup_p2p(hs)
     outs, t = [], 0.0
     for b in batches + [None]:
         if b is not None:
@@ -25,7 +27,7 @@ def sharded_run(qname, batches, world, **cfg):
                     if n:
                         h.q.push(d[o:o + n], t)
                 t += 1.0
-        run_batch(hs, ex, t, flush=b is None)
+        run_batch(hs, ex, t, flush=b is None, p2p=p2p)
         rows = [h.q.read_lr1() if qname.startswith("LR1") else h.q.read_agg() for h in hs]
         recs = [h.q.record(h.q.num_batches() - 1) for h in hs]
         outs.append((rows, recs))
@@ -34,10 +36,11 @@ def sharded_run(qname, batches, world, **cfg):
     return outs
 
 
+@pytest.mark.parametrize("p2p", [False, True], ids=["alltoall", "p2p"])
 @pytest.mark.parametrize("qname,traffic,world", [("CM2S", "B(1.3)", 2), ("CM2S", "R(0.2,1.5)", 3),
                                                   ("LR2S", "B(1.7)", 2), ("LR2S", "U(0.8)", 4),
                                                   ("CM1S", "B(0.9)", 3), ("CM1T", "B(0.7)", 2)])
-def test_virtual_shards_match_oracle(qname, traffic, world):
+def test_virtual_shards_match_oracle(qname, traffic, world, p2p):
     import numpy as np
     fam = qname[:2]
     params = g.CMParams(num_jobs=300) if fam == "CM" else None
@@ -49,7 +52,7 @@ def test_virtual_shards_match_oracle(qname, traffic, world):
         i += s
     batches.append(secs[i:])
     ora = oracle_rows(qname, batches)
-    prod = sharded_run(qname, batches, world)
+    prod = sharded_run(qname, batches, world, p2p=p2p)
     assert len(prod) == len(ora)
     for (rows, recs), o in zip(prod, ora):
         compare_agg(qname, np.concatenate(rows), o.rows)

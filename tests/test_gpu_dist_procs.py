@@ -22,7 +22,7 @@ def _port():
     return p
 
 
-def _rank_main(rank, world, port, qname, batches, out_q):
+def _rank_main(rank, world, port, qname, batches, out_q, p2p=False):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
@@ -33,6 +33,8 @@ def _rank_main(rank, world, port, qname, batches, out_q):
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch, split_points
         h = RankHandle(P.Query(qname, mode="manual", rank=rank, world=world))
         ex = TorchDistExchange()
+        if p2p:
+            ex.setup_p2p([h])            # CUDA IPC: each process maps the other's owner state
         t, outs = 0.0, []
         for b in batches + [None]:
             if b is not None:
@@ -41,7 +43,7 @@ def _rank_main(rank, world, port, qname, batches, out_q):
                     if n:
                         h.q.push(d[o:o + n], t)
                     t += 1.0
-            run_batch([h], ex, t, flush=b is None)
+            run_batch([h], ex, t, flush=b is None, p2p=p2p)
             rec = h.q.record(h.q.num_batches() - 1)
             rows = h.q.read_lr1() if qname.startswith("LR1") else h.q.read_agg()
             outs.append((rows.tobytes(), rec["num_records"], rec["windows_closed"]))
@@ -51,9 +53,11 @@ def _rank_main(rank, world, port, qname, batches, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("qname,traffic", [("CM2S", "B(1.5)"), ("LR2S", "R(0.5,2)"), ("CM1S", "B(0.8)"),
-                                           ("LR1S", "B(0.4)")])
-def test_two_processes_match_oracle(qname, traffic):
+@pytest.mark.parametrize("qname,traffic,p2p", [("CM2S", "B(1.5)", False), ("LR2S", "R(0.5,2)", False),
+                                               ("CM1S", "B(0.8)", False), ("LR1S", "B(0.4)", False),
+                                               ("CM2S", "B(1.5)", True), ("LR2S", "R(0.5,2)", True),
+                                               ("CM1S", "B(0.8)", True)])
+def test_two_processes_match_oracle(qname, traffic, p2p):
     import torch.multiprocessing as mp
     from paper_2111_04289_b200 import AGG_DTYPE, LR1_DTYPE
     fam = qname[:2]
@@ -64,7 +68,7 @@ def test_two_processes_match_oracle(qname, traffic):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, qname, batches, q)) for r in range(2)]
+    ps = [ctx.Process(target=_rank_main, args=(r, 2, port, qname, batches, q, p2p)) for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(2))
