@@ -320,21 +320,28 @@ def run_batch(handles, exchange, now: float, flush: bool = False, p2p: bool = Fa
     if handles[0].windows_closed() == 0:   # same on every rank: nothing to exchange (most batches)
         return sts
     if p2p:
-        k0, k1 = handles[0].last_close_range()
-        wmerge = handles[0].merge_window()
-        for k in range(k0, k1 + 1, wmerge):
-            nwin = min(wmerge, k1 - k + 1)
-            for h in handles:
-                h.p2p_push(k, nwin)            # partials -> owners' accumulators (peer memory)
-            exchange.barrier(handles)
-            for h in handles:
-                h.p2p_finalize(k, nwin)        # owners: AVG / HAVING / rank -> host rows
-            exchange.barrier(handles)
+        exchange_p2p(handles, exchange)
         return sts
     recvs = exchange.all_to_all(handles, [h.partials() for h in handles])
     for h, rows in zip(handles, recvs):
         h.merge(rows)
     return sts
+
+
+def exchange_p2p(handles, exchange):
+    """Fused exchange of a synced batch that closed windows: per merge-window pass, every rank
+    pushes its partials into the owners' accumulators (peer memory), barrier, every owner
+    finalizes its keys (rows -> host), barrier."""
+    k0, k1 = handles[0].last_close_range()
+    wmerge = handles[0].merge_window()
+    for k in range(k0, k1 + 1, wmerge):
+        nwin = min(wmerge, k1 - k + 1)
+        for h in handles:
+            h.p2p_push(k, nwin)
+        exchange.barrier(handles)
+        for h in handles:
+            h.p2p_finalize(k, nwin)
+        exchange.barrier(handles)
 
 
 def _close_range(handles):

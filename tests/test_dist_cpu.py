@@ -210,15 +210,7 @@ def _p2p_worker(rank, world, port, q):
         h = FakeP2PHandle(rank)
         ex = D.TorchDistExchange()
         ex.setup_p2p([h])
-        # the close / exchange tail of run_batch(p2p=True) on an already-synced batch
-        k0, k1 = h.last_close_range()
-        w = h.merge_window()
-        for k in range(k0, k1 + 1, w):
-            n = min(w, k1 - k + 1)
-            h.p2p_push(k, n)
-            ex.barrier([h])
-            h.p2p_finalize(k, n)
-            ex.barrier([h])
+        D.exchange_p2p([h], ex)          # the exchange tail of run_batch(p2p=True)
         q.put((rank, h.imported, h.calls))
     finally:
         dist.destroy_process_group()
