@@ -136,7 +136,7 @@ def gen_inputs(wl, seconds, t0, seed, torch):
     return bufs
 
 
-def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
+def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p=False):
     import numpy as np
     import paper_2111_04289_b200 as P
     dev = torch.cuda.current_device()
@@ -147,11 +147,13 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
     if world > 1:
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
         h, ex = RankHandle(q), TorchDistExchange()
+        if p2p:
+            ex.setup_p2p([h])
 
     def step(buf, n, t):
         q.push_device(buf.data_ptr(), n, float(t))
-        if world > 1:                     # partial aggregates merged by key owner over NCCL
-            run_batch([h], ex, float(t) + 1.0)
+        if world > 1:                     # partial aggregates merged by key owner
+            run_batch([h], ex, float(t) + 1.0, p2p=p2p)
         else:
             q.force(float(t) + 1.0)
             q.sync()
@@ -196,7 +198,7 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist):
     return out
 
 
-def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None):
+def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None, p2p=False):
     """Inputs in pinned host memory; each step: lms_push (H2D) + batch + rows to host.
     N > 1: every rank pushes its own partition; batches run the dist.py protocol; the time is
     the max over ranks."""
@@ -219,12 +221,14 @@ def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None):
     if world > 1:
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
         hd, ex = RankHandle(q), TorchDistExchange()
+        if p2p:
+            ex.setup_p2p([hd])
     d2h = []
 
     def step(h, n, t):
         q.push((h.data_ptr(), n), float(t))
         if world > 1:
-            run_batch([hd], ex, float(t) + 1.0)
+            run_batch([hd], ex, float(t) + 1.0, p2p=p2p)
         else:
             q.force(float(t) + 1.0)
             q.sync()
@@ -351,6 +355,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--seed", type=int, default=211104289)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "p2p"],
+                    help="N > 1: partial-aggregate exchange (NCCL all-to-all + owner merge, or the fused "
+                         "peer-memory push into the owners' accumulators)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -376,7 +383,8 @@ def main():
     from paper_2111_04289_b200 import build  # noqa: F401  (library must already be built)
 
     seed = args.seed + 7919 * rank        # each rank: its own partition of the global batch
-    res = device_run(wl, args.steps, args.warmup, seed, rank, world, torch, dist)
+    p2p = args.exchange == "p2p"
+    res = device_run(wl, args.steps, args.warmup, seed, rank, world, torch, dist, p2p)
     el = res["elapsed_s"]
     if world > 1:
         el = max_over_ranks(el, torch, dist)
@@ -388,7 +396,7 @@ def main():
     sec = None
     if args.secondary and args.secondary != args.workload:
         w2 = WORKLOADS[args.secondary]
-        r2 = device_run(w2, max(5, args.steps // 2), args.warmup, seed, rank, world, torch, dist)
+        r2 = device_run(w2, max(5, args.steps // 2), args.warmup, seed, rank, world, torch, dist, p2p)
         if world > 1:
             r2["elapsed_s"] = max_over_ranks(r2["elapsed_s"], torch, dist)
         a2 = statistics.mean(r2["agg_s"])
@@ -401,7 +409,7 @@ def main():
                "traffic_ncu_bytes": ncu_traffic(args.secondary), "clocks": r2["clocks"]}
     e2e = None
     if args.e2e_steps > 0:
-        e = e2e_run(wl, args.e2e_steps, 1, seed, torch, rank, world, dist)
+        e = e2e_run(wl, args.e2e_steps, 1, seed, torch, rank, world, dist, p2p)
         e2e = {"value": wl["records"] * world * args.e2e_steps / e["elapsed_s"], "unit": "records/s",
                "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
                "steps": args.e2e_steps, "proc_ms_p50": 1e3 * pct(e["proc_s"], 50),
@@ -420,7 +428,8 @@ def main():
             "vs_baseline": None, "dtype": "u64 fixed-point sums + f64 AVG", "data": "synthetic (lmsgen, seeded)",
             "config": {"workload": wl["desc"], "records_per_batch_per_gpu": wl["records"],
                        "global_batch": wl["records"] * world, "batch_bytes_per_gpu": res["bytes_per_step"],
-                       "parallelism": f"dp{world} (row partition per rank)" if world > 1 else "single GPU",
+                       "parallelism": (f"dp{world} (row partition per rank; exchange: {args.exchange})"
+                                       if world > 1 else "single GPU"),
                        "l2": "inputs (>= 0.7 GB/step) exceed the 126 MB L2; no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(args.workload),

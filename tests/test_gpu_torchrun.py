@@ -23,13 +23,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("workload", ["cm2", "lr2"])
-def test_torchrun_two_ranks(workload):
+@pytest.mark.parametrize("workload,exchange", [("cm2", "alltoall"), ("lr2", "alltoall"), ("cm2", "p2p")])
+def test_torchrun_two_ranks(workload, exchange):
     env = dict(os.environ, LMS_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--workload", workload, "--secondary", "",
-           "--e2e-steps", "1", "--no-cpu-baseline"]
+           "--e2e-steps", "1", "--no-cpu-baseline", "--exchange", exchange]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
