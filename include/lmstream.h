@@ -111,6 +111,10 @@ typedef struct {
 } lms_config;
 
 #define LMS_FLAG_ONLINE_INFPT 0x1u  /* Eq. 10 online regression of InfPT */
+#define LMS_FLAG_PIPELINE     0x2u  /* single GPU: lms_force_batch may launch batch i+1 while
+                                       batch i still runs (two batches in flight, separate
+                                       report / row buffers); lms_sync and reads complete
+                                       them in order.  Stream order keeps window state exact. */
 
 /* One aggregate result row (LR2S, CM1S, CM1T, CM2S) of window instance
  * [win_start_s, win_end_s) (readings R5/R6 in DESIGN.md).                    */

@@ -123,7 +123,6 @@ struct lms_query {
   uint8_t* d_in[2] = {nullptr, nullptr};
   uint64_t in_cap = 0, in_used[2] = {0, 0};
   int in_cur = 0;
-  BatchReport* h_report = nullptr;
   std::vector<Pending> pending;
   uint64_t next_ds_id = 0;
   double last_ingest = -std::numeric_limits<double>::infinity();
@@ -134,14 +133,26 @@ struct lms_query {
   double infpt = 150e3;
   std::deque<std::array<double, 3>> reg_hist;
   Dag dag;
-  // in-flight batch
+  // in-flight batches: slot `cur_slot` holds the newest batch (in_flight), and with
+  // LMS_FLAG_PIPELINE the other slot may hold the previous, still running one (parked), so the
+  // host prepares and launches batch i+1 while the GPU runs batch i
+  struct Flight {
+    lms_batch_record cur{};
+    int in_buf = 0;
+    bool flush = false;
+    cudaEvent_t ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
+    BatchReport* h_report = nullptr;   // mapped pinned
+    BatchReport* d_report = nullptr;
+    void* d_rows = nullptr;            // result rows of this batch
+  };
+  Flight fl[2];
+  int cur_slot = 0;
+  bool pipeline = false;
+  bool parked = false;
   bool in_flight = false;
-  int in_flight_buf = 0;
-  bool in_flight_flush = false;
   bool awaiting_close = false;     // multi-GPU: aggregate pass launched, close not yet
   BatchReport last_report{};
-  cudaEvent_t ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
-  lms_batch_record cur{};
+  Flight& F() { return fl[cur_slot]; }
   std::vector<lms_batch_record> records;
   RowFifo<lms_agg_row> agg_rows;
   RowFifo<lms_lr1_row> lr1_rows;
@@ -157,10 +168,12 @@ struct lms_query {
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (void* p : dallocs) cudaFree(p);
-    if (h_report) cudaFreeHost(h_report);
+    for (Flight& f : fl) {
+      if (f.h_report) cudaFreeHost(f.h_report);
+      for (cudaEvent_t e : {f.ev_start, f.ev_agg, f.ev_close, f.ev_end})
+        if (e) cudaEventDestroy(e);
+    }
     if (h_count) cudaFreeHost(h_count);
-    for (cudaEvent_t e : {ev_start, ev_agg, ev_close, ev_end})
-      if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
   }
@@ -208,8 +221,11 @@ lms_status validate_config(const lms_config* c) {
 lms_status launch_close_stage(lms_query* q);
 
 lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bool flush) {
+  // the slot's report / rows buffers are what this batch's kernels write
+  q->qd.report = q->F().d_report;
+  q->qd.rows = q->F().d_rows;
   // ---- batch composition: every pending dataset (Alg. 1 admits tmpMicroBatch whole)
-  lms_batch_record& r = q->cur;
+  lms_batch_record& r = q->F().cur;
   r = lms_batch_record{};
   r.index = q->records.size();
   r.num_datasets = q->pending.size();
@@ -246,12 +262,12 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
   for (const Pending& d : q->pending)
     if (d.dptr) segs.push_back({d.dptr, d.nbytes});
   q->pending.clear();
-  q->in_flight_buf = buf;
+  q->F().in_buf = buf;
   q->in_cur ^= 1;
   q->in_used[q->in_cur] = 0;
 
   const bool lr = is_lr(q->kind);
-  CUDA_TRY(cudaEventRecord(q->ev_start, q->stream));
+  CUDA_TRY(cudaEventRecord(q->F().ev_start, q->stream));
   for (size_t s0 = 0; s0 < segs.size(); s0 += kMaxSegs) {
     SegTable t{};
     t.n = (int)std::min<size_t>(kMaxSegs, segs.size() - s0);
@@ -265,8 +281,8 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
     CUDA_TRY(lr ? launch_lr_agg(q->qd, t, q->stream) : launch_cm_agg(q->qd, t, q->stream));
     q->launches++;
   }
-  CUDA_TRY(cudaEventRecord(q->ev_agg, q->stream));
-  q->in_flight_flush = flush;
+  CUDA_TRY(cudaEventRecord(q->F().ev_agg, q->stream));
+  q->F().flush = flush;
   if (q->qd.world > 1) {            // multi-GPU: the caller all-reduces the watermark first
     q->awaiting_close = true;
     return LMS_OK;
@@ -276,7 +292,7 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
 
 // Window close (+ LR1 eviction, + multi-GPU owner bucketing), batch report, end event.
 lms_status launch_close_stage(lms_query* q) {
-  CUDA_TRY(launch_close(q->qd, q->in_flight_flush ? 1 : 0, q->stream));
+  CUDA_TRY(launch_close(q->qd, q->F().flush ? 1 : 0, q->stream));
   q->launches++;
   if (is_lr1(q->kind)) {
     CUDA_TRY(launch_lr1_evict(q->qd, q->stream));
@@ -286,25 +302,24 @@ lms_status launch_close_stage(lms_query* q) {
     CUDA_TRY(launch_bucket(q->qd, q->stream));
     q->launches += 2;
   }
-  CUDA_TRY(cudaEventRecord(q->ev_close, q->stream));
+  CUDA_TRY(cudaEventRecord(q->F().ev_close, q->stream));
   // the batch report lives in mapped pinned memory: the close kernel writes it to the host
-  CUDA_TRY(cudaEventRecord(q->ev_end, q->stream));
+  CUDA_TRY(cudaEventRecord(q->F().ev_end, q->stream));
   q->awaiting_close = false;
   q->in_flight = true;
   return LMS_OK;
 }
 
-lms_status complete(lms_query* q) {
-  if (!q->in_flight) return LMS_OK;
-  CUDA_TRY(cudaEventSynchronize(q->ev_end));
-  q->in_flight = false;
-  lms_batch_record& r = q->cur;
-  const BatchReport rep = *q->h_report;
+// Complete the batch of slot f (its end event, report, rows -> host FIFO, Eq. 4/5/10).
+lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
+  CUDA_TRY(cudaEventSynchronize(f.ev_end));
+  lms_batch_record& r = f.cur;
+  const BatchReport rep = *f.h_report;
   float ms_total = 0, ms_agg = 0, ms_close = 0, ms_end = 0;
-  CUDA_TRY(cudaEventElapsedTime(&ms_total, q->ev_start, q->ev_close));
-  CUDA_TRY(cudaEventElapsedTime(&ms_agg, q->ev_start, q->ev_agg));
-  CUDA_TRY(cudaEventElapsedTime(&ms_close, q->ev_agg, q->ev_close));
-  CUDA_TRY(cudaEventElapsedTime(&ms_end, q->ev_start, q->ev_end));
+  CUDA_TRY(cudaEventElapsedTime(&ms_total, f.ev_start, f.ev_close));
+  CUDA_TRY(cudaEventElapsedTime(&ms_agg, f.ev_start, f.ev_agg));
+  CUDA_TRY(cudaEventElapsedTime(&ms_close, f.ev_agg, f.ev_close));
+  CUDA_TRY(cudaEventElapsedTime(&ms_end, f.ev_start, f.ev_end));
   q->last_batch_s = ms_total * 1e-3;
   q->last_agg_s = ms_agg * 1e-3;
   q->last_close_s = ms_close * 1e-3;
@@ -316,7 +331,7 @@ lms_status complete(lms_query* q) {
   if (nrows) {
     const double t0 = now_host();
     // device rows -> (DMA) -> pinned host FIFO
-    const uint8_t* src = static_cast<const uint8_t*>(q->qd.rows);
+    const uint8_t* src = static_cast<const uint8_t*>(f.d_rows);
     if (is_lr1(q->kind)) {
       CUDA_TRY(q->lr1_rows.reserve(nrows));
       CUDA_TRY(cudaMemcpyAsync(q->lr1_rows.tail_ptr(), src, nrows * sizeof(lms_lr1_row), cudaMemcpyDeviceToHost, q->stream));
@@ -329,7 +344,7 @@ lms_status complete(lms_query* q) {
     else q->agg_rows.commit(nrows);
     d2h = now_host() - t0;
   }
-  q->in_used[q->in_flight_buf] = 0;
+  q->in_used[f.in_buf] = 0;
   r.num_records = rep.n_records;
   r.device_s = q->last_batch_s;
   r.d2h_s = d2h;
@@ -370,6 +385,36 @@ lms_status complete(lms_query* q) {
     st = fail(LMS_EOVERFLOW, "batch " + std::to_string(r.index) + ": capacity exceeded (pane ring, keys, rows or FIFO)");
   q->last_completion = st;
   return st;
+}
+
+// Complete the oldest in-flight batch (the parked one first).
+lms_status complete(lms_query* q) {
+  if (q->parked) {
+    q->parked = false;
+    return complete_flight(q, q->fl[q->cur_slot ^ 1]);
+  }
+  if (!q->in_flight) return LMS_OK;
+  q->in_flight = false;
+  return complete_flight(q, q->F());
+}
+
+// Complete every in-flight batch (oldest first); the first error wins.
+lms_status complete_all(lms_query* q) {
+  lms_status a = complete(q);
+  lms_status b = complete(q);
+  return a ? a : b;
+}
+
+// Pipelined launch (LMS_FLAG_PIPELINE): park the running batch in its slot and switch to the
+// other slot, completing the batch that still occupies it first.
+lms_status park_current(lms_query* q) {
+  if (!q->in_flight) return LMS_OK;
+  lms_status s = LMS_OK;
+  if (q->parked) s = complete(q);
+  q->parked = true;
+  q->in_flight = false;
+  q->cur_slot ^= 1;
+  return s;
 }
 
 }  // namespace
@@ -440,14 +485,21 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
 #define QC_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return bail(fail(LMS_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_))); } while (0)
     QC_TRY(cudaStreamCreateWithFlags(&q->stream, cudaStreamNonBlocking));
     QC_TRY(cudaStreamCreateWithFlags(&q->copy_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&q->ev_start, &q->ev_agg, &q->ev_close, &q->ev_end}) QC_TRY(cudaEventCreate(e));
-    QC_TRY(cudaHostAlloc((void**)&q->h_report, sizeof(BatchReport), cudaHostAllocMapped));
+    // pipelining (two batches in flight) only for single-GPU handles
+    q->pipeline = (cfg->flags & LMS_FLAG_PIPELINE) && cfg->world == 1;
+    const int nslots = q->pipeline ? 2 : 1;
+    for (int sl = 0; sl < nslots; sl++) {
+      lms_query::Flight& f = q->fl[sl];
+      for (cudaEvent_t* e : {&f.ev_start, &f.ev_agg, &f.ev_close, &f.ev_end}) QC_TRY(cudaEventCreate(e));
+      QC_TRY(cudaHostAlloc((void**)&f.h_report, sizeof(BatchReport), cudaHostAllocMapped));
+      std::memset(f.h_report, 0, sizeof(BatchReport));
+      QC_TRY(cudaHostGetDevicePointer((void**)&f.d_report, f.h_report, 0));   // zero-copy report
+    }
     QC_TRY(cudaHostAlloc((void**)&q->h_count, sizeof(unsigned long long), cudaHostAllocDefault));
     {   // pre-size the result FIFO (pinned, pages touched) for up to 64 K rows
       const uint64_t pre = std::min<uint64_t>(cfg->max_result_rows, 1ull << 16);
       QC_TRY(is_lr1(q->kind) ? q->lr1_rows.reserve(pre) : q->agg_rows.reserve(pre));
     }
-    std::memset(q->h_report, 0, sizeof(BatchReport));
 
     QueryDev& d = q->qd;
     d.kind = q->kind;
@@ -463,7 +515,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     d.rank = (uint32_t)cfg->rank;
     d.world = (uint32_t)cfg->world;
     Q_TRY(q->dalloc(&d.state, 1, 0));
-    QC_TRY(cudaHostGetDevicePointer((void**)&d.report, q->h_report, 0));   // zero-copy report
+    d.report = q->fl[0].d_report;
     if (d.world > 1 && !is_lr1(q->kind)) {   // owner-side merge of partial rows
       lms_agg_row* send;
       Q_TRY(q->dalloc(&send, cfg->max_result_rows, 0));
@@ -508,19 +560,24 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       Q_TRY(q->dalloc(&d.dict.key_by_idx, cfg->max_keys, 0));
     }
     d.row_cap = cfg->max_result_rows;
+    for (int sl = 0; sl < nslots; sl++) {   // result rows, one buffer per in-flight slot
+      if (is_lr1(q->kind)) {
+        lms_lr1_row* rows;
+        Q_TRY(q->dalloc(&rows, d.row_cap, 0));
+        q->fl[sl].d_rows = rows;
+      } else {
+        lms_agg_row* rows;
+        Q_TRY(q->dalloc(&rows, d.row_cap, 0));
+        q->fl[sl].d_rows = rows;
+      }
+    }
+    d.rows = q->fl[0].d_rows;
     if (is_lr1(q->kind)) {
-      lms_lr1_row* rows;
-      Q_TRY(q->dalloc(&rows, d.row_cap, 0));
-      d.rows = rows;
       // every retained row is emitted exactly once (as an L row of its pane's instance), so
       // the FIFO never needs more room than the rows one close may emit
       d.fifo_cap = cfg->max_result_rows + 1024;
       Q_TRY(q->dalloc(&d.fifo[0], d.fifo_cap, 0));
       Q_TRY(q->dalloc(&d.fifo[1], d.fifo_cap, 0));
-    } else {
-      lms_agg_row* rows;
-      Q_TRY(q->dalloc(&rows, d.row_cap, 0));
-      d.rows = rows;
     }
     q->in_cap = cfg->max_batch_bytes;
     for (int b = 0; b < 2; b++) Q_TRY(q->dalloc(&q->d_in[b], q->in_cap + 4096, 0));
@@ -564,9 +621,14 @@ lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, 
     if (!bytes) return fail(LMS_EINVAL, "null bytes");
     if (!is_lr(q->kind) && static_cast<const uint8_t*>(bytes)[nbytes - 1] != '\n')
       return fail(LMS_EINVAL, "CM dataset does not end with a newline");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    // pipelined: the staging buffer may still feed the parked (previous) batch
+    if (q->parked && q->fl[q->cur_slot ^ 1].in_buf == q->in_cur) {
+      lms_status c = complete(q);
+      if (c && c != LMS_EFORMAT && c != LMS_EOVERFLOW) return c;
+    }
     const int b = q->in_cur;
     if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
-    CUDA_TRY(cudaSetDevice(q->cfg.device));
     const double t0 = now_host();
     CUDA_TRY(cudaMemcpyAsync(q->d_in[b] + q->in_used[b], bytes, nbytes, cudaMemcpyHostToDevice, q->copy_stream));
     CUDA_TRY(cudaStreamSynchronize(q->copy_stream));
@@ -609,11 +671,13 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
     if (admitted) *admitted = 0;
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status cs = LMS_OK;
+    if (q->parked) cs = complete(q);                  // (pipelined handles polled: drain)
     if (q->in_flight) {
-      cudaError_t e = cudaEventQuery(q->ev_end);
-      if (e == cudaErrorNotReady) return LMS_OK;    // one micro-batch in flight at a time
+      cudaError_t e = cudaEventQuery(q->F().ev_end);
+      if (e == cudaErrorNotReady) return cs;        // one micro-batch in flight at a time
       if (e != cudaSuccess) return fail(LMS_ECUDA, cudaGetErrorString(e));
-      cs = complete(q);
+      lms_status c2 = complete(q);
+      cs = cs ? cs : c2;
     }
     const Mode mode = (Mode)q->cfg.mode;
     bool admit = false;
@@ -642,9 +706,9 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
     if (admit) {
       lms_status s = launch_batch(q, now, reason, est, false);
       if (s) return s;
-      q->cur.admit_overhead_s = admit_overhead;
+      q->F().cur.admit_overhead_s = admit_overhead;
       if (admitted) *admitted = 1;
-      if (bidx) *bidx = q->cur.index;
+      if (bidx) *bidx = q->F().cur.index;
     }
     return cs;
   } catch (...) {
@@ -656,14 +720,16 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
     if (bidx) *bidx = UINT64_MAX;
-    if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
+    if (q->awaiting_close || (q->in_flight && !q->pipeline))
+      return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
     // multi-GPU ranks run their batches in lockstep: an empty rank still runs the batch
     if (q->pending.empty() && q->qd.world == 1) return LMS_OK;
     CUDA_TRY(cudaSetDevice(q->cfg.device));
+    lms_status c = park_current(q);     // pipelined: the running batch keeps its slot
     lms_status s = launch_batch(q, now, kAdmitForced, std::nan(""), false);
     if (s) return s;
-    if (bidx) *bidx = q->cur.index;
-    return LMS_OK;
+    if (bidx) *bidx = q->F().cur.index;
+    return c;
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in force_batch");
   }
@@ -674,8 +740,7 @@ lms_status lms_sync(lms_query* q) {
     if (!q) return fail(LMS_EINVAL, "null query");
     if (q->awaiting_close) return fail(LMS_ESTATE, "multi-GPU batch: call lms_run_close first");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
-    if (!q->in_flight) return LMS_OK;
-    return complete(q);
+    return complete_all(q);
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in sync");
   }
@@ -686,11 +751,11 @@ lms_status lms_flush(lms_query* q, double now) {
     if (!q) return fail(LMS_EINVAL, "null query");
     if (q->awaiting_close) return fail(LMS_ESTATE, "multi-GPU batch: call lms_run_close first");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
-    lms_status s1 = complete(q);
+    lms_status s1 = complete_all(q);
     lms_status s = launch_batch(q, now, kAdmitFlush, std::nan(""), true);
     if (s) return s;
     if (q->qd.world > 1) return s1;   // the caller completes the multi-GPU protocol
-    lms_status s2 = complete(q);
+    lms_status s2 = complete_all(q);
     return s2 ? s2 : s1;
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in flush");
@@ -778,7 +843,7 @@ lms_status lms_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) {
       const long long W = (long long)s.wm - 1, R = q->qd.R, S = q->qd.S;
       auto fdiv = [](long long a, long long b) { long long d = a / b; return (a % b != 0 && ((a < 0) != (b < 0))) ? d - 1 : d; };
       *k_first = s.next_k_valid ? s.next_k : fdiv((long long)s.ts_min - R, S) + 1;
-      *k_last = q->in_flight_flush ? fdiv(W, S) : fdiv(W - R, S);
+      *k_last = q->F().flush ? fdiv(W, S) : fdiv(W - R, S);
     }
     return LMS_OK;
   } catch (...) {

@@ -3,9 +3,12 @@
 # kernel path (CM fast + general decode, malformed records, LR, LR1, close, multi-GPU kernels).
 OUT=gpurun_out/${1:-sanitizer}
 mkdir -p $OUT
-SEL='tests/test_gpu_parity.py::test_cm_fast_path_fuzz tests/test_gpu_parity.py::test_malformed_records_counted_and_dropped tests/test_gpu_parity.py::test_cm_field_shape_variants tests/test_gpu_parity.py::test_empty_flush_and_tiny_batches tests/test_gpu_parity.py::test_many_segments_more_than_one_launch tests/test_gpu_dist.py'
+SEL='tests/test_gpu_parity.py::test_cm_fast_path_fuzz tests/test_gpu_parity.py::test_malformed_records_counted_and_dropped tests/test_gpu_parity.py::test_cm_field_shape_variants tests/test_gpu_parity.py::test_empty_flush_and_tiny_batches tests/test_gpu_parity.py::test_many_segments_more_than_one_launch tests/test_gpu_dist.py::test_virtual_shards_lr1_match_oracle'
 for tool in memcheck synccheck racecheck; do
   timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python -m pytest $SEL -q -x \
-    -k "not U(0.8) and not R(0.2" > $OUT/$tool.txt 2>&1
+    > $OUT/$tool.txt 2>&1
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python -m pytest -q -x \
+    "tests/test_gpu_dist.py::test_virtual_shards_match_oracle[CM2S-B(1.3)-2-p2p]" \
+    "tests/test_gpu_dist.py::test_virtual_shards_match_oracle[LR2S-B(1.7)-2-alltoall]" >> $OUT/$tool.txt 2>&1
   tail -3 $OUT/$tool.txt
 done
