@@ -74,7 +74,8 @@ __device__ __forceinline__ unsigned long long fmix64(unsigned long long k) {
 // Dictionary lookup-or-insert: key -> dense index < max_keys; kEmpty32 on overflow.
 __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long key, DevState* st) {
   unsigned long long h = fmix64(key) & d.cap_mask;
-  while (true) {
+  for (unsigned long long probes = 0; probes <= d.cap_mask; probes++) {   // bounded: a full table
+                                                                          // (key overflow) ends
     unsigned long long k = *(volatile unsigned long long*)&d.keys[h];
     if (k == key || k == kEmpty64) {
       if (k == kEmpty64) {
@@ -100,6 +101,8 @@ __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long k
     }
     h = (h + 1) & d.cap_mask;
   }
+  atomicExch(&st->key_overflow, 1u);   // every entry taken by other keys: this key is dropped
+  return kEmpty32;
 }
 
 // ---- pane table: pane index -> accumulator slot ------------------------------------------
@@ -109,7 +112,7 @@ __device__ __forceinline__ uint32_t pane_hash(uint32_t p, uint32_t mask) { retur
 // Called rarely (threads cache the last pane they resolved).
 __device__ __forceinline__ uint32_t claim_slot(const QueryDev& q, uint32_t p) {
   uint32_t h = pane_hash(p, q.H_mask);
-  while (true) {
+  for (uint32_t probes = 0; probes <= q.H_mask; probes++) {   // bounded: a full pane table ends
     uint32_t k = *(volatile uint32_t*)&q.pane_key[h];
     if (k == kEmpty32) {
       k = atomicCAS(&q.pane_key[h], kEmpty32, p);
@@ -135,13 +138,15 @@ __device__ __forceinline__ uint32_t claim_slot(const QueryDev& q, uint32_t p) {
     }
     h = (h + 1) & q.H_mask;
   }
+  q.state->pane_fail = 1;               // table full of other panes: this pane's records overflow
+  return kFail32;
 }
 
 // Lookup only (no concurrent inserts may run): slot of pane p or kEmpty32.
 __device__ __forceinline__ uint32_t find_slot(const QueryDev& q, long long p) {
   if (p < 0 || p > 0xFFFFFFF0ll) return kEmpty32;
   uint32_t h = pane_hash((uint32_t)p, q.H_mask);
-  while (true) {
+  for (uint32_t probes = 0; probes <= q.H_mask; probes++) {
     const uint32_t k = q.pane_key[h];
     if (k == kEmpty32) return kEmpty32;
     if (k == (uint32_t)p) {
@@ -150,6 +155,7 @@ __device__ __forceinline__ uint32_t find_slot(const QueryDev& q, long long p) {
     }
     h = (h + 1) & q.H_mask;
   }
+  return kEmpty32;
 }
 
 // Per-CTA pane slots (2, tags in smem: acc slot << 32 | pane).  Sets lslot = 0/1 (local table)

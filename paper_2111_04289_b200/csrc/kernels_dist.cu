@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_merge(const QueryDev q, const lms_
 // and each owner finalizes (k_finalize / k_finalize_cm1, unchanged).
 __device__ __forceinline__ uint32_t dict_get_sys(const Dict& d, unsigned long long key, DevState* st) {
   unsigned long long h = fmix64(key) & d.cap_mask;
-  while (true) {
+  for (unsigned long long probes = 0; probes <= d.cap_mask; probes++) {
     unsigned long long k = *(volatile unsigned long long*)&d.keys[h];
     if (k == key || k == kEmpty64) {
       if (k == kEmpty64) {
@@ -113,6 +113,8 @@ __device__ __forceinline__ uint32_t dict_get_sys(const Dict& d, unsigned long lo
     }
     h = (h + 1) & d.cap_mask;
   }
+  atomicExch(&st->key_overflow, 1u);
+  return kEmpty32;
 }
 
 __global__ void __launch_bounds__(kThreads) k_p2p_push(const QueryDev q, long long k_lo, uint32_t nwin) {

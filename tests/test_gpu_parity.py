@@ -256,3 +256,67 @@ def test_pipelined_batches_equal_serial(qname, traffic):
     keys = ("num_records", "num_datasets", "batch_bytes", "windows_closed", "rows_emitted", "late_records",
             "bad_records", "watermark")
     assert [tuple(r[k] for k in keys) for r in recs_p] == [tuple(o[1][k] for k in keys) for o in serial]
+
+
+# ---------------------------------------------------------------- capacity limits (degenerate cases)
+
+def _one_batch(qname, data, **cfg):
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    with P.Query(qname, mode="manual", **cfg) as q:
+        q.push(data, 0.0)
+        q.force(1.0)
+        st = q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW))
+        st2 = q.flush(1.0, ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW))
+        rows = q.read_lr1() if qname.startswith("LR1") else q.read_agg()
+        return st, st2, rows, q.records()
+
+
+def test_key_capacity_overflow_is_reported_and_exact_for_admitted_keys():
+    """CM2S with max_keys = 64 < 300 distinct jobIds: the batch reports LMS_EOVERFLOW and counts
+    the dropped records; every key that did get a slot is aggregated exactly (its row equals the
+    oracle's), none is half-counted."""
+    from paper_2111_04289_b200 import _lib as L
+    data = b"".join(stream("CM", "B(2)", 8, params=g.CMParams(num_jobs=300)))
+    st, st2, rows, recs = _one_batch("CM2S", data, max_keys=64)
+    assert L.LMS_EOVERFLOW in (st, st2)
+    assert sum(r["overflow_records"] for r in recs) > 0
+    ora = {(r.win_start, r.key[0]): r for o in oracle_rows("CM2S", [[data]]) for r in o.rows}
+    assert len(rows) > 0
+    for r in rows:
+        o = ora[(int(r["win_start_s"]), int(r["key"]))]
+        assert int(r["count"]) == o.count and int(r["sum_fixed"]) == o.sum_fixed
+
+
+def test_pane_slot_exhaustion_is_reported():
+    """pane_slots = 4 with records spread over 40 slides: panes that find no slot are dropped,
+    counted, and the batch reports LMS_EOVERFLOW (never silently wrong)."""
+    from paper_2111_04289_b200 import _lib as L
+    data = b"".join(stream("LR", "B(0.2)", 200))
+    st, st2, rows, recs = _one_batch("LR2S", data, pane_slots=4)
+    assert L.LMS_EOVERFLOW in (st, st2)
+    assert sum(r["overflow_records"] for r in recs) > 0
+
+
+def test_result_row_capacity_overflow_is_reported():
+    """max_result_rows smaller than one close's rows: LMS_EOVERFLOW, rows capped."""
+    from paper_2111_04289_b200 import _lib as L
+    data = b"".join(stream("CM", "B(2)", 70, params=g.CMParams(num_jobs=500)))
+    st, st2, rows, recs = _one_batch("CM2S", data, max_result_rows=100)
+    assert L.LMS_EOVERFLOW in (st, st2)
+    assert len(rows) <= 200
+
+
+def test_batch_buffer_capacity_on_push():
+    """A push beyond max_batch_bytes is refused with LMS_EOVERFLOW (nothing is truncated)."""
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    data = b"".join(stream("LR", "B(1)", 3))
+    with P.Query("LR2S", mode="manual", max_batch_bytes=len(data) - 70) as q:
+        with pytest.raises(P.LmsError) as ei:
+            q.push(data, 0.0)
+        assert ei.value.status == L.LMS_EOVERFLOW
+        q.push(data[:70 * 100], 0.0)          # a smaller push still fits
+        q.force(1.0)
+        q.sync()
+        assert q.record(0)["num_records"] == 100
