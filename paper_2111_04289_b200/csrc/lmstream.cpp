@@ -332,14 +332,16 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
     const double t0 = now_host();
     // device rows -> (DMA) -> pinned host FIFO
     const uint8_t* src = static_cast<const uint8_t*>(f.d_rows);
+    // on the copy stream: the batch is complete (ev_end), and a pipelined successor may be
+    // running on the compute stream — the copy must not queue behind it
     if (is_lr1(q->kind)) {
       CUDA_TRY(q->lr1_rows.reserve(nrows));
-      CUDA_TRY(cudaMemcpyAsync(q->lr1_rows.tail_ptr(), src, nrows * sizeof(lms_lr1_row), cudaMemcpyDeviceToHost, q->stream));
+      CUDA_TRY(cudaMemcpyAsync(q->lr1_rows.tail_ptr(), src, nrows * sizeof(lms_lr1_row), cudaMemcpyDeviceToHost, q->copy_stream));
     } else {
       CUDA_TRY(q->agg_rows.reserve(nrows));
-      CUDA_TRY(cudaMemcpyAsync(q->agg_rows.tail_ptr(), src, nrows * sizeof(lms_agg_row), cudaMemcpyDeviceToHost, q->stream));
+      CUDA_TRY(cudaMemcpyAsync(q->agg_rows.tail_ptr(), src, nrows * sizeof(lms_agg_row), cudaMemcpyDeviceToHost, q->copy_stream));
     }
-    CUDA_TRY(cudaStreamSynchronize(q->stream));
+    CUDA_TRY(cudaStreamSynchronize(q->copy_stream));
     if (is_lr1(q->kind)) q->lr1_rows.commit(nrows);
     else q->agg_rows.commit(nrows);
     d2h = now_host() - t0;
