@@ -246,6 +246,15 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   const uint32_t P = q.P;
   __shared__ uint32_t wslots[256];   // R/S <= 256
 
+  // Most batches close no window (slide S > batch span): nothing to merge (CM: the aggregate
+  // pass wrote the pane accumulators directly), emit or evict — CTA 0 alone advances the state.
+  // (finish() leaves wm / next_k as they are when nothing closes, so a late CTA that reads the
+  // state after it computes the same empty range.)
+  if (q.kind != kLR2S && !(w.any && w.k_last >= w.nk)) {
+    if (blockIdx.x == 0) finish(q, w);
+    return;
+  }
+
   // 1. merge LR2 partials of this batch into the pane accumulators (my key slice)
   if (q.kind == kLR2S) merge_partials(q, k0, k1);
   __syncthreads();
