@@ -440,8 +440,8 @@ __device__ __forceinline__ uint32_t swar4d(uint32_t d) {
 // record has that shape AND is valid under reading R1 (then r holds its fields); false means
 // "not decided here": the caller re-parses the record with the exact general path (cm_parse),
 // so the fast path never rejects anything itself.  sb / e: mask bits of the record start and
-// of its '\n'.  Every smem address is clamped into the stage so that predicated-off garbage
-// positions cannot fault.
+// of its '\n' (sb <= 4096).  Every smem address stays inside the stage (see `ec`), so that
+// predicated-off garbage positions cannot fault.
 __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
@@ -453,7 +453,11 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   const uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
   const uint32_t m0 = __funnelshift_r(v2, v3, sh) & low_bits(min(L - 128u, 32u));
   const uint32_t m1 = __funnelshift_r(v3, v4, sh) & low_bits(clamp32((int)L - 160));
-  const uint32_t tp = min(max(e, 64u) - 64u, (uint32_t)(kMaskBits - 64));
+  // e clamped into the window for addressing only (e = 0xFFFF: no '\n' in reach; L above
+  // already rejects it): with S <= 16 + 4096 and o0, a4, q7 < 35 every load below stays
+  // inside the stage, so no address needs its own clamp
+  const uint32_t ec = min(max(e, 64u), (uint32_t)kMaskBits - 1u);
+  const uint32_t tp = ec - 64u;
   const uint32_t* u = cm32 + (tp >> 5);
   const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
   const uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
@@ -475,12 +479,11 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   ok &= (t1 >> 2) == 0x10080402u;
   const uint32_t pc = __funnelshift_r(t0, t1, 30u) & 0x1Fu;
   ok &= pc == 0x0Au || pc == 0x05u;
-  const uint32_t cat_at = kCmHaloL + e - (pc == 0x0Au ? 32u : 33u);  // c6 + 1
+  const uint32_t cat_at = kCmHaloL + ec - (pc == 0x0Au ? 32u : 33u);  // c6 + 1
   // ---- fields (digit checks accumulate into bad; bit 7 of a byte = not a digit)
-  const uint32_t lim = kCmStage - 12u;
   // ts: the 8 bytes ending at c0; the (8 - o0) bytes before the digits become '0'
   uint32_t a0, a1;
-  load8(buf, min(S + o0 - 8u, lim), a0, a1);
+  load8(buf, S + o0 - 8u, a0, a1);
   const unsigned long long pm = (~0ull >> (min(max(8u * o0, 8u), 64u) - 1u)) >> 1;   // ~0 >> 8*o0
   const uint32_t pm0 = (uint32_t)pm, pm1 = (uint32_t)(pm >> 32);
   const uint32_t da0 = ((a0 & ~pm0) | (0x30303030u & pm0)) - 0x30303030u;
@@ -489,7 +492,7 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   r.ts = swar4d(da0) * 10000u + swar4d(da1);
   // jobId: 10 digits at c1 + 1 = S + o0 + 2
   uint32_t d0, d1, d2;
-  load12(buf, min(S + o0 + 2u, lim), d0, d1, d2);
+  load12(buf, S + o0 + 2u, d0, d1, d2);
   d0 -= 0x30303030u;
   d1 -= 0x30303030u;
   d2 -= 0x30303030u;
@@ -497,13 +500,13 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   const uint32_t lo2 = __byte_perm(d2 * 0xA01u, 0u, 0x4441u);     // 10 * d2_0 + d2_1
   r.job = (unsigned long long)(swar4d(d0) * 10000u + swar4d(d1)) * 100ull + lo2;
   // eventType at c4 + 1 = S + o0 + 14 + a4; category at c6 + 1
-  r.event = (uint32_t)buf[min(S + o0 + 14u + a4, lim)] - 48u;
-  r.cat = (uint32_t)buf[min(cat_at, lim)] - 48u;
+  r.event = (uint32_t)buf[S + o0 + 14u + a4] - 48u;
+  r.cat = (uint32_t)buf[cat_at] - 48u;
   ok &= r.event <= 9u && r.cat <= 9u;
   // cpu = D.DDDDDD at c8 + 1 = e - 28: the '.' is swapped for '0' for the digit check and
   // SWAR value (D0DD DDDD), and the integer digit's weight is fixed up (10^7 -> 10^6)
   uint32_t p0, p1;
-  load8(buf, min(kCmHaloL + e - 28u, lim), p0, p1);
+  load8(buf, kCmHaloL + ec - 28u, p0, p1);
   ok &= ((p0 >> 8) & 0xFFu) == '.';
   const uint32_t dp0 = (p0 ^ 0x1E00u) - 0x30303030u, dp1 = p1 - 0x30303030u;
   bad |= dbad(dp0) | dbad(dp1);
