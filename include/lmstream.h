@@ -115,6 +115,10 @@ typedef struct {
                                        batch i still runs (two batches in flight, separate
                                        report / row buffers); lms_sync and reads complete
                                        them in order.  Stream order keeps window state exact. */
+#define LMS_FLAG_DENSE_VEHICLES 0x4u /* LR1: vehicle ids index the per-pane counts directly
+                                       (VID < max_keys; larger VIDs are dropped and counted as
+                                       overflow) instead of the key dictionary.  Always on for
+                                       multi-GPU LR1.                                       */
 
 /* One aggregate result row (LR2S, CM1S, CM1T, CM2S) of window instance
  * [win_start_s, win_end_s) (readings R5/R6 in DESIGN.md).                    */

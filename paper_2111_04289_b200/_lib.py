@@ -29,6 +29,7 @@ LMS_MODE_LMSTREAM, LMS_MODE_DEADLINE, LMS_MODE_TRIGGER, LMS_MODE_MANUAL = range(
 MODE = {"lmstream": 0, "deadline": 1, "trigger": 2, "manual": 3}
 LMS_FLAG_ONLINE_INFPT = 1
 LMS_FLAG_PIPELINE = 2
+LMS_FLAG_DENSE_VEHICLES = 4
 LMS_OP_SCAN, LMS_OP_FILTER, LMS_OP_PROJECT, LMS_OP_HASHAGG, LMS_OP_HASHJOIN, LMS_OP_SORT, \
     LMS_OP_SHUFFLE, LMS_OP_EXPAND = range(8)
 LMS_DEV_CPU, LMS_DEV_GPU = 0, 1

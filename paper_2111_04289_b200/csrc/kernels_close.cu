@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
     Lr1Retained r{};
     long long k = 0;
     uint32_t m = 0;
-    if (i < n) {
+    if (i < n && src[i].vidx != kEmpty32) {      // (holes: records the aggregate pass dropped)
       r = src[i];
       const long long p = (long long)pane_of(r.ts, q.S, q.div_magic);
       k = p - (long long)q.ppw + 1;              // instance whose newest slide is pane p
@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_probe(const QueryDev q, l
     const uint32_t i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
     bool emit = false, keep = false;
     Lr1Retained r{};
-    if (i < n) {
+    if (i < n && src[i].vidx != kEmpty32) {
       r = src[i];
       const long long p = (long long)pane_of(r.ts, q.S, q.div_magic);
       emit = p - (long long)q.ppw + 1 == k;      // instance whose newest slide is pane p

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kLrStages];
   __shared__ unsigned long long slot_tag[2], loaded_tag[2];
+  __shared__ uint32_t s_fbase, s_fcur;      // LR1: this tile's reserved FIFO range
   const QueryDev& q = a.q;
   uint8_t* stage = smem;
   uint32_t* tsum = reinterpret_cast<uint32_t*>(smem + kLrStages * kLrTileBytes);   // [2][K]
@@ -167,7 +168,14 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
     const uint32_t bytes = (uint32_t)(rem < (unsigned long long)kLrTileBytes ? rem : kLrTileBytes);
     const uint32_t nrec = bytes / kLrRecBytes;
     uint8_t* buf = stage + s * kLrTileBytes;
+    if (kLR1) {   // one FIFO reservation per tile (was one contended atomic per warp and record)
+      if (tid == 0) {
+        s_fcur = q.state->fifo_cur;
+        s_fbase = atomicAdd(&q.state->fifo_count[s_fcur], nrec);
+      }
+    }
     mbar_wait(&full[s], ph);
+    if (kLR1) __syncthreads();
     if (bytes & 15u) {   // segment tail: copy the last < 16 bytes by hand (uniform branch)
       const uint32_t bulk = bytes & ~15u;
       if ((uint32_t)tid < bytes - bulk) buf[bulk + tid] = a.segs.s[si].ptr[off + bulk + tid];
@@ -191,6 +199,36 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
         const LrRec& r = rr[h];
         // Linear Road domains (reading R1): Dir in {0,1}, Seg <= 99, XWay < num_xways
         const bool valid = ((ok >> h) & 1u) && r.dir <= 1u && r.seg <= 99u && r.xway < q.num_xways;
+        if (kLR1) {
+          // LR1: vehicle count of the record's pane + its projected row in the retained FIFO
+          // at the tile's reserved position (a hole, vidx = kEmpty32, for a dropped record)
+          uint32_t vidx = kEmpty32;
+          if (!valid) cnt.bad++;
+          else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;   // R7
+          else {
+            cnt.ts_min = min(cnt.ts_min, r.ts);
+            cnt.ts_max1 = max(cnt.ts_max1, r.ts + 1u);
+            const uint32_t p = pane_of(r.ts, q.S, q.div_magic);
+            if (p != c_pane) { c_pane = p; c_gslot = claim_slot(q, p); }
+            // lr1_dense (multi-GPU, LMS_FLAG_DENSE_VEHICLES): the vehicle id is the index
+            vidx = c_gslot == kFail32 ? kEmpty32
+                 : q.lr1_dense ? (r.vid < K ? (uint32_t)r.vid : kEmpty32)
+                               : dict_get(q.dict, r.vid, q.state);
+            if (vidx == kEmpty32) cnt.overflow++;
+            else atomicAdd(&q.acc_cnt32[(size_t)c_gslot * K + vidx], 1u);
+          }
+          const uint32_t pos = s_fbase + recA + h;
+          if (pos < q.fifo_cap) {
+            Lr1Retained row;
+            row.ts = r.ts; row.vidx = vidx; row.speed = (uint16_t)r.speed; row.xway = (uint16_t)r.xway;
+            row.seg = (uint16_t)r.seg; row.lane = (uint8_t)r.lane; row.dir = (uint8_t)r.dir;
+            q.fifo[s_fcur][pos] = row;
+          } else if (vidx != kEmpty32) {
+            atomicExch(&q.state->fifo_overflow, 1u);
+            cnt.overflow++;
+          }
+          continue;
+        }
         if (!valid) { cnt.bad++; continue; }
         if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) { cnt.late++; continue; }   // R7
         cnt.ts_min = min(cnt.ts_min, r.ts);
@@ -210,31 +248,6 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
             const size_t g = (size_t)c_gslot * K + key;
             atomicAdd(&q.acc_sum[g], (unsigned long long)r.speed);
             atomicAdd(&q.acc_cnt[g], 1ull);
-          }
-        } else {
-          if (p != c_pane) { c_pane = p; c_gslot = claim_slot(q, p); }
-          // multi-GPU (lr1_dense): the vehicle id is the index, identical on every rank
-          uint32_t vidx = c_gslot == kFail32 ? kEmpty32
-                        : q.lr1_dense ? (r.vid < K ? (uint32_t)r.vid : kEmpty32)
-                                      : dict_get(q.dict, r.vid, q.state);
-          if (vidx == kEmpty32) { cnt.overflow++; continue; }
-          atomicAdd(&q.acc_cnt32[(size_t)c_gslot * K + vidx], 1u);
-          // projection into the retained FIFO (one atomic per warp)
-          const uint32_t cur = q.state->fifo_cur;
-          const uint32_t m = __activemask();
-          const uint32_t lane = tid & 31, leader = __ffs(m) - 1;
-          uint32_t base = 0;
-          if (lane == leader) base = atomicAdd(&q.state->fifo_count[cur], __popc(m));
-          base = __shfl_sync(m, base, leader);
-          const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-          if (pos < q.fifo_cap) {
-            Lr1Retained row;
-            row.ts = r.ts; row.vidx = vidx; row.speed = (uint16_t)r.speed; row.xway = (uint16_t)r.xway;
-            row.seg = (uint16_t)r.seg; row.lane = (uint8_t)r.lane; row.dir = (uint8_t)r.dir;
-            q.fifo[cur][pos] = row;
-          } else {
-            atomicExch(&q.state->fifo_overflow, 1u);
-            cnt.overflow++;
           }
         }
       }

@@ -539,10 +539,8 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     }
     if (is_lr1(q->kind)) {
       Q_TRY(q->dalloc(&d.acc_cnt32, (size_t)q->P * d.K, 0));
-      if (d.world > 1) {              // vehicle-indexed counts + the all-reduced window counts
-        d.lr1_dense = 1;
-        Q_TRY(q->dalloc(&d.lr1_w, d.K, 0));
-      }
+      if (d.world > 1 || (cfg->flags & LMS_FLAG_DENSE_VEHICLES)) d.lr1_dense = 1;   // vehicle-indexed counts
+      if (d.world > 1) Q_TRY(q->dalloc(&d.lr1_w, d.K, 0));    // + the all-reduced window counts
     } else {
       Q_TRY(q->dalloc(&d.acc_sum, (size_t)q->P * d.K, 0));
       Q_TRY(q->dalloc(&d.acc_cnt, (size_t)q->P * d.K, 0));

@@ -320,3 +320,14 @@ def test_batch_buffer_capacity_on_push():
         q.force(1.0)
         q.sync()
         assert q.record(0)["num_records"] == 100
+
+
+@pytest.mark.parametrize("qname,traffic", [("LR1S", "B(0.4)"), ("LR1T", "B(0.3)")])
+def test_lr1_dense_vehicles_match_oracle(qname, traffic):
+    """LMS_FLAG_DENSE_VEHICLES (vehicle ids index the counts, no dictionary): same rows as the
+    oracle for VIDs < max_keys (the generator's V = 10^6 < 2^20)."""
+    from paper_2111_04289_b200 import _lib as L
+    secs = stream("LR", traffic, 65, params=g.LRParams(num_vehicles=400))
+    batches = split(secs, [7, 11, 3, 30])
+    compare_run(qname, product_run(qname, batches, flags=L.LMS_FLAG_DENSE_VEHICLES),
+                oracle_rows(qname, batches))

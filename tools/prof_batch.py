@@ -17,10 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cm2")
 ap.add_argument("--batches", type=int, default=3)
 ap.add_argument("--records", type=int, default=10_000_000)
+ap.add_argument("--flags", type=int, default=0)
 a = ap.parse_args()
 kind, fam = {"cm2": ("CM2S", "CM"), "lr2": ("LR2S", "LR"), "cm1": ("CM1S", "CM"), "lr1": ("LR1S", "LR")}[a.workload]
 bufs = [gcu.second_tensor(fam, t, a.records) for t in range(a.batches)]
-q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=max(1 << 20, 2 * a.records))
+q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=max(1 << 20, 2 * a.records),
+            flags=a.flags)
 for t, (b, n) in enumerate(bufs):
     q.push_device(b.data_ptr(), n, float(t))
     q.force(t + 1.0)
