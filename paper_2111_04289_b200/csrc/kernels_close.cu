@@ -106,7 +106,7 @@ __device__ void evict_rebuild_cta(const QueryDev& q, long long upto) {
 }
 
 // Last CTA (all threads): state advance + report.
-__device__ void finish(const QueryDev& q, const WinRange& w) {
+__device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = true) {
   DevState* st = q.state;
   const bool lr1 = (q.kind == kLR1S || q.kind == kLR1T);
   if (q.kind == kLR2S)
@@ -129,7 +129,7 @@ __device__ void finish(const QueryDev& q, const WinRange& w) {
       st->next_k = w.k_last + 1 > w.nk ? w.k_last + 1 : w.nk;
       st->next_k_valid = 1;
     }
-    if (lr1) {
+    if (lr1 && swap_fifo) {
       st->fifo_count[st->fifo_cur] = 0;
       st->fifo_cur ^= 1u;
     }
@@ -378,6 +378,12 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
   const QueryDev& q = a.q;
   DevState* st = q.state;
   const WinRange w = win_range(q, a.flush);
+  // no instance closes (most batches): the retained rows all stay — leave the FIFO as it is
+  // instead of copying every row into the other FIFO; CTA 0 advances the state
+  if (!(w.any && w.k_last >= w.nk)) {
+    if (blockIdx.x == 0) finish(q, w, false);
+    return;
+  }
   const uint32_t cur = st->fifo_cur;
   const uint32_t n = min((unsigned long long)st->fifo_count[cur], q.fifo_cap);
   const Lr1Retained* src = q.fifo[cur];

@@ -21,8 +21,9 @@ ap.add_argument("--flags", type=int, default=0)
 a = ap.parse_args()
 kind, fam = {"cm2": ("CM2S", "CM"), "lr2": ("LR2S", "LR"), "cm1": ("CM1S", "CM"), "lr1": ("LR1S", "LR")}[a.workload]
 bufs = [gcu.second_tensor(fam, t, a.records) for t in range(a.batches)]
-q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=max(1 << 20, 2 * a.records),
-            flags=a.flags)
+# LR1 keeps every record of the current slide in its retained FIFO: room for 8 batches
+rows_cap = max(1 << 20, (8 if kind.startswith("LR1") else 2) * a.records)
+q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=rows_cap, flags=a.flags)
 for t, (b, n) in enumerate(bufs):
     q.push_device(b.data_ptr(), n, float(t))
     q.force(t + 1.0)
