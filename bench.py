@@ -365,9 +365,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--seed", type=int, default=211104289)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "p2p"],
-                    help="N > 1: partial-aggregate exchange (NCCL all-to-all + owner merge, or the fused "
-                         "peer-memory push into the owners' accumulators)")
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "p2p", "p2p-async"],
+                    help="N > 1: partial-aggregate exchange (NCCL all-to-all + owner merge; the fused "
+                         "peer-memory push into the owners' accumulators with host-driven passes; or "
+                         "the same fully enqueued with a device-side barrier)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -393,7 +394,7 @@ def main():
     from paper_2111_04289_b200 import build  # noqa: F401  (library must already be built)
 
     seed = args.seed + 7919 * rank        # each rank: its own partition of the global batch
-    p2p = args.exchange == "p2p"
+    p2p = {"alltoall": False, "p2p": True, "p2p-async": "async"}[args.exchange]
     res = device_run(wl, args.steps, args.warmup, seed, rank, world, torch, dist, p2p)
     el = res["elapsed_s"]
     if world > 1:

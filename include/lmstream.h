@@ -295,6 +295,19 @@ lms_status  lms_merge_window(lms_query* q, uint32_t* wmerge);
 lms_status  lms_last_close_range(lms_query* q, int64_t* k_first, int64_t* k_last);
 lms_status  lms_p2p_push(lms_query* q, int64_t k_lo, uint32_t nwin);
 lms_status  lms_p2p_finalize(lms_query* q, int64_t k_lo, uint32_t nwin);
+/* Fully device-side variant (no host round trip inside the batch): after lms_run_close, and
+ * without lms_sync, lms_p2p_exchange_async enqueues on the handle's stream: push of the
+ * partials of the close's instances (at most lms_merge_window of them) into the owners'
+ * accumulators -> device barrier (every rank bumps every rank's arrival counter through peer
+ * memory; the owner's finalize waits for world arrivals) -> owner finalize -> completion
+ * signal to every rank (the next exchange's pushes wait for it).  A batch that closes nothing
+ * does nothing (identical on every rank).  lms_p2p_collect then completes the batch (the one
+ * host synchronisation) and moves the owner's final rows to the host FIFO; instances beyond
+ * the merge window (a long flush) are left to lms_p2p_push / lms_p2p_finalize passes
+ * (lms_last_close_range).  Waits are bounded (20 s): a missing peer gives LMS_ECUDA, never a
+ * hang.  ESTATE: not after lms_run_close, or a previous exchange not collected.            */
+lms_status  lms_p2p_exchange_async(lms_query* q);
+lms_status  lms_p2p_collect(lms_query* q);
 
 /* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
  * index the per-pane counts directly (VID < max_keys; larger VIDs count as overflow), every

@@ -59,6 +59,10 @@ struct DevState {
   unsigned long long part_rows;            // partial rows of the last close (multi-GPU)
   unsigned int owner_count[kMaxWorld];     // partial rows per owner rank
   unsigned int owner_cursor[kMaxWorld];
+  // fused exchange, device-side barrier: every rank adds 1 to every rank's p2p_arrive when its
+  // pushes of an exchange are done, and to every rank's p2p_done when its finalize is done;
+  // p2p_gen counts the exchanges that had instances to close (identical on every rank)
+  unsigned int p2p_arrive, p2p_done, p2p_gen, p2p_err, p2p_ticket;
 };
 
 // Copied to the host after every batch.
@@ -161,6 +165,7 @@ cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st);
 cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cudaStream_t st);
+cudaError_t launch_p2p_exchange_async(const QueryDev& q, cudaStream_t st);
 int close_ctas(const QueryDev& q);
 
 }  // namespace lms

@@ -138,6 +138,100 @@ __global__ void __launch_bounds__(kThreads) k_p2p_push(const QueryDev q, long lo
   __threadfence_system();
 }
 
+// The instances of the last close, clamped to one merge window (async exchange: nwin == 0
+// on the host side; flushes with more instances use the host-driven passes).
+__device__ __forceinline__ void close_window(const QueryDev& q, long long& k_lo, uint32_t& nwin) {
+  const long long k0 = q.state->close_k_first, k1 = q.state->close_k_last;
+  k_lo = k0;
+  nwin = k1 >= k0 ? (uint32_t)min(k1 - k0 + 1, (long long)q.Wmerge) : 0u;
+}
+
+// ---- device-side barrier of the fused exchange (no host round trip) ----------------------
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Thread 0 spins until *c >= target (bounded: 20 s, then the error flag is raised and the
+// exchange proceeds — results of that batch are reported as failed, nothing hangs).
+__device__ __forceinline__ void spin_until(DevState* st, const unsigned int* c, unsigned int target) {
+  const unsigned long long t0 = gtimer();
+  while (*(volatile const unsigned int*)c < target) {
+    if (gtimer() - t0 > 20000000000ull) { atomicExch(&st->p2p_err, 1u); break; }
+    __nanosleep(256);
+  }
+  __threadfence_system();
+}
+// +1 on counter `which` (0 arrive, 1 done) of every rank, after this rank's writes are visible.
+__device__ __forceinline__ void signal_all(const QueryDev& q, int which) {
+  __threadfence_system();
+  for (uint32_t r = 0; r < q.world; r++) {
+    DevState* ps = q.peers[r].state;
+    atomicAdd_system(which == 0 ? &ps->p2p_arrive : &ps->p2p_done, 1u);
+  }
+}
+
+// Async fused exchange, step 1 (every CTA): wait until every owner finished the previous
+// exchange's finalize (it zeroes what it reads), push this rank's partials of the last close's
+// instances into the owners' accumulators; the last CTA signals arrival to every rank.
+__global__ void __launch_bounds__(kThreads) k_p2p_push_async(const QueryDev q) {
+  DevState* st = q.state;
+  long long k_lo;
+  uint32_t nwin;
+  close_window(q, k_lo, nwin);
+  if (nwin == 0) return;                      // no instance closed (same on every rank)
+  const unsigned int gen = st->p2p_gen;       // exchanges with instances before this one
+  __shared__ bool last;
+  if (threadIdx.x == 0) spin_until(st, &st->p2p_done, gen * q.world);
+  __syncthreads();
+  const unsigned long long n = st->part_rows;
+  const lms_agg_row* rows = reinterpret_cast<const lms_agg_row*>(q.send_rows);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const lms_agg_row r = rows[i];
+    const long long w = floor_div(r.win_start_s, (long long)q.S) - k_lo;
+    if (w < 0 || w >= (long long)nwin) continue;
+    const PeerView P = q.peers[owner_of(q, r)];
+    uint32_t idx;
+    if (q.kind == kCM2S) idx = dict_get_sys(P.dict, r.key, P.state);
+    else idx = (uint32_t)r.key;
+    if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
+    const size_t g = (size_t)w * q.K + idx;
+    atomicAdd(&P.macc_sum[g], r.sum_fixed);
+    atomicAdd(&P.macc_cnt[g], r.count);
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&st->p2p_ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    st->p2p_ticket = 0;
+    signal_all(q, 0);
+  }
+}
+
+// Step 2 (1 thread, before the owner's finalize): every rank has pushed.
+__global__ void k_p2p_wait_arrive(const QueryDev q) {
+  DevState* st = q.state;
+  long long k_lo;
+  uint32_t nwin;
+  close_window(q, k_lo, nwin);
+  if (nwin == 0) return;
+  spin_until(st, &st->p2p_arrive, (st->p2p_gen + 1u) * q.world);
+}
+
+// Step 3 (1 thread, after the owner's finalize): signal completion to every rank, count the
+// exchange.
+__global__ void k_p2p_finish(const QueryDev q) {
+  DevState* st = q.state;
+  long long k_lo;
+  uint32_t nwin;
+  close_window(q, k_lo, nwin);
+  if (nwin == 0) return;
+  st->p2p_gen += 1u;
+  signal_all(q, 1);
+}
+
 __device__ __forceinline__ unsigned long long append_row(DevState* st, bool want) {
   const uint32_t act = __activemask();
   const uint32_t m = __ballot_sync(act, want);
@@ -152,6 +246,7 @@ __device__ __forceinline__ unsigned long long append_row(DevState* st, bool want
 // Merged accumulators -> final rows (AVG, HAVING) for LR2 / CM2; zeroes what it reads.
 __global__ void __launch_bounds__(kThreads) k_finalize(const QueryDev q, long long k_lo, uint32_t nwin) {
   DevState* st = q.state;
+  if (nwin == 0) close_window(q, k_lo, nwin);
   const uint32_t K = q.kind == kCM2S ? min(st->n_keys, q.K) : q.K;
   lms_agg_row* rows = reinterpret_cast<lms_agg_row*>(q.rows);
   const unsigned long long total = (unsigned long long)nwin * K;
@@ -201,9 +296,11 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const QueryDev q, long lo
 }
 
 // CM1: one CTA per instance; ORDER BY SUM(cpu) ascending, ties by category (reading R9).
-__global__ void __launch_bounds__(32) k_finalize_cm1(const QueryDev q, long long k_lo) {
+__global__ void __launch_bounds__(32) k_finalize_cm1(const QueryDev q, long long k_lo, uint32_t nwin) {
   DevState* st = q.state;
+  if (nwin == 0) close_window(q, k_lo, nwin);
   const uint32_t w = blockIdx.x, c = threadIdx.x;
+  if (w >= nwin) return;
   __shared__ unsigned long long s_sum[10], s_cnt[10];
   if (c < 10) {
     const size_t g = (size_t)w * q.K + c;
@@ -261,10 +358,19 @@ cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cu
   return cudaGetLastError();
 }
 
+cudaError_t launch_p2p_exchange_async(const QueryDev& q, cudaStream_t st) {
+  k_p2p_push_async<<<sm_count(), kThreads, 0, st>>>(q);
+  k_p2p_wait_arrive<<<1, 32, 0, st>>>(q);
+  if (q.kind == kCM1S || q.kind == kCM1T) k_finalize_cm1<<<q.Wmerge, 32, 0, st>>>(q, 0, 0u);
+  else k_finalize<<<sm_count(), kThreads, 0, st>>>(q, 0, 0u);
+  k_p2p_finish<<<1, 32, 0, st>>>(q);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st) {
   if (n) k_merge<<<sm_count(), kThreads, 0, st>>>(q, static_cast<const lms_agg_row*>(rows), n, k_lo, nwin);
-  if (q.kind == kCM1S || q.kind == kCM1T) k_finalize_cm1<<<nwin, 32, 0, st>>>(q, k_lo);
+  if (q.kind == kCM1S || q.kind == kCM1T) k_finalize_cm1<<<nwin, 32, 0, st>>>(q, k_lo, nwin);
   else k_finalize<<<sm_count(), kThreads, 0, st>>>(q, k_lo, nwin);
   return cudaGetLastError();
 }

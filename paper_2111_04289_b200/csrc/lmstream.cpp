@@ -151,6 +151,7 @@ struct lms_query {
   bool parked = false;
   bool in_flight = false;
   bool awaiting_close = false;     // multi-GPU: aggregate pass launched, close not yet
+  bool p2p_async_pending = false;  // fused exchange enqueued behind the close (lms_p2p_collect)
   BatchReport last_report{};
   Flight& F() { return fl[cur_slot]; }
   std::vector<lms_batch_record> records;
@@ -722,6 +723,7 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
     if (bidx) *bidx = UINT64_MAX;
     if (q->awaiting_close || (q->in_flight && !q->pipeline))
       return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
+    if (q->p2p_async_pending) return fail(LMS_ESTATE, "fused exchange pending (call lms_p2p_collect)");
     // multi-GPU ranks run their batches in lockstep: an empty rank still runs the batch
     if (q->pending.empty() && q->qd.world == 1) return LMS_OK;
     CUDA_TRY(cudaSetDevice(q->cfg.device));
@@ -1016,6 +1018,51 @@ lms_status lms_p2p_push(lms_query* q, int64_t k_lo, uint32_t nwin) {
     return LMS_OK;
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in p2p_push");
+  }
+}
+
+lms_status lms_p2p_exchange_async(lms_query* q) {
+  try {
+    if (lms_status e = p2p_check(q)) return e;
+    if (q->awaiting_close || !q->in_flight) return fail(LMS_ESTATE, "call after lms_run_close, before lms_sync");
+    if (q->peers_h.size() != q->qd.world) return fail(LMS_ESTATE, "peers not imported");
+    for (const PeerView& v : q->peers_h)
+      if (!v.macc_sum) return fail(LMS_ESTATE, "peers not imported (lms_p2p_import for every rank)");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    CUDA_TRY(launch_p2p_exchange_async(q->qd, q->stream));
+    q->launches += 4;
+    q->p2p_async_pending = true;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in p2p_exchange_async");
+  }
+}
+
+lms_status lms_p2p_collect(lms_query* q) {
+  try {
+    if (lms_status e = p2p_check(q)) return e;
+    if (!q->p2p_async_pending) return fail(LMS_ESTATE, "no async exchange pending");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    lms_status s1 = complete_all(q);                 // batch record (the close's report)
+    CUDA_TRY(cudaStreamSynchronize(q->stream));      // + the exchange kernels behind it
+    q->p2p_async_pending = false;
+    unsigned int err = 0;
+    CUDA_TRY(cudaMemcpy(&err, &q->qd.state->p2p_err, sizeof(err), cudaMemcpyDeviceToHost));
+    if (err) return fail(LMS_ECUDA, "fused exchange: a peer did not arrive within 20 s");
+    unsigned long long total = 0;
+    CUDA_TRY(cudaMemcpy(&total, &q->qd.state->rows, sizeof(total), cudaMemcpyDeviceToHost));
+    const uint64_t nrows = std::min<uint64_t>(total, q->cfg.max_result_rows);
+    if (nrows) {
+      CUDA_TRY(q->agg_rows.reserve(nrows));
+      CUDA_TRY(cudaMemcpy(q->agg_rows.tail_ptr(), q->qd.rows, nrows * sizeof(lms_agg_row), cudaMemcpyDeviceToHost));
+      q->agg_rows.commit(nrows);
+    }
+    CUDA_TRY(cudaMemset(&q->qd.state->rows, 0, sizeof(unsigned long long)));
+    if (!q->records.empty()) q->records.back().rows_emitted = nrows;
+    if (total > nrows) return fail(LMS_EOVERFLOW, "merged rows exceed max_result_rows");
+    return s1;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in p2p_collect");
   }
 }
 

@@ -130,6 +130,12 @@ class RankHandle:
     def p2p_push(self, k_lo: int, nwin: int):
         check(L.lms_p2p_push(self.q.h, k_lo, nwin), "lms_p2p_push")
 
+    def p2p_exchange_async(self):
+        check(L.lms_p2p_exchange_async(self.q.h), "lms_p2p_exchange_async")
+
+    def p2p_collect(self) -> int:
+        return check(L.lms_p2p_collect(self.q.h), "lms_p2p_collect", (L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW))
+
     def p2p_finalize(self, k_lo: int, nwin: int):
         return check(L.lms_p2p_finalize(self.q.h, k_lo, nwin), "lms_p2p_finalize", (L.LMS_OK, L.LMS_EOVERFLOW))
 
@@ -304,10 +310,11 @@ class _Null:
 
 # ----------------------------------------------------------------------------- protocol
 
-def run_batch(handles, exchange, now: float, flush: bool = False, p2p: bool = False) -> list[int]:
+def run_batch(handles, exchange, now: float, flush: bool = False, p2p=False) -> list[int]:
     """One micro-batch on every local handle (steps 1-6 above; LR1: close_lr1's steps).
-    p2p: fused exchange (exchange.setup_p2p done once) instead of all-to-all + lms_merge.
-    Returns the sync statuses."""
+    p2p=True: fused exchange (exchange.setup_p2p done once) instead of all-to-all + lms_merge,
+    host-driven passes; p2p="async": the same exchange fully enqueued behind the close with a
+    device-side barrier (one host synchronisation per batch).  Returns the sync statuses."""
     for h in handles:
         st = L.lms_flush(h.q.h, now) if flush else L.lms_force_batch(h.q.h, now, None)
         check(st, "lms_flush" if flush else "lms_force_batch", (L.LMS_OK, L.LMS_EFORMAT))
@@ -316,6 +323,16 @@ def run_batch(handles, exchange, now: float, flush: bool = False, p2p: bool = Fa
         return close_lr1(handles, exchange)
     for h in handles:
         h.run_close()
+    if p2p == "async":
+        # fully enqueued: push -> device barrier -> owner finalize -> signal; one host sync
+        for h in handles:
+            h.p2p_exchange_async()
+        sts = [h.p2p_collect() for h in handles]
+        k0, k1 = handles[0].last_close_range()
+        w = handles[0].merge_window()
+        if k1 - k0 + 1 > w:                  # a long flush: the rest in host-driven passes
+            exchange_p2p(handles, exchange, k_from=k0 + w)
+        return sts
     sts = [h.sync() for h in handles]
     if handles[0].windows_closed() == 0:   # same on every rank: nothing to exchange (most batches)
         return sts
@@ -328,11 +345,13 @@ def run_batch(handles, exchange, now: float, flush: bool = False, p2p: bool = Fa
     return sts
 
 
-def exchange_p2p(handles, exchange):
+def exchange_p2p(handles, exchange, k_from=None):
     """Fused exchange of a synced batch that closed windows: per merge-window pass, every rank
     pushes its partials into the owners' accumulators (peer memory), barrier, every owner
     finalizes its keys (rows -> host), barrier."""
     k0, k1 = handles[0].last_close_range()
+    if k_from is not None:
+        k0 = k_from
     wmerge = handles[0].merge_window()
     for k in range(k0, k1 + 1, wmerge):
         nwin = min(wmerge, k1 - k + 1)

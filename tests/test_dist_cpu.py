@@ -211,6 +211,7 @@ def _p2p_worker(rank, world, port, q):
         ex = D.TorchDistExchange()
         ex.setup_p2p([h])
         D.exchange_p2p([h], ex)          # the exchange tail of run_batch(p2p=True)
+        D.exchange_p2p([h], ex, k_from=10 + h.merge_window())   # run_batch(p2p="async") remainder
         q.put((rank, h.imported, h.calls))
     finally:
         dist.destroy_process_group()
@@ -231,4 +232,5 @@ def test_gloo_world2_p2p_setup_and_passes():
         assert p.exitcode == 0
     for rank, imported, calls in res:
         assert imported == [0, 1]
-        assert calls == [("push", 10, 2), ("fin", 10, 2), ("push", 12, 1), ("fin", 12, 1)]
+        assert calls == [("push", 10, 2), ("fin", 10, 2), ("push", 12, 1), ("fin", 12, 1),
+                         ("push", 12, 1), ("fin", 12, 1)]   # + the remainder after an async pass

@@ -56,7 +56,8 @@ def _rank_main(rank, world, port, qname, batches, out_q, p2p=False):
 @pytest.mark.parametrize("qname,traffic,p2p", [("CM2S", "B(1.5)", False), ("LR2S", "R(0.5,2)", False),
                                                ("CM1S", "B(0.8)", False), ("LR1S", "B(0.4)", False),
                                                ("CM2S", "B(1.5)", True), ("LR2S", "R(0.5,2)", True),
-                                               ("CM1S", "B(0.8)", True)])
+                                               ("CM1S", "B(0.8)", True), ("CM2S", "B(1.5)", "async"),
+                                               ("LR2S", "R(0.5,2)", "async")])
 def test_two_processes_match_oracle(qname, traffic, p2p):
     import torch.multiprocessing as mp
     from paper_2111_04289_b200 import AGG_DTYPE, LR1_DTYPE
