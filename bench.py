@@ -152,7 +152,7 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p=False):
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
         h, ex = RankHandle(q), TorchDistExchange()
         if p2p:
-            ex.setup_p2p([h])
+            ex.setup_p2p([h], device_watermark=p2p == "device")
 
     def step(buf, n, t):
         q.push_device(buf.data_ptr(), n, float(t))
@@ -232,7 +232,7 @@ def e2e_run(wl, steps, warmup, seed, torch, rank=0, world=1, dist=None, p2p=Fals
         from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange, run_batch
         hd, ex = RankHandle(q), TorchDistExchange()
         if p2p:
-            ex.setup_p2p([hd])
+            ex.setup_p2p([hd], device_watermark=p2p == "device")
     d2h = []
 
     def step(h, n, t):
@@ -365,10 +365,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--seed", type=int, default=211104289)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "p2p", "p2p-async"],
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "p2p", "p2p-async", "device"],
                     help="N > 1: partial-aggregate exchange (NCCL all-to-all + owner merge; the fused "
                          "peer-memory push into the owners' accumulators with host-driven passes; or "
-                         "the same fully enqueued with a device-side barrier)")
+                         "the same fully enqueued with a device-side barrier; or also the watermark "
+                         "exchange on the device: no per-batch collective)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -394,7 +395,7 @@ def main():
     from paper_2111_04289_b200 import build  # noqa: F401  (library must already be built)
 
     seed = args.seed + 7919 * rank        # each rank: its own partition of the global batch
-    p2p = {"alltoall": False, "p2p": True, "p2p-async": "async"}[args.exchange]
+    p2p = {"alltoall": False, "p2p": True, "p2p-async": "async", "device": "device"}[args.exchange]
     res = device_run(wl, args.steps, args.warmup, seed, rank, world, torch, dist, p2p)
     el = res["elapsed_s"]
     if world > 1:

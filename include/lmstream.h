@@ -308,6 +308,14 @@ lms_status  lms_p2p_finalize(lms_query* q, int64_t k_lo, uint32_t nwin);
  * hang.  ESTATE: not after lms_run_close, or a previous exchange not collected.            */
 lms_status  lms_p2p_exchange_async(lms_query* q);
 lms_status  lms_p2p_collect(lms_query* q);
+/* enable != 0 (after lms_p2p_import of every rank; agg kinds): the watermark / first-ts
+ * all-reduce (reading R7) also moves to the device — a one-thread kernel after the aggregate
+ * pass folds this rank's values into every rank's slot through peer memory and waits for all
+ * ranks (bounded) — so lms_force_batch enqueues aggregate, watermark exchange and close
+ * without the caller's collective or lms_run_close; with lms_p2p_exchange_async +
+ * lms_p2p_collect a whole multi-GPU micro-batch runs with one host synchronisation and no
+ * per-batch NCCL call.  ESTATE: batch in flight, peers not imported.                       */
+lms_status  lms_p2p_device_watermark(lms_query* q, int32_t enable);
 
 /* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
  * index the per-pane counts directly (VID < max_keys; larger VIDs count as overflow), every

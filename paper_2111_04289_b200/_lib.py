@@ -120,6 +120,7 @@ _PROTOS = {
     "lms_p2p_finalize": (C.c_int32, [_Q, C.c_int64, C.c_uint32]),
     "lms_p2p_exchange_async": (C.c_int32, [_Q]),
     "lms_p2p_collect": (C.c_int32, [_Q]),
+    "lms_p2p_device_watermark": (C.c_int32, [_Q, C.c_int32]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "lms_kernel_launches": (C.c_int32, [_Q, _P(C.c_uint64)]),
     "lms_est_max_lat": (C.c_int32, [_P(C.c_double), _P(C.c_uint64), C.c_uint64, C.c_double, _P(C.c_double)]),

@@ -63,6 +63,10 @@ struct DevState {
   // pushes of an exchange are done, and to every rank's p2p_done when its finalize is done;
   // p2p_gen counts the exchanges that had instances to close (identical on every rank)
   unsigned int p2p_arrive, p2p_done, p2p_gen, p2p_err, p2p_ticket;
+  // device-side watermark exchange (reading R7 needs one global watermark): batch b's ranks
+  // fold their wm (MAX) and ts_min (MIN) into every rank's slot b % 2 and count arrivals
+  unsigned long long wmx_max[2], wmx_min[2];
+  unsigned int wmx_arrive, wmx_gen;
 };
 
 // Copied to the host after every batch.
@@ -166,6 +170,11 @@ cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long
                          uint32_t nwin, cudaStream_t st);
 cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cudaStream_t st);
 cudaError_t launch_p2p_exchange_async(const QueryDev& q, cudaStream_t st);
+cudaError_t launch_wm_exchange(const QueryDev& q, cudaStream_t st);
 int close_ctas(const QueryDev& q);
+void preload_cm_kernels();
+void preload_lr_kernels();
+void preload_close_kernels();
+void preload_dist_kernels();
 
 }  // namespace lms

@@ -517,6 +517,19 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_probe(const QueryDev q, l
 
 }  // namespace
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily, at first launch, and a
+// lazy load waits for the device: a first launch behind a running spin-wait kernel of another
+// handle — the multi-GPU device barriers on a shared GPU — would wait for that spin to time
+// out).  Called once per process from lms_query_create.
+void preload_close_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_close_agg);
+  cudaFuncGetAttributes(&fa, k_close_lr1);
+  cudaFuncGetAttributes(&fa, k_lr1_evict);
+  cudaFuncGetAttributes(&fa, k_lr1_wsum);
+  cudaFuncGetAttributes(&fa, k_lr1_probe);
+}
+
 int close_ctas(const QueryDev& q) {
   if (q.kind == kCM1S || q.kind == kCM1T) return 1;
   static int nsm = -1;

@@ -28,6 +28,8 @@
 //    accumulators, one RED.64 pair per CTA and key at the end.
 #include "common.cuh"
 
+#include <mutex>
+
 namespace lms {
 namespace {
 
@@ -793,6 +795,16 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
 
 }  // namespace
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily, at first launch, and a
+// lazy load waits for the device: a first launch behind a running spin-wait kernel of another
+// handle — the multi-GPU device barriers on a shared GPU — would wait for that spin to time
+// out).  Called once per process from lms_query_create.
+void preload_cm_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_cm_agg<kCM2S>);
+  cudaFuncGetAttributes(&fa, k_cm_agg<kCM1S>);
+}
+
 int cm_agg_ctas(const QueryDev& q) {
   static int nsm = -1;
   if (nsm < 0) {
@@ -802,6 +814,23 @@ int cm_agg_ctas(const QueryDev& q) {
   }
   (void)q;
   return nsm * kCtasPerSm;
+}
+
+// cudaFuncSetAttribute once per (kernel, device, size): it is not a per-launch call (and the
+// driver may serialise it against running work, which the multi-GPU device-side barriers of
+// other handles on the same device must never wait behind).
+static cudaError_t set_smem_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static const void* done_fn[16];
+  static int done_dev[16], done_bytes[16], n_done = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < n_done; i++)
+    if (done_fn[i] == fn && done_dev[i] == dev && done_bytes[i] >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && n_done < 16) { done_fn[n_done] = fn; done_dev[n_done] = dev; done_bytes[n_done] = bytes; n_done++; }
+  return e;
 }
 
 cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st) {
@@ -817,11 +846,11 @@ cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   const int grid = (int)q.n_agg_ctas;
   cudaError_t e;
   if (q.kind == kCM2S) {
-    e = cudaFuncSetAttribute(k_cm_agg<kCM2S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = set_smem_once((const void*)k_cm_agg<kCM2S>, (int)smem);
     if (e != cudaSuccess) return e;
     k_cm_agg<kCM2S><<<grid, kCmThreads, smem, st>>>(a);
   } else {
-    e = cudaFuncSetAttribute(k_cm_agg<kCM1S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = set_smem_once((const void*)k_cm_agg<kCM1S>, (int)smem);
     if (e != cudaSuccess) return e;
     k_cm_agg<kCM1S><<<grid, kCmThreads, smem, st>>>(a);
   }

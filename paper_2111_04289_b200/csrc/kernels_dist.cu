@@ -147,17 +147,14 @@ __device__ __forceinline__ void close_window(const QueryDev& q, long long& k_lo,
 }
 
 // ---- device-side barrier of the fused exchange (no host round trip) ----------------------
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-// Thread 0 spins until *c >= target (bounded: 20 s, then the error flag is raised and the
-// exchange proceeds — results of that batch are reported as failed, nothing hangs).
+// Thread 0 spins until *c >= target (bounded: ~20 s of SM clock, then the error flag is raised
+// and the exchange proceeds — that batch is reported as failed, nothing hangs).  clock64 is
+// the SM's own cycle counter: monotonic for the spinning thread (%globaltimer proved unusable
+// for this: its first reads can jump).
 __device__ __forceinline__ void spin_until(DevState* st, const unsigned int* c, unsigned int target) {
-  const unsigned long long t0 = gtimer();
+  const long long t0 = clock64();
   while (*(volatile const unsigned int*)c < target) {
-    if (gtimer() - t0 > 20000000000ull) { atomicExch(&st->p2p_err, 1u); break; }
+    if (clock64() - t0 > 40000000000ll) { atomicExch(&st->p2p_err, 1u); break; }
     __nanosleep(256);
   }
   __threadfence_system();
@@ -230,6 +227,33 @@ __global__ void k_p2p_finish(const QueryDev q) {
   if (nwin == 0) return;
   st->p2p_gen += 1u;
   signal_all(q, 1);
+}
+
+// Device-side watermark exchange (one thread; replaces the host-issued all-reduce): fold this
+// rank's watermark / first ts into every rank's slot of this batch, signal arrival, wait for
+// world arrivals, adopt the global values, and re-arm the slot for batch b + 2.  A rank can
+// run at most one batch ahead of the slowest (its next fold waits on everyone's arrival of
+// the current batch), so two slots suffice.
+__global__ void k_wm_exchange(const QueryDev q) {
+  DevState* st = q.state;
+  const unsigned int gen = st->wmx_gen, slot = gen & 1u;
+  const unsigned long long wm = st->wm, tsmin = st->ts_min;
+  for (uint32_t r = 0; r < q.world; r++) {
+    DevState* ps = q.peers[r].state;
+    atomicMax_system(&ps->wmx_max[slot], wm);
+    atomicMin_system(&ps->wmx_min[slot], tsmin);
+  }
+  __threadfence_system();
+  for (uint32_t r = 0; r < q.world; r++) atomicAdd_system(&q.peers[r].state->wmx_arrive, 1u);
+  spin_until(st, &st->wmx_arrive, (gen + 1u) * q.world);
+  st->wm = *(volatile unsigned long long*)&st->wmx_max[slot];
+  st->ts_min = *(volatile unsigned long long*)&st->wmx_min[slot];
+  // re-arm my slot for batch gen + 2: a peer folds into it only after every rank (me included)
+  // has arrived for batch gen + 1, which I do after this
+  st->wmx_max[slot] = 0;
+  st->wmx_min[slot] = 0xFFFFFFFFull;
+  st->wmx_gen = gen + 1u;
+  __threadfence_system();
 }
 
 __device__ __forceinline__ unsigned long long append_row(DevState* st, bool want) {
@@ -347,6 +371,24 @@ int sm_count() {
 
 }  // namespace
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily, at first launch, and a
+// lazy load waits for the device: a first launch behind a running spin-wait kernel of another
+// handle — the multi-GPU device barriers on a shared GPU — would wait for that spin to time
+// out).  Called once per process from lms_query_create.
+void preload_dist_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_bucket_count);
+  cudaFuncGetAttributes(&fa, k_bucket_scatter);
+  cudaFuncGetAttributes(&fa, k_merge);
+  cudaFuncGetAttributes(&fa, k_finalize);
+  cudaFuncGetAttributes(&fa, k_finalize_cm1);
+  cudaFuncGetAttributes(&fa, k_p2p_push);
+  cudaFuncGetAttributes(&fa, k_p2p_push_async);
+  cudaFuncGetAttributes(&fa, k_p2p_wait_arrive);
+  cudaFuncGetAttributes(&fa, k_p2p_finish);
+  cudaFuncGetAttributes(&fa, k_wm_exchange);
+}
+
 cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st) {
   k_bucket_count<<<sm_count(), kThreads, 0, st>>>(q);
   k_bucket_scatter<<<sm_count(), kThreads, 0, st>>>(q);
@@ -355,6 +397,11 @@ cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st) {
 
 cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cudaStream_t st) {
   k_p2p_push<<<sm_count(), kThreads, 0, st>>>(q, k_lo, nwin);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_wm_exchange(const QueryDev& q, cudaStream_t st) {
+  k_wm_exchange<<<1, 1, 0, st>>>(q);
   return cudaGetLastError();
 }
 

@@ -17,6 +17,8 @@
 // vehicle counts per pane (global REDs) + projection of a 16 B row into the retained FIFO.
 #include "common.cuh"
 
+#include <mutex>
+
 namespace lms {
 namespace {
 
@@ -286,6 +288,16 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
 
 }  // namespace
 
+// Load every kernel of this file now (CUDA 12 loads kernels lazily, at first launch, and a
+// lazy load waits for the device: a first launch behind a running spin-wait kernel of another
+// handle — the multi-GPU device barriers on a shared GPU — would wait for that spin to time
+// out).  Called once per process from lms_query_create.
+void preload_lr_kernels() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, k_lr_agg<kLR2S>);
+  cudaFuncGetAttributes(&fa, k_lr_agg<kLR1S>);
+}
+
 int lr_agg_ctas(const QueryDev& q) {
   static int nsm = -1;
   if (nsm < 0) {
@@ -302,6 +314,23 @@ size_t lr_agg_smem(const QueryDev& q) {
   return (size_t)kLrStages * kLrTileBytes + (lr1 ? 0 : (size_t)4 * q.K * sizeof(uint32_t));
 }
 
+// cudaFuncSetAttribute once per (kernel, device, size): it is not a per-launch call (and the
+// driver may serialise it against running work, which the multi-GPU device-side barriers of
+// other handles on the same device must never wait behind).
+static cudaError_t set_smem_once(const void* fn, int bytes) {
+  static std::mutex mu;
+  static const void* done_fn[16];
+  static int done_dev[16], done_bytes[16], n_done = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (int i = 0; i < n_done; i++)
+    if (done_fn[i] == fn && done_dev[i] == dev && done_bytes[i] >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && n_done < 16) { done_fn[n_done] = fn; done_dev[n_done] = dev; done_bytes[n_done] = bytes; n_done++; }
+  return e;
+}
+
 cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st) {
   LrArgs a;
   a.q = q;
@@ -313,13 +342,13 @@ cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   cudaError_t e;
   switch (q.kind) {
     case kLR2S:
-      e = cudaFuncSetAttribute(k_lr_agg<kLR2S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = set_smem_once((const void*)k_lr_agg<kLR2S>, (int)smem);
       if (e != cudaSuccess) return e;
       k_lr_agg<kLR2S><<<grid, kLrThreads, smem, st>>>(a);
       break;
     case kLR1S:
     case kLR1T:
-      e = cudaFuncSetAttribute(k_lr_agg<kLR1S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = set_smem_once((const void*)k_lr_agg<kLR1S>, (int)smem);
       if (e != cudaSuccess) return e;
       k_lr_agg<kLR1S><<<grid, kLrThreads, smem, st>>>(a);
       break;

@@ -12,7 +12,9 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <algorithm>
 #include <limits>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -152,6 +154,7 @@ struct lms_query {
   bool in_flight = false;
   bool awaiting_close = false;     // multi-GPU: aggregate pass launched, close not yet
   bool p2p_async_pending = false;  // fused exchange enqueued behind the close (lms_p2p_collect)
+  bool device_wm = false;          // multi-GPU: watermark exchanged by a kernel (lms_p2p_device_watermark)
   BatchReport last_report{};
   Flight& F() { return fl[cur_slot]; }
   std::vector<lms_batch_record> records;
@@ -284,9 +287,13 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
   }
   CUDA_TRY(cudaEventRecord(q->F().ev_agg, q->stream));
   q->F().flush = flush;
-  if (q->qd.world > 1) {            // multi-GPU: the caller all-reduces the watermark first
+  if (q->qd.world > 1 && !q->device_wm) {   // multi-GPU: the caller all-reduces the watermark first
     q->awaiting_close = true;
     return LMS_OK;
+  }
+  if (q->qd.world > 1) {            // device-side watermark exchange through peer memory
+    CUDA_TRY(launch_wm_exchange(q->qd, q->stream));
+    q->launches++;
   }
   return launch_close_stage(q);
 }
@@ -486,6 +493,18 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     auto bail = [&](lms_status st) { delete q; return st; };
 #define Q_TRY(x) do { lms_status st_ = (x); if (st_) return bail(st_); } while (0)
 #define QC_TRY(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) return bail(fail(LMS_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_))); } while (0)
+    {   // every kernel loaded up front (see preload_*_kernels), once per process and device
+      static std::mutex mu;
+      static std::vector<int> loaded;
+      std::lock_guard<std::mutex> lock(mu);
+      if (std::find(loaded.begin(), loaded.end(), cfg->device) == loaded.end()) {
+        preload_cm_kernels();
+        preload_lr_kernels();
+        preload_close_kernels();
+        preload_dist_kernels();
+        loaded.push_back(cfg->device);
+      }
+    }
     QC_TRY(cudaStreamCreateWithFlags(&q->stream, cudaStreamNonBlocking));
     QC_TRY(cudaStreamCreateWithFlags(&q->copy_stream, cudaStreamNonBlocking));
     // pipelining (two batches in flight) only for single-GPU handles
@@ -584,6 +603,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     for (int b = 0; b < 2; b++) Q_TRY(q->dalloc(&q->d_in[b], q->in_cap + 4096, 0));
     DevState init{};
     init.ts_min = kEmpty32;
+    init.wmx_min[0] = init.wmx_min[1] = kEmpty32;
     init.free_top = (int)q->P;
     QC_TRY(cudaMemcpy(d.state, &init, sizeof(init), cudaMemcpyHostToDevice));
     QC_TRY(cudaDeviceSynchronize());
@@ -1036,6 +1056,18 @@ lms_status lms_p2p_exchange_async(lms_query* q) {
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in p2p_exchange_async");
   }
+}
+
+lms_status lms_p2p_device_watermark(lms_query* q, int32_t enable) {
+  if (lms_status e = p2p_check(q)) return e;
+  if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch in flight");
+  if (enable) {
+    if (q->peers_h.size() != q->qd.world) return fail(LMS_ESTATE, "peers not imported");
+    for (const PeerView& v : q->peers_h)
+      if (!v.state) return fail(LMS_ESTATE, "peers not imported (lms_p2p_import for every rank)");
+  }
+  q->device_wm = enable != 0;
+  return LMS_OK;
 }
 
 lms_status lms_p2p_collect(lms_query* q) {

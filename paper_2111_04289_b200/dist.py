@@ -133,6 +133,9 @@ class RankHandle:
     def p2p_exchange_async(self):
         check(L.lms_p2p_exchange_async(self.q.h), "lms_p2p_exchange_async")
 
+    def p2p_device_watermark(self, enable: bool = True):
+        check(L.lms_p2p_device_watermark(self.q.h, int(enable)), "lms_p2p_device_watermark")
+
     def p2p_collect(self) -> int:
         return check(L.lms_p2p_collect(self.q.h), "lms_p2p_collect", (L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW))
 
@@ -223,7 +226,7 @@ class TorchDistExchange:
             wm.copy_(both[:1])
             tsmin.copy_(-both[1:])
 
-    def setup_p2p(self, handles):
+    def setup_p2p(self, handles, device_watermark: bool = False):
         """Fused exchange: every rank maps every rank's owner state (CUDA IPC handles sent with
         all_gather_object)."""
         (h,) = handles
@@ -231,6 +234,8 @@ class TorchDistExchange:
         self.dist.all_gather_object(blobs, h.p2p_export(), group=self.group)
         for b in blobs:
             h.p2p_import(b)
+        if device_watermark:
+            h.p2p_device_watermark(True)
 
     def barrier(self, handles):
         self.dist.barrier(group=self.group)
@@ -259,10 +264,13 @@ class TorchDistExchange:
 class LocalExchange:
     """All ranks' handles in one process (virtual shards on one GPU)."""
 
-    def setup_p2p(self, handles):
+    def setup_p2p(self, handles, device_watermark: bool = False):
         for h in handles:
             for o in handles:
                 h.p2p_import_local(o)
+        if device_watermark:
+            for h in handles:
+                h.p2p_device_watermark(True)
 
     def barrier(self, handles):
         pass                        # pushes are synchronous: nothing in flight
@@ -314,25 +322,22 @@ def run_batch(handles, exchange, now: float, flush: bool = False, p2p=False) -> 
     """One micro-batch on every local handle (steps 1-6 above; LR1: close_lr1's steps).
     p2p=True: fused exchange (exchange.setup_p2p done once) instead of all-to-all + lms_merge,
     host-driven passes; p2p="async": the same exchange fully enqueued behind the close with a
-    device-side barrier (one host synchronisation per batch).  Returns the sync statuses."""
+    device-side barrier (one host synchronisation per batch); p2p="device": in addition the
+    watermark exchange runs on the device (handles set up with p2p_device_watermark), so no
+    collective is issued per batch.  Returns the sync statuses."""
     for h in handles:
         st = L.lms_flush(h.q.h, now) if flush else L.lms_force_batch(h.q.h, now, None)
         check(st, "lms_flush" if flush else "lms_force_batch", (L.LMS_OK, L.LMS_EFORMAT))
+    if p2p == "device":
+        # aggregate, watermark exchange and close are already enqueued (device-side exchange)
+        return _exchange_async(handles, exchange)
     exchange.allreduce_watermarks(handles)
     if handles[0].q.kind in (L.LMS_LR1S, L.LMS_LR1T):
         return close_lr1(handles, exchange)
     for h in handles:
         h.run_close()
     if p2p == "async":
-        # fully enqueued: push -> device barrier -> owner finalize -> signal; one host sync
-        for h in handles:
-            h.p2p_exchange_async()
-        sts = [h.p2p_collect() for h in handles]
-        k0, k1 = handles[0].last_close_range()
-        w = handles[0].merge_window()
-        if k1 - k0 + 1 > w:                  # a long flush: the rest in host-driven passes
-            exchange_p2p(handles, exchange, k_from=k0 + w)
-        return sts
+        return _exchange_async(handles, exchange)
     sts = [h.sync() for h in handles]
     if handles[0].windows_closed() == 0:   # same on every rank: nothing to exchange (most batches)
         return sts
@@ -361,6 +366,19 @@ def exchange_p2p(handles, exchange, k_from=None):
         for h in handles:
             h.p2p_finalize(k, nwin)
         exchange.barrier(handles)
+
+
+def _exchange_async(handles, exchange):
+    """Fused exchange fully enqueued behind the close: push -> device barrier -> owner
+    finalize -> signal; one host synchronisation (collect) per rank."""
+    for h in handles:
+        h.p2p_exchange_async()
+    sts = [h.p2p_collect() for h in handles]
+    k0, k1 = handles[0].last_close_range()
+    w = handles[0].merge_window()
+    if k1 - k0 + 1 > w:                      # a long flush: the rest in host-driven passes
+        exchange_p2p(handles, exchange, k_from=k0 + w)
+    return sts
 
 
 def _close_range(handles):

@@ -18,7 +18,7 @@ def sharded_run(qname, batches, world, p2p=False, **cfg):
     hs = [RankHandle(P.Query(qname, mode="manual", rank=r, world=world, **cfg)) for r in range(world)]
     ex = LocalExchange()
     if p2p:
-        ex.setup_p2p(hs)
+        ex.setup_p2p(hs, device_watermark=p2p == "device")
     outs, t = [], 0.0
     for b in batches + [None]:
         if b is not None:
@@ -36,7 +36,7 @@ def sharded_run(qname, batches, world, p2p=False, **cfg):
     return outs
 
 
-@pytest.mark.parametrize("p2p", [False, True, "async"], ids=["alltoall", "p2p", "p2p_async"])
+@pytest.mark.parametrize("p2p", [False, True, "async", "device"], ids=["alltoall", "p2p", "p2p_async", "device"])
 @pytest.mark.parametrize("qname,traffic,world", [("CM2S", "B(1.3)", 2), ("CM2S", "R(0.2,1.5)", 3),
                                                   ("LR2S", "B(1.7)", 2), ("LR2S", "U(0.8)", 4),
                                                   ("CM1S", "B(0.9)", 3), ("CM1T", "B(0.7)", 2)])

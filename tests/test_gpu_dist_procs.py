@@ -34,7 +34,7 @@ def _rank_main(rank, world, port, qname, batches, out_q, p2p=False):
         h = RankHandle(P.Query(qname, mode="manual", rank=rank, world=world))
         ex = TorchDistExchange()
         if p2p:
-            ex.setup_p2p([h])            # CUDA IPC: each process maps the other's owner state
+            ex.setup_p2p([h], device_watermark=p2p == "device")   # CUDA IPC mappings
         t, outs = 0.0, []
         for b in batches + [None]:
             if b is not None:
@@ -57,7 +57,8 @@ def _rank_main(rank, world, port, qname, batches, out_q, p2p=False):
                                                ("CM1S", "B(0.8)", False), ("LR1S", "B(0.4)", False),
                                                ("CM2S", "B(1.5)", True), ("LR2S", "R(0.5,2)", True),
                                                ("CM1S", "B(0.8)", True), ("CM2S", "B(1.5)", "async"),
-                                               ("LR2S", "R(0.5,2)", "async")])
+                                               ("LR2S", "R(0.5,2)", "async"), ("CM2S", "B(1.5)", "device"),
+                                               ("CM1S", "B(0.8)", "device")])
 def test_two_processes_match_oracle(qname, traffic, p2p):
     import torch.multiprocessing as mp
     from paper_2111_04289_b200 import AGG_DTYPE, LR1_DTYPE
