@@ -331,3 +331,14 @@ def test_lr1_dense_vehicles_match_oracle(qname, traffic):
     batches = split(secs, [7, 11, 3, 30])
     compare_run(qname, product_run(qname, batches, flags=L.LMS_FLAG_DENSE_VEHICLES),
                 oracle_rows(qname, batches))
+
+
+@pytest.mark.parametrize("sel_ppm,jobs,max_keys", [(1_000_000, 2_000, 1 << 16), (10_000, 2_000, 1 << 16),
+                                                   (260_000, 200_000, 1 << 18)])
+def test_cm2_selectivity_and_key_space_sweep(sel_ppm, jobs, max_keys):
+    """CM2 across the §8(d) sweeps: eventType==1 selectivity 1.0 and 0.01 (every / almost no
+    record survives the WHERE), and a large jobId key space (2*10^5 distinct keys in the
+    dictionary, max_keys 2^18) — exact against the oracle."""
+    secs = stream("CM", "B(4)", 14, params=g.CMParams(num_jobs=jobs, sel_ppm=sel_ppm))
+    batches = split(secs, [5, 4, 5])
+    compare_run("CM2S", product_run("CM2S", batches, max_keys=max_keys), oracle_rows("CM2S", batches))
