@@ -49,3 +49,39 @@ def test_full_size_batches_every_row(qname, seconds):
         compare_agg(qname, rows, want)
         emitted += len(want)
     assert emitted > 1000
+
+
+def test_full_size_pipelined_as_bench_runs_it():
+    """bench.py's exact configuration: 10M-record CM2 batches with LMS_FLAG_PIPELINE (batch i+1
+    launched while batch i runs, rows read as batches complete); the union of all emitted rows
+    equals the oracle's, row by row."""
+    import numpy as np
+    import torch
+
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    from lmsgen import cuda as gcu
+    seconds, seed = 10, 211104289
+    q = Q.query_spec("CM2S")
+    rp = B.BulkReplay(q)
+    want, got, live = [], [], []
+    with P.Query("CM2S", mode="manual", max_batch_bytes=1 << 20, flags=L.LMS_FLAG_PIPELINE) as dq:
+        for t in range(seconds):
+            buf, n = gcu.second_tensor("CM", t, N, seed=seed)
+            live.append(buf)                       # borrowed until its batch completes
+            dq.push_device(buf.data_ptr(), n, float(t))
+            dq.force(float(t) + 1.0)
+            got.append(dq.read_agg())
+            want += rp.batch(t, vec.cm_columns(seed, t, N))
+            if len(live) > 3:
+                live.pop(0)
+        dq.sync()
+        got.append(dq.read_agg())
+        dq.flush(float(seconds) + 1.0)
+        got.append(dq.read_agg())
+        want += rp.flush()
+        recs = dq.records()
+    assert [r["num_records"] for r in recs[:seconds]] == [N] * seconds
+    compare_agg("CM2S", np.concatenate(got), want)
+    del live
+    torch.cuda.empty_cache()
