@@ -130,8 +130,10 @@ struct QueryDev {
   uint32_t H_mask;              // H - 1
   uint32_t* slot_pane;          // [P] pane held by accumulator slot s (kEmpty32 = free)
   uint32_t* free_stack;         // [P]
-  unsigned long long* acc_sum;  // [P][K]
-  unsigned long long* acc_cnt;  // [P][K]
+  unsigned long long* acc_sum;  // [P][stripes][K]
+  unsigned long long* acc_cnt;  // [P][stripes][K]
+  uint32_t stripes;             // CM2: CTAs add into stripe blockIdx % stripes (hot keys spread
+                                // over `stripes` addresses); the close sums the stripes. Else 1.
   uint32_t* acc_cnt32;          // LR1 [P][K]
   uint32_t* part32;             // LR2 [C][2][2][K]
   unsigned long long* part64;   // CM1 [C][2][2][K]

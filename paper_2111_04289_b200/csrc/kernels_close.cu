@@ -311,8 +311,12 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
         if (key < k1) {
           for (uint32_t j = 0; j < q.ppw; j++) {
             const uint32_t g = wslots[j];
-            if (g != kEmpty32) { s += q.acc_sum[(size_t)g * q.K + key];
-                                 c += q.acc_cnt[(size_t)g * q.K + key]; }
+            if (g != kEmpty32)
+              for (uint32_t sp = 0; sp < q.stripes; sp++) {   // (stripes > 1: CM2)
+                const size_t gi = ((size_t)g * q.stripes + sp) * q.K + key;
+                s += q.acc_sum[gi];
+                c += q.acc_cnt[gi];
+              }
           }
         }
         bool want = c > 0;
@@ -364,10 +368,11 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
     const uint32_t nev = s_nev;
     for (uint32_t i = 0; i < nev; i++) {
       const size_t g = s_ev[i];
-      for (uint32_t k = kk0 + threadIdx.x; k < kk1; k += blockDim.x) {
-        q.acc_sum[g * q.K + k] = 0;
-        q.acc_cnt[g * q.K + k] = 0;
-      }
+      for (uint32_t sp = 0; sp < q.stripes; sp++)
+        for (uint32_t k = kk0 + threadIdx.x; k < kk1; k += blockDim.x) {
+          q.acc_sum[(g * q.stripes + sp) * q.K + k] = 0;
+          q.acc_cnt[(g * q.stripes + sp) * q.K + k] = 0;
+        }
     }
   }
   if (ticket(st)) finish(q, w);

@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       const uint32_t idx = c_gslot != kFail32 ? dict_get(q.dict, sv_job[kCM2 ? warp : 0][lane], q.state) : kEmpty32;
       if (idx == kEmpty32) n_ovf++;
       else {
-        const size_t gi = (size_t)c_gslot * q.K + idx;
+        const size_t gi = ((size_t)c_gslot * q.stripes + (blockIdx.x & (q.stripes - 1u))) * q.K + idx;
         atomicAdd(&q.acc_sum[gi], (unsigned long long)sv_m[kCM2 ? warp : 0][lane]);
         atomicAdd(&q.acc_cnt[gi], 1ull);
       }

@@ -18,12 +18,19 @@ ap.add_argument("--workload", default="cm2")
 ap.add_argument("--batches", type=int, default=3)
 ap.add_argument("--records", type=int, default=10_000_000)
 ap.add_argument("--flags", type=int, default=0)
+ap.add_argument("--jobs", type=int, default=None, help="CM: distinct jobIds J (default 1e4)")
+ap.add_argument("--max-keys", type=int, default=None)
+ap.add_argument("--sel-ppm", type=int, default=None, help="CM: eventType==1 selectivity in ppm")
 a = ap.parse_args()
 kind, fam = {"cm2": ("CM2S", "CM"), "lr2": ("LR2S", "LR"), "cm1": ("CM1S", "CM"), "lr1": ("LR1S", "LR")}[a.workload]
-bufs = [gcu.second_tensor(fam, t, a.records) for t in range(a.batches)]
+import lmsgen as g  # noqa: E402
+params = g.CMParams(num_jobs=a.jobs or 10 ** 4, sel_ppm=a.sel_ppm) if fam == "CM" else None
+bufs = [gcu.second_tensor(fam, t, a.records, params=params) if params else gcu.second_tensor(fam, t, a.records)
+        for t in range(a.batches)]
 # LR1 keeps every record of the current slide in its retained FIFO: room for 8 batches
 rows_cap = max(1 << 20, (8 if kind.startswith("LR1") else 2) * a.records)
-q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=rows_cap, flags=a.flags)
+extra = {"max_keys": a.max_keys} if a.max_keys else {}
+q = P.Query(kind, mode="manual", max_batch_bytes=1 << 20, max_result_rows=rows_cap, flags=a.flags, **extra)
 for t, (b, n) in enumerate(bufs):
     q.push_device(b.data_ptr(), n, float(t))
     q.force(t + 1.0)
