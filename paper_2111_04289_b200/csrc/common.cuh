@@ -74,30 +74,31 @@ __device__ __forceinline__ unsigned long long fmix64(unsigned long long k) {
 // Dictionary lookup-or-insert: key -> dense index < max_keys; kEmpty32 on overflow.
 __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long key, DevState* st) {
   unsigned long long h = fmix64(key) & d.cap_mask;
-  for (unsigned long long probes = 0; probes <= d.cap_mask; probes++) {   // bounded: a full table
-                                                                          // (key overflow) ends
-    unsigned long long k = *(volatile unsigned long long*)&d.keys[h];
-    if (k == key || k == kEmpty64) {
-      if (k == kEmpty64) {
-        k = atomicCAS(&d.keys[h], kEmpty64, key);
-        if (k == kEmpty64) {   // we own the slot: allocate the index and publish it
-          uint32_t idx = atomicAdd(&st->n_keys, 1u);
-          if (idx >= d.max_keys) {
-            atomicExch(&st->key_overflow, 1u);
-            idx = kEmpty32 - 1;   // poison: entry exists but is unusable
-          } else {
-            d.key_by_idx[idx] = key;
-          }
-          __threadfence();
-          atomicExch(&d.vals[h], idx);
-          return idx >= d.max_keys ? kEmpty32 : idx;
+  for (unsigned long long probes = 0; probes <= d.cap_mask; probes++) {   // bounded: a full
+                                                                          // table (key overflow) ends
+    unsigned long long* ent = d.keys + 2 * h;
+    unsigned long long k, kv;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(kv) : "l"(ent));
+    if (k == kEmpty64) {
+      k = atomicCAS(ent, kEmpty64, key);
+      if (k == kEmpty64) {     // we own the entry: allocate the index and publish it
+        uint32_t idx = atomicAdd(&st->n_keys, 1u);
+        if (idx >= d.max_keys) {
+          atomicExch(&st->key_overflow, 1u);
+          idx = kEmpty32 - 1;   // poison: entry exists but is unusable
+        } else {
+          d.key_by_idx[idx] = key;
         }
+        __threadfence();
+        atomicExch(reinterpret_cast<unsigned int*>(ent + 1), idx);
+        return idx >= d.max_keys ? kEmpty32 : idx;
       }
-      if (k == key) {
-        uint32_t v;
-        while ((v = *(volatile uint32_t*)&d.vals[h]) == kEmpty32) { }
-        return v >= d.max_keys ? kEmpty32 : v;
-      }
+      kv = kEmpty32;            // someone else inserted: re-read its index below if it is ours
+    }
+    if (k == key) {
+      uint32_t v = (uint32_t)kv;
+      while (v == kEmpty32) v = *(volatile uint32_t*)(ent + 1);
+      return v >= d.max_keys ? kEmpty32 : v;
     }
     h = (h + 1) & d.cap_mask;
   }

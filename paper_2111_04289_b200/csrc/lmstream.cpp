@@ -583,8 +583,8 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       const uint64_t cap = next_pow2(2 * cfg->max_keys);
       d.dict.cap_mask = cap - 1;
       d.dict.max_keys = (uint32_t)cfg->max_keys;
-      Q_TRY(q->dalloc(&d.dict.keys, cap, 0xFF));
-      Q_TRY(q->dalloc(&d.dict.vals, cap, 0xFF));
+      Q_TRY(q->dalloc(&d.dict.keys, 2 * cap, 0xFF));   // {key, index} entries of 16 B
+      d.dict.vals = nullptr;
       Q_TRY(q->dalloc(&d.dict.key_by_idx, cfg->max_keys, 0));
     }
     d.row_cap = cfg->max_result_rows;

@@ -21,10 +21,12 @@ ap.add_argument("--flags", type=int, default=0)
 ap.add_argument("--jobs", type=int, default=None, help="CM: distinct jobIds J (default 1e4)")
 ap.add_argument("--max-keys", type=int, default=None)
 ap.add_argument("--sel-ppm", type=int, default=None, help="CM: eventType==1 selectivity in ppm")
+ap.add_argument("--vehicles", type=int, default=None, help="LR: distinct vehicles V (default 1e6)")
 a = ap.parse_args()
 kind, fam = {"cm2": ("CM2S", "CM"), "lr2": ("LR2S", "LR"), "cm1": ("CM1S", "CM"), "lr1": ("LR1S", "LR")}[a.workload]
 import lmsgen as g  # noqa: E402
-params = g.CMParams(num_jobs=a.jobs or 10 ** 4, sel_ppm=a.sel_ppm) if fam == "CM" else None
+params = (g.CMParams(num_jobs=a.jobs or 10 ** 4, sel_ppm=a.sel_ppm) if fam == "CM"
+          else (g.LRParams(num_vehicles=a.vehicles) if a.vehicles else None))
 bufs = [gcu.second_tensor(fam, t, a.records, params=params) if params else gcu.second_tensor(fam, t, a.records)
         for t in range(a.batches)]
 # LR1 keeps every record of the current slide in its retained FIFO: room for 8 batches
