@@ -42,6 +42,7 @@ struct DevState {
   unsigned long long wm_prev;   // snapshot at batch start: late iff ts + 1 < wm_prev
   long long next_k;             // first window instance not yet emitted
   long long evict_upto;         // LR1: panes <= this are evicted by k_lr1_evict
+  long long evicted_upto;       // LR1: evict_upto of the last eviction that ran
   unsigned int next_k_valid;
   unsigned long long ts_min;    // min kept ts of the current batch (0xFFFFFFFF = none); u64 so
                                 // that multi-GPU ranks can all-reduce it as int64

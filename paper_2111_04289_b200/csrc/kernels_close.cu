@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
 }
 
 // LR1: probe retained rows whose pane is the newest slide of a closing instance.
+constexpr int kLr1Items = 4;             // retained rows per thread and iteration
+constexpr int kLr1SlotCache = 1024;      // panes whose slots a CTA resolves up front
+constexpr int kLr1MaxPpw = 8;            // window panes summed with unrolled loads
 __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) {
   const QueryDev& q = a.q;
   DevState* st = q.state;
@@ -394,47 +397,102 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
   const Lr1Retained* src = q.fifo[cur];
   Lr1Retained* dst = q.fifo[cur ^ 1u];
   lms_lr1_row* rows = reinterpret_cast<lms_lr1_row*>(q.rows);
-  const uint32_t stride = gridDim.x * blockDim.x;
-  const uint32_t iters = (n + stride - 1) / stride;
+  // accumulator slots of the panes the closing instances span, resolved once per CTA (a row of
+  // instance k sums panes k .. k+ppw-1; outside the cached span: per-row pane-table lookups)
+  __shared__ uint32_t s_slot[kLr1SlotCache + kLr1MaxPpw];
+  const long long pbase = w.nk;
+  const long long pspan = w.k_last + (long long)q.ppw - pbase;
+  const bool cached = pspan <= kLr1SlotCache;
+  if (cached)
+    for (uint32_t j = threadIdx.x; j < (uint32_t)pspan; j += blockDim.x) s_slot[j] = find_slot(q, pbase + j);
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t ppw = min(q.ppw, (uint32_t)kLr1MaxPpw);   // (R/S <= 8 unrolled; more: loop)
+  const uint32_t per_cta = blockDim.x * kLr1Items;
+  const uint32_t iters = (n + per_cta * gridDim.x - 1) / (per_cta * gridDim.x);
   for (uint32_t it = 0; it < iters; it++) {
-    const uint32_t i = it * stride + blockIdx.x * blockDim.x + threadIdx.x;
-    bool emit = false, keep = false;
-    Lr1Retained r{};
-    long long k = 0;
-    uint32_t m = 0;
-    if (i < n && src[i].vidx != kEmpty32) {      // (holes: records the aggregate pass dropped)
-      r = src[i];
-      const long long p = (long long)pane_of(r.ts, q.S, q.div_magic);
-      k = p - (long long)q.ppw + 1;              // instance whose newest slide is pane p
-      if (w.any && k <= w.k_last) {
-        emit = true;
-        for (long long j = k; j <= p; j++) {
-          const uint32_t g = find_slot(q, j);
-          if (g != kEmpty32) m += q.acc_cnt32[(size_t)g * q.K + r.vidx];
+    const uint32_t base = (it * gridDim.x + blockIdx.x) * per_cta;
+    Lr1Retained r[kLr1Items];
+    long long kk[kLr1Items];
+    uint32_t m[kLr1Items];
+    uint32_t emit = 0, keep = 0;     // bit i: item i
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) {
+      const uint32_t idx = base + i * blockDim.x + threadIdx.x;   // coalesced 16 B loads
+      m[i] = 0; kk[i] = 0;
+      if (idx < n) {
+        r[i] = src[idx];
+        if (r[i].vidx != kEmpty32) {          // (holes: records the aggregate pass dropped)
+          const long long p = (long long)pane_of(r[i].ts, q.S, q.div_magic);
+          kk[i] = p - (long long)q.ppw + 1;   // instance whose newest slide is pane p
+          if (kk[i] <= w.k_last) emit |= 1u << i; else keep |= 1u << i;
         }
-      } else {
-        keep = true;
       }
     }
-    const unsigned long long pos = row_slot(st, emit);
-    if (emit) {
-      if (pos < q.row_cap) {
-        lms_lr1_row o;
-        o.win_start_s = k * (long long)q.S;
-        o.vehicle = q.lr1_dense ? r.vidx : q.dict.key_by_idx[r.vidx];
-        o.ts = r.ts; o.multiplicity = m; o.speed = r.speed; o.xway = r.xway; o.segment = r.seg;
-        o.lane = r.lane; o.dir = r.dir;
-        rows[pos] = o;
-      } else {
-        atomicExch(&st->row_overflow, 1u);
+    // multiplicity: the vehicle's count over the instance's panes; all loads of the items
+    // are independent and issued back to back (latency-bound: L2-resident count tables)
+    uint32_t c[kLr1Items][kLr1MaxPpw];
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) {
+      const long long off = kk[i] - pbase;
+      const bool fast = (emit >> i & 1u) && cached && off >= 0;
+#pragma unroll
+      for (int j = 0; j < kLr1MaxPpw; j++) {
+        const uint32_t g = (fast && (uint32_t)j < ppw) ? s_slot[off + j] : kEmpty32;
+        c[i][j] = g != kEmpty32 ? __ldcg(&q.acc_cnt32[(size_t)g * q.K + r[i].vidx]) : 0u;
       }
+      if ((emit >> i & 1u) && !fast)          // rare: panes outside the cached span
+        for (uint32_t j = 0; j < q.ppw; j++) {
+          const uint32_t g = find_slot(q, kk[i] + j);
+          if (g != kEmpty32) m[i] += q.acc_cnt32[(size_t)g * q.K + r[i].vidx];
+        }
+      else if (fast)
+        for (uint32_t j = kLr1MaxPpw; j < q.ppw; j++) {   // R/S > 8
+          const uint32_t g = s_slot[off + j];
+          if (g != kEmpty32) m[i] += q.acc_cnt32[(size_t)g * q.K + r[i].vidx];
+        }
     }
-    // compaction of the rows still needed into the other FIFO
-    const uint32_t km = __ballot_sync(0xffffffffu, keep);
-    uint32_t base = 0;
-    if ((threadIdx.x & 31) == 0 && km) base = atomicAdd(&st->fifo_count[cur ^ 1u], __popc(km));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) dst[base + __popc(km & ((1u << (threadIdx.x & 31)) - 1u))] = r;
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++)
+#pragma unroll
+      for (int j = 0; j < kLr1MaxPpw; j++) m[i] += c[i][j];
+    // warp-aggregated appends, item-major so that every store instruction writes consecutive
+    // rows: one atomic per warp and iteration on each cursor
+    uint32_t em[kLr1Items], km[kLr1Items], ne = 0, nk = 0;
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) {
+      em[i] = __ballot_sync(0xffffffffu, emit >> i & 1u);
+      km[i] = __ballot_sync(0xffffffffu, keep >> i & 1u);
+      ne += __popc(em[i]); nk += __popc(km[i]);
+    }
+    unsigned long long rbase = 0;
+    uint32_t fbase = 0;
+    if (lane == 0) {
+      if (ne) rbase = atomicAdd(&st->rows, (unsigned long long)ne);
+      if (nk) fbase = atomicAdd(&st->fifo_count[cur ^ 1u], nk);
+    }
+    rbase = __shfl_sync(0xffffffffu, rbase, 0);
+    fbase = __shfl_sync(0xffffffffu, fbase, 0);
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) {
+      if (emit >> i & 1u) {
+        const unsigned long long pos = rbase + __popc(em[i] & lt);
+        if (pos < q.row_cap) {
+          lms_lr1_row o;
+          o.win_start_s = kk[i] * (long long)q.S;
+          o.vehicle = q.lr1_dense ? r[i].vidx : q.dict.key_by_idx[r[i].vidx];
+          o.ts = r[i].ts; o.multiplicity = m[i]; o.speed = r[i].speed; o.xway = r[i].xway;
+          o.segment = r[i].seg; o.lane = r[i].lane; o.dir = r[i].dir;
+          rows[pos] = o;
+        } else {
+          atomicExch(&st->row_overflow, 1u);
+        }
+      }
+      if (keep >> i & 1u) dst[fbase + __popc(km[i] & lt)] = r[i];   // rows still needed
+      rbase += __popc(em[i]);
+      fbase += __popc(km[i]);
+    }
   }
   if (ticket(st)) finish(q, w);
 }
@@ -443,6 +501,9 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
 __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   DevState* st = q.state;
   const long long upto = st->evict_upto;
+  // nothing new to evict (no instance closed since the last eviction: a kept record's pane is
+  // always past the last emitted instance): every CTA sees the same values and returns
+  if (upto <= st->evicted_upto && !st->pane_fail) return;
   const uint32_t nk = q.lr1_dense ? q.K : min(st->n_keys, q.K);
   for (uint32_t g = 0; g < q.P; g++) {
     const uint32_t p = q.slot_pane[g];
@@ -452,7 +513,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   }
   if (ticket(st)) {
     evict_rebuild_cta(q, upto);
-    if (threadIdx.x == 0) { st->close_ticket = 0; __threadfence(); }
+    if (threadIdx.x == 0) { st->evicted_upto = upto; st->close_ticket = 0; __threadfence(); }
   }
 }
 
@@ -545,7 +606,8 @@ int close_ctas(const QueryDev& q) {
   }
   // LR2: ~3 keys per CTA, so each (key, entry-lane) thread walks only ~7 of the 2C partial
   // entries (the merge is load-latency bound, not bandwidth bound)
-  return q.kind == kLR2S ? 4 * nsm : nsm;
+  // LR1: the closing probe is load-latency bound (two 256-thread CTAs per SM at its register count)
+  return q.kind == kLR2S ? 4 * nsm : (q.kind == kLR1S || q.kind == kLR1T) ? 2 * nsm : nsm;
 }
 
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {

@@ -612,6 +612,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     DevState init{};
     init.ts_min = kEmpty32;
     init.wmx_min[0] = init.wmx_min[1] = kEmpty32;
+    init.evicted_upto = -(1ll << 62);
     init.free_top = (int)q->P;
     QC_TRY(cudaMemcpy(d.state, &init, sizeof(init), cudaMemcpyHostToDevice));
     QC_TRY(cudaDeviceSynchronize());
