@@ -14,4 +14,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cm_agg -s 2 -c 1 -o $OUT/cm2_agg python tools/prof_batch.py --workload cm2 --batches 3 > $OUT/ncu_cm2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lr_agg -s 2 -c 1 -o $OUT/lr2_agg python tools/prof_batch.py --workload lr2 --batches 3 > $OUT/ncu_lr2.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:k_close -s 2 -c 1 -o $OUT/lr2_close python tools/prof_batch.py --workload lr2 --batches 3 > $OUT/ncu_lr2c.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_close_lr1 -s 5 -c 1 -o $OUT/lr1_close python tools/prof_batch.py --workload lr1 --batches 7 --records 2000000 --flags 4 > $OUT/ncu_lr1c.log 2>&1
+{ for w in cm2 cm1 lr2; do echo "== $w"; timeout 300 python tools/prof_batch.py --workload $w --batches 4; done
+  for f in 0 4; do echo "== lr1 flags=$f (2M records per batch; batch 5 closes the first instance)"; timeout 300 python tools/prof_batch.py --workload lr1 --batches 7 --records 2000000 --flags $f; done; } > $OUT/kernel_timings_by_kind.txt 2>&1
 ls -la $OUT

@@ -55,7 +55,7 @@ def main(src, dst):
                 traffic[wl] = {"kernel": name, "dram_bytes_per_launch":
                                to_bytes(raw["dram__bytes_read.sum"]) + to_bytes(raw["dram__bytes_write.sum"]),
                                "duration": raw.get("gpu__time_duration.sum")}
-        elif f.startswith("launches_") or f in ("bench.json", "nvsmi.txt", "pytest_gpu.txt", "smoke.txt"):
+        elif f.startswith("launches_") or f in ("bench.json", "nvsmi.txt", "pytest_gpu.txt", "smoke.txt", "kernel_timings_by_kind.txt"):
             shutil.copy(p, os.path.join(dst, f))
     if traffic:
         tp = os.path.join(os.path.dirname(os.path.abspath(dst)), "ncu_traffic.json")
