@@ -428,9 +428,9 @@ def main():
                "proc_ms_p99": 1e3 * pct(e["proc_s"], 99), "h2d_ms_mean": 1e3 * statistics.mean(e["h2d_s"])}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        s = cpu_sample(wl["kind"], seconds=2, rate=450_000)
+        s = cpu_sample(wl["kind"], seconds=2, rate=800_000)   # ~10 s of oracle CPU
         cpu = {"value": s["records_per_s"], "unit": "records/s", "cores": 1, "kind": "oracle",
-               "sample": f"{s['records']} records (2 x 450000-record datasets of the same generator), "
+               "sample": f"{s['records']} records (2 x 800000-record datasets of the same generator), "
                          f"{s['elapsed_s']:.1f} s single-threaded Python"}
     if rank == 0:
         line = {

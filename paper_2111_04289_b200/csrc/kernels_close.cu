@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
 }
 
 // LR1: probe retained rows whose pane is the newest slide of a closing instance.
-constexpr int kLr1Items = 4;             // retained rows per thread and iteration
+constexpr int kLr1Items = 2;             // retained rows per thread and iteration
 constexpr int kLr1SlotCache = 1024;      // panes whose slots a CTA resolves up front
 constexpr int kLr1MaxPpw = 8;            // window panes summed with unrolled loads
 __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) {
@@ -607,7 +607,7 @@ int close_ctas(const QueryDev& q) {
   // LR2: ~3 keys per CTA, so each (key, entry-lane) thread walks only ~7 of the 2C partial
   // entries (the merge is load-latency bound, not bandwidth bound)
   // LR1: the closing probe is load-latency bound (two 256-thread CTAs per SM at its register count)
-  return q.kind == kLR2S ? 4 * nsm : (q.kind == kLR1S || q.kind == kLR1T) ? 2 * nsm : nsm;
+  return q.kind == kLR2S ? 4 * nsm : (q.kind == kLR1S || q.kind == kLR1T) ? 4 * nsm : nsm;
 }
 
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {
