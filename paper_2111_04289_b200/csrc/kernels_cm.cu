@@ -714,6 +714,37 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       } else {
         // CM1: reduce per (pane, category) inside the warp
         bool pend = surv;
+        const uint32_t s_all = __ballot_sync(0xffffffffu, surv);
+        if (s_all) {
+          const uint32_t p0 = __shfl_sync(0xffffffffu, p, __ffs(s_all) - 1);
+          if (__all_sync(0xffffffffu, !surv || p == p0)) {
+            // the usual round: every record in one pane — per category c <= the largest
+            // present, one REDUX sum and one ballot count; lane c then adds category c's
+            const uint32_t cmax = __reduce_max_sync(0xffffffffu, surv ? r.cat : 0u);
+            uint32_t my_s = 0, my_n = 0;
+            for (uint32_t c = 0; c <= cmax; c++) {
+              const bool me = surv && r.cat == c;
+              const uint32_t sc = __reduce_add_sync(0xffffffffu, me ? r.cpu_m : 0u);   // < 32 * 1e7
+              const uint32_t nc = __popc(__ballot_sync(0xffffffffu, me));
+              my_s = sel((uint32_t)lane == c, sc, my_s);
+              my_n = sel((uint32_t)lane == c, nc, my_n);
+            }
+            if (my_n) {
+              if (p0 != c_pane) { c_pane = p0; local_slot(slot_tag, q, p0, c_slot, c_gslot); }
+              if (c_gslot == kFail32) n_ovf += my_n;
+              else if (c_slot < 2) {
+                w_sum[warp][c_slot][lane] += my_s;
+                w_cnt[warp][c_slot][lane] += my_n;
+              } else {
+                const size_t gi = (size_t)c_gslot * q.K + lane;
+                atomicAdd(&q.acc_sum[gi], (unsigned long long)my_s);
+                atomicAdd(&q.acc_cnt[gi], (unsigned long long)my_n);
+              }
+            }
+            pend = false;
+            __syncwarp();   // order lane c's accumulator update before any later leader's
+          }
+        }
         uint32_t left = __ballot_sync(0xffffffffu, pend);
         while (left) {
           const int leader = __ffs(left) - 1;

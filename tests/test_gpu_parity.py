@@ -210,6 +210,30 @@ def test_cm_fast_path_fuzz():
         compare_run(q, prod, oracle_rows(q, batches))
 
 
+def test_cm_mixed_panes_in_warp_rounds():
+    """Records whose timestamps jump around inside a batch (every warp round of 32 lines spans
+    several panes) and categories 0..9: CM1's per-(pane, category) reduction takes its general
+    path (the single-pane fast path only when a round is uniform), CM2's survivor drain mixes
+    pane slots; both against the oracle.  Batch 2 overlaps batch 1's time range, so its records
+    older than the watermark are dropped as late (reading R7) exactly as the oracle drops them."""
+    rng = random.Random(4289)
+    digits = lambda n: "".join(rng.choice("0123456789") for _ in range(n))
+
+    def lines(t0, t1, n, uniform_every=0):
+        out = []
+        for i in range(n):
+            # every `uniform_every`-th block of 64 lines keeps one ts (fast-path rounds in between)
+            ts = t0 if uniform_every and (i // 64) % uniform_every == 0 else rng.randrange(t0, t1)
+            out.append(_cm_line(ts=str(ts), job=str(10 ** 9 + rng.randrange(50)), ev=str(rng.choice([1, 1, 0, 4])),
+                                cat=str(rng.randrange(10)), cpu="0." + digits(6),
+                                user="".join(rng.choice("ABCdef+/019") for _ in range(rng.randint(20, 60)))))
+        return b"".join(out)
+    batches = [[lines(100, 160, 5000, uniform_every=3)], [lines(150, 230, 5000, uniform_every=2)]]
+    for q in ("CM1S", "CM1T", "CM2S"):
+        prod = product_run(q, batches)
+        compare_run(q, prod, oracle_rows(q, batches))
+
+
 def _pipelined_run(qname, batches, device_mask):
     """Push a batch's datasets, force it WITHOUT syncing (LMS_FLAG_PIPELINE: the previous batch
     may still run), sync only at the end; returns (rows of all batches, batch records)."""
