@@ -425,7 +425,9 @@ def main():
         e2e = {"value": wl["records"] * world * args.e2e_steps / e["elapsed_s"], "unit": "records/s",
                "h2d_bytes_per_step": e["h2d_bytes_per_step"], "d2h_bytes_per_step": e["d2h_bytes_per_step"],
                "steps": args.e2e_steps, "proc_ms_p50": 1e3 * pct(e["proc_s"], 50),
-               "proc_ms_p99": 1e3 * pct(e["proc_s"], 99), "h2d_ms_mean": 1e3 * statistics.mean(e["h2d_s"])}
+               "proc_ms_p99": 1e3 * pct(e["proc_s"], 99), "h2d_ms_mean": 1e3 * statistics.mean(e["h2d_s"]),
+               # the e2e leg is bound by the host link: its achieved pinned H2D bandwidth
+               "h2d_gbs": e["h2d_bytes_per_step"] / statistics.mean(e["h2d_s"]) / 1e9}
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         s = cpu_sample(wl["kind"], seconds=2, rate=800_000)   # ~10 s of oracle CPU
