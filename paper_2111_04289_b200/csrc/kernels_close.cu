@@ -118,32 +118,40 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
     st->owner_cursor[i] = 0;
   }
   if (threadIdx.x == 0) {
-    st->close_k_first = 0;
-    st->close_k_last = -1;
+    // every field is read up front, in one round trip: interleaved with the report stores
+    // (which may alias as far as the compiler knows) each load would wait for the last one
+    const unsigned long long wm = st->wm, n_records = st->n_records, bad = st->bad, late = st->late,
+                             overflow = st->overflow, rows = st->rows, wclosed = st->windows_closed;
+    const uint32_t n_keys = st->n_keys, row_ovf = st->row_overflow, key_ovf = st->key_overflow,
+                   fifo_ovf = st->fifo_overflow, fcur = st->fifo_cur;
+    long long ck_first = 0, ck_last = -1;
+    unsigned long long wc = wclosed;
     if (w.any) {
-      const long long closed = w.k_last >= w.nk ? (w.k_last - w.nk + 1) : 0;
-      st->windows_closed += (unsigned long long)closed;
-      st->close_k_first = w.nk;
-      st->close_k_last = w.k_last;
+      wc += (unsigned long long)(w.k_last >= w.nk ? (w.k_last - w.nk + 1) : 0);
+      ck_first = w.nk;
+      ck_last = w.k_last;
       st->evict_upto = w.k_last;
       st->next_k = w.k_last + 1 > w.nk ? w.k_last + 1 : w.nk;
       st->next_k_valid = 1;
     }
     if (lr1 && swap_fifo) {
-      st->fifo_count[st->fifo_cur] = 0;
-      st->fifo_cur ^= 1u;
+      st->fifo_count[fcur] = 0;
+      st->fifo_cur = fcur ^ 1u;
     }
-    st->wm_prev = st->wm;
-    st->part_rows = st->rows < q.row_cap ? st->rows : q.row_cap;
+    const unsigned long long part_rows = rows < q.row_cap ? rows : q.row_cap;
+    st->close_k_first = ck_first;
+    st->close_k_last = ck_last;
+    st->wm_prev = wm;
+    st->part_rows = part_rows;
     BatchReport* r = q.report;
-    r->n_records = st->n_records; r->bad = st->bad; r->late = st->late; r->overflow = st->overflow;
-    r->rows = st->rows; r->windows_closed = st->windows_closed;
-    r->watermark = st->wm ? (long long)st->wm - 1 : -1;
-    r->n_keys = st->n_keys; r->row_overflow = st->row_overflow; r->key_overflow = st->key_overflow;
-    r->fifo_overflow = st->fifo_overflow;
-    r->close_k_first = st->close_k_first;
-    r->close_k_last = st->close_k_last;
-    r->part_rows = st->part_rows;
+    r->n_records = n_records; r->bad = bad; r->late = late; r->overflow = overflow;
+    r->rows = rows; r->windows_closed = wc;
+    r->watermark = wm ? (long long)wm - 1 : -1;
+    r->n_keys = n_keys; r->row_overflow = row_ovf; r->key_overflow = key_ovf;
+    r->fifo_overflow = fifo_ovf;
+    r->close_k_first = ck_first;
+    r->close_k_last = ck_last;
+    r->part_rows = part_rows;
     st->n_records = st->bad = st->late = st->overflow = st->rows = st->windows_closed = 0;
     st->row_overflow = 0;
     st->fifo_overflow = 0;
