@@ -32,6 +32,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
 }
 // global -> shared, bytes % 16 == 0, both addresses 16-byte aligned; completes on mbarrier b.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  // (no L2 evict-first hint here, unlike the CM copies: measured 3 % slower on LR2, where no
+  // table competes with the stream for L2)
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_addr(dst)),

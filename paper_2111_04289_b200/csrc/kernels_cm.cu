@@ -172,9 +172,13 @@ __device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t phase) {
       " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra CM_WAIT;\n}" ::"r"(bar), "r"(phase) : "memory");
 }
+// The input is read once: copies carry an L2 evict-first policy, so a 1.4 GB micro-batch does
+// not push the jobId dictionary and the pane accumulators out of the 126 MB L2 (J = 10^6 keys:
+// 0.48 -> 0.40 ms per 10M records; J = 10^4: unchanged).
 __device__ __forceinline__ void issue_s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+  asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"   // read-once input
+               " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 // Issue the copy of the producer iterator's tile into stage `dst` (full tiles: constant size).
