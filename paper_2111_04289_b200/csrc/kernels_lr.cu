@@ -110,6 +110,7 @@ struct LrArgs {
 
 // Issue the bulk copy for global tile `tile` into stage buffer `dst` (the <16 B remainder of
 // a segment's last tile is copied by threads later).
+template <bool EVICT_FIRST>
 __device__ __forceinline__ void lr_issue(const SegTable& segs, SegCursor& c, unsigned long long tile,
                                         uint8_t* dst, uint64_t* bar) {
   c.seek(segs, tile);
@@ -118,7 +119,10 @@ __device__ __forceinline__ void lr_issue(const SegTable& segs, SegCursor& c, uns
   const uint32_t bytes = (uint32_t)(rem < (unsigned long long)kLrTileBytes ? rem : kLrTileBytes);
   const uint32_t bulk = bytes & ~15u;
   mbar_arrive_expect_tx(bar, bulk);
-  if (bulk) bulk_g2s(dst, segs.s[c.si].ptr + off, bulk, bar);
+  if (bulk) {
+    if (EVICT_FIRST) bulk_g2s_evict_first(dst, segs.s[c.si].ptr + off, bulk, bar);
+    else bulk_g2s(dst, segs.s[c.si].ptr + off, bulk, bar);
+  }
 }
 
 template <int KIND>
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   iss.init(a.segs);
   if (tid == 0) {
     for (int s = 0; s < kLrStages; s++)
-      if (t0 + s < t1) lr_issue(a.segs, iss, t0 + s, stage + s * kLrTileBytes, &full[s]);
+      if (t0 + s < t1) lr_issue<kLR1>(a.segs, iss, t0 + s, stage + s * kLrTileBytes, &full[s]);
   }
 
   const unsigned long long wm_prev = q.state->wm_prev;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
       }
     }
     __syncthreads();   // stage s fully consumed
-    if (tid == 0 && t + kLrStages < t1) lr_issue(a.segs, iss, t + kLrStages, buf, &full[s]);
+    if (tid == 0 && t + kLrStages < t1) lr_issue<kLR1>(a.segs, iss, t + kLrStages, buf, &full[s]);
   }
 
   if (!kLR1) {
