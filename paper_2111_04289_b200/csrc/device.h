@@ -92,7 +92,7 @@ struct SegTable {
 };
 
 // Retained LR1 row (projection of the 7 output columns; vehicle via dictionary index).
-struct Lr1Retained {
+struct __align__(16) Lr1Retained {
   uint32_t ts;
   uint32_t vidx;
   uint16_t speed, xway, seg;

@@ -430,7 +430,10 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
       const uint32_t idx = base + i * blockDim.x + threadIdx.x;   // coalesced 16 B loads
       m[i] = 0; kk[i] = 0;
       if (idx < n) {
-        r[i] = src[idx];
+        {   // read once: streaming load (the FIFO is not re-read from L2)
+          const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + idx));
+          r[i] = *reinterpret_cast<const Lr1Retained*>(&v);
+        }
         if (r[i].vidx != kEmpty32) {          // (holes: records the aggregate pass dropped)
           const long long p = (long long)pane_of(r[i].ts, q.S, q.div_magic);
           kk[i] = p - (long long)q.ppw + 1;   // instance whose newest slide is pane p
@@ -492,7 +495,10 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
           o.vehicle = q.lr1_dense ? r[i].vidx : q.dict.key_by_idx[r[i].vidx];
           o.ts = r[i].ts; o.multiplicity = m[i]; o.speed = r[i].speed; o.xway = r[i].xway;
           o.segment = r[i].seg; o.lane = r[i].lane; o.dir = r[i].dir;
-          rows[pos] = o;
+          // streaming stores: 320 MB of rows per 10M probes must not evict the count tables
+          const uint4* ov = reinterpret_cast<const uint4*>(&o);
+          __stcs(reinterpret_cast<uint4*>(rows + pos), ov[0]);
+          __stcs(reinterpret_cast<uint4*>(rows + pos) + 1, ov[1]);
         } else {
           atomicExch(&st->row_overflow, 1u);
         }

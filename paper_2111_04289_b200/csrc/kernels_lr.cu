@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
             Lr1Retained row;
             row.ts = r.ts; row.vidx = vidx; row.speed = (uint16_t)r.speed; row.xway = (uint16_t)r.xway;
             row.seg = (uint16_t)r.seg; row.lane = (uint8_t)r.lane; row.dir = (uint8_t)r.dir;
-            q.fifo[s_fcur][pos] = row;
+            __stcs(reinterpret_cast<uint4*>(q.fifo[s_fcur] + pos), *reinterpret_cast<const uint4*>(&row));
           } else if (vidx != kEmpty32) {
             atomicExch(&q.state->fifo_overflow, 1u);
             cnt.overflow++;
