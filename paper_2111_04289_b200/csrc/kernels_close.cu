@@ -576,7 +576,9 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_probe(const QueryDev q, l
         o.vehicle = r.vidx;
         o.ts = r.ts; o.multiplicity = q.lr1_w[r.vidx]; o.speed = r.speed; o.xway = r.xway;
         o.segment = r.seg; o.lane = r.lane; o.dir = r.dir;
-        rows[pos] = o;
+        const uint4* ov = reinterpret_cast<const uint4*>(&o);   // two 16 B streaming stores
+        __stcs(reinterpret_cast<uint4*>(rows + pos), ov[0]);
+        __stcs(reinterpret_cast<uint4*>(rows + pos) + 1, ov[1]);
       } else {
         atomicExch(&st->row_overflow, 1u);
       }
