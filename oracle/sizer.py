@@ -48,9 +48,20 @@ def est_max_lat(now: float, datasets, avg_thput_prev: float) -> float:
     return max_buff + total / avg_thput_prev
 
 
+def seq_sum(xs) -> float:
+    """Plain left-to-right fp64 sum in batch order (reading R28).  Not Python's sum(): since
+    3.12 that is a compensated (Neumaier) sum, a different rounding from the online running
+    sum the method keeps, and an admission decision (EstMaxLat >= target) compares values
+    that can differ in the last bit."""
+    s = 0.0
+    for x in xs:
+        s += x
+    return s
+
+
 def avg_thput(batch_bytes: list[int], procs: list[float]) -> float:
     """Eq. 4 over batches 0..i."""
-    return sum(batch_bytes) / sum(procs)
+    return sum(batch_bytes) / seq_sum(procs)
 
 
 def max_lat(max_buff: float, proc: float) -> float:
@@ -94,7 +105,7 @@ def construct_micro_batch(buffered, new_files, now: float, *, mode: str, slide_s
     else:
         if len(max_lat_history) < 2:
             return Decision(True, tmp, est_max_lat=est, reason="tumbling-bootstrap")
-        mean = sum(max_lat_history) / len(max_lat_history)
+        mean = seq_sum(max_lat_history) / len(max_lat_history)
         if est >= mean:
             return Decision(True, tmp, est_max_lat=est, reason="tumbling")
     return Decision(False, carried=tmp, est_max_lat=est, reason="buffer")
