@@ -413,6 +413,9 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
   const bool cached = pspan <= kLr1SlotCache;
   if (cached)
     for (uint32_t j = threadIdx.x; j < (uint32_t)pspan; j += blockDim.x) s_slot[j] = find_slot(q, pbase + j);
+  __shared__ uint32_t s_wtot[kCloseThreads / 32], s_woff[kCloseThreads / 32];
+  __shared__ unsigned long long s_rbase;
+  __shared__ uint32_t s_fbase;
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
@@ -477,14 +480,26 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
       km[i] = __ballot_sync(0xffffffffu, keep >> i & 1u);
       ne += __popc(em[i]); nk += __popc(km[i]);
     }
-    unsigned long long rbase = 0;
-    uint32_t fbase = 0;
-    if (lane == 0) {
-      if (ne) rbase = atomicAdd(&st->rows, (unsigned long long)ne);
-      if (nk) fbase = atomicAdd(&st->fifo_count[cur ^ 1u], nk);
+    // CTA-wide appends: warp totals -> thread 0 -> one atomic per cursor per CTA and iteration
+    // (per-warp atomics on the two global cursors were the probe's main serialisation)
+    const uint32_t warp = threadIdx.x >> 5;
+    if (lane == 0) s_wtot[warp] = ne | (nk << 16);          // <= 64 rows each per warp
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t e_acc = 0, k_acc = 0;
+      for (uint32_t wi = 0; wi < blockDim.x / 32u; wi++) {
+        const uint32_t t = s_wtot[wi];
+        s_woff[wi] = e_acc | (k_acc << 16);
+        e_acc += t & 0xFFFFu;
+        k_acc += t >> 16;
+      }
+      s_rbase = e_acc ? atomicAdd(&st->rows, (unsigned long long)e_acc) : 0ull;
+      s_fbase = k_acc ? atomicAdd(&st->fifo_count[cur ^ 1u], k_acc) : 0u;
     }
-    rbase = __shfl_sync(0xffffffffu, rbase, 0);
-    fbase = __shfl_sync(0xffffffffu, fbase, 0);
+    __syncthreads();
+    const uint32_t wo = s_woff[warp];
+    unsigned long long rbase = s_rbase + (wo & 0xFFFFu);
+    uint32_t fbase = s_fbase + (wo >> 16);
 #pragma unroll
     for (int i = 0; i < kLr1Items; i++) {
       if (emit >> i & 1u) {
