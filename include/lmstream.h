@@ -116,9 +116,10 @@ typedef struct {
                                        report / row buffers); lms_sync and reads complete
                                        them in order.  Stream order keeps window state exact. */
 #define LMS_FLAG_DENSE_VEHICLES 0x4u /* LR1: vehicle ids index the per-pane counts directly
-                                       (VID < max_keys; larger VIDs are dropped and counted as
-                                       overflow) instead of the key dictionary.  Always on for
-                                       multi-GPU LR1.                                       */
+                                       (VID < max_keys) instead of the key dictionary.  A record
+                                       with VID >= max_keys is rejected: dropped, counted in
+                                       overflow_records, and its batch completes with
+                                       LMS_EINVAL.  Always on for multi-GPU LR1.              */
 
 /* One aggregate result row (LR2S, CM1S, CM1T, CM2S) of window instance
  * [win_start_s, win_end_s) (readings R5/R6 in DESIGN.md).                    */
@@ -201,12 +202,25 @@ lms_status  lms_query_destroy(lms_query* q);          /* NULL is a no-op        
 /* Push one dataset (whole records: LR nbytes % 70 == 0; CM ends with '\n').
  * The bytes are copied to device memory before return (the caller's buffer is
  * free on return); pinned caller memory takes the direct DMA path.
- * ingest_time_s must be non-decreasing.  nbytes > 0.                          */
+ * ingest_time_s must be non-decreasing.  nbytes > 0.  The datasets buffered for
+ * one micro-batch (host-pushed and borrowed together) may total at most 2^37 B:
+ * beyond it LMS_EOVERFLOW (admit what is buffered first); host-pushed bytes are
+ * also bounded by cfg.max_batch_bytes (LMS_EOVERFLOW).                        */
 lms_status  lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double ingest_time_s,
                      uint64_t* dataset_id_out);
+/* Asynchronous push of a dataset in PAGE-LOCKED host memory (cudaHostAlloc'd or
+ * cudaHostRegister'ed; else LMS_EINVAL): the H2D copy into the library's staging
+ * buffer is enqueued on the handle's copy stream and the call returns at once, so
+ * the copy of the next micro-batch overlaps the kernels of the running one (the
+ * batch's kernels wait for it on the device).  The host buffer is BORROWED until
+ * the batch containing the dataset completes (lms_sync / a later lms_poll); its
+ * device-timed H2D is reported in the batch record's h2d_s.  Same checks and caps
+ * as lms_push.                                                                */
+lms_status  lms_push_pinned(lms_query* q, const void* bytes, uint64_t nbytes, double ingest_time_s,
+                            uint64_t* dataset_id_out);
 /* Push a dataset already in device memory of the query's device (16-byte
  * aligned).  The buffer is BORROWED until the batch containing it completes
- * (lms_sync / a later lms_poll returns).                                     */
+ * (lms_sync / a later lms_poll returns).  Same 2^37 B per-batch cap as lms_push. */
 lms_status  lms_push_device(lms_query* q, const void* dptr, uint64_t nbytes, double ingest_time_s,
                             uint64_t* dataset_id_out);
 
@@ -223,8 +237,9 @@ lms_status  lms_force_batch(lms_query* q, double now_s, uint64_t* batch_index);
 lms_status  lms_flush(lms_query* q, double now_s);
 /* Wait for the in-flight batch (no-op if none); move its rows to the host
  * queue and fill its batch record.  Returns LMS_EFORMAT if it contained
- * malformed records, LMS_EOVERFLOW if a capacity was exceeded (rows of valid
- * records are still delivered).                                              */
+ * malformed records, LMS_EOVERFLOW if a capacity was exceeded, LMS_EINVAL if a
+ * dense-vehicle LR1 batch held a VID >= max_keys (rows of the valid records
+ * are still delivered in every case).                                        */
 lms_status  lms_sync(lms_query* q);
 
 /* ------------------------------------------------------------------ results */
@@ -319,7 +334,7 @@ lms_status  lms_p2p_collect(lms_query* q);
 lms_status  lms_p2p_device_watermark(lms_query* q, int32_t enable);
 
 /* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
- * index the per-pane counts directly (VID < max_keys; larger VIDs count as overflow), every
+ * index the per-pane counts directly (VID < max_keys; a larger VID is rejected: LMS_EINVAL), every
  * rank keeps and probes its own rows, and the multiplicity m of a probed row counts the
  * vehicle in the whole window over ALL ranks.  Per micro-batch, after the watermark
  * all-reduce and before lms_run_close:
@@ -333,6 +348,16 @@ lms_status  lms_p2p_device_watermark(lms_query* q, int32_t enable);
  * ESTATE: not a multi-GPU LR1 handle, or no aggregate pass awaiting its close.          */
 lms_status  lms_lr1_window_counts(lms_query* q, int64_t k, void** counts_dptr, uint64_t* n_counts);
 lms_status  lms_lr1_probe(lms_query* q, int64_t k);
+
+/* Record-boundary row partition of one dataset for `parts` GPUs (the paper's
+ * partitioning of a micro-batch): offsets[0..parts] (caller-owned, parts + 1 entries),
+ * offsets[0] = 0, offsets[parts] = nbytes, non-decreasing, every range whole records.  LR
+ * (kind LR*): cut i = the 70 B multiple at or below i*nbytes/parts.  CM: cut i = the first
+ * byte after a '\n' at or after i*nbytes/parts (a part may be empty when records are longer
+ * than nbytes/parts).  `bytes` may be host or device memory (device: only the bytes around
+ * each cut are read).  EINVAL: null / empty, LR size not a multiple of 70, CM not ending in
+ * '\n'.                                                                                   */
+lms_status  lms_split(int32_t kind, const void* bytes, uint64_t nbytes, uint32_t parts, uint64_t* offsets);
 
 /* ------------------------------------------------------------------ timing hooks */
 /* Device time of the last completed batch's kernels, and of its dominant

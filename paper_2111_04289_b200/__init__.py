@@ -76,6 +76,12 @@ class Query:
         check(L.lms_push(self.h, C.c_void_p(ptr), n, ingest_time, C.byref(did)), "lms_push")
         return did.value
 
+    def push_pinned(self, ptr: int, nbytes: int, ingest_time: float) -> int:
+        """Asynchronous push of page-locked host memory (borrowed until its batch completes)."""
+        did = C.c_uint64()
+        check(L.lms_push_pinned(self.h, C.c_void_p(ptr), nbytes, ingest_time, C.byref(did)), "lms_push_pinned")
+        return did.value
+
     def push_device(self, dptr: int, nbytes: int, ingest_time: float) -> int:
         did = C.c_uint64()
         check(L.lms_push_device(self.h, C.c_void_p(dptr), nbytes, ingest_time, C.byref(did)), "lms_push_device")
@@ -148,3 +154,12 @@ class Query:
         n = C.c_uint64()
         check(L.lms_kernel_launches(self.h, C.byref(n)), "lms_kernel_launches")
         return n.value
+
+
+def percentile(values, p: float) -> float:
+    """Nearest-rank percentile computed by the library (lms_percentile)."""
+    v = np.ascontiguousarray(np.asarray(values, dtype=np.float64))
+    out = C.c_double()
+    check(L.lms_percentile(v.ctypes.data_as(C.POINTER(C.c_double)), len(v), float(p), C.byref(out)),
+          "lms_percentile")
+    return out.value

@@ -95,6 +95,7 @@ _PROTOS = {
     "lms_query_create": (C.c_int32, [_P(lms_config), _P(_Q)]),
     "lms_query_destroy": (C.c_int32, [_Q]),
     "lms_push": (C.c_int32, [_Q, C.c_void_p, C.c_uint64, C.c_double, _P(C.c_uint64)]),
+    "lms_push_pinned": (C.c_int32, [_Q, C.c_void_p, C.c_uint64, C.c_double, _P(C.c_uint64)]),
     "lms_push_device": (C.c_int32, [_Q, C.c_void_p, C.c_uint64, C.c_double, _P(C.c_uint64)]),
     "lms_poll": (C.c_int32, [_Q, C.c_double, _P(C.c_int32), _P(C.c_uint64)]),
     "lms_force_batch": (C.c_int32, [_Q, C.c_double, _P(C.c_uint64)]),
@@ -121,6 +122,7 @@ _PROTOS = {
     "lms_p2p_exchange_async": (C.c_int32, [_Q]),
     "lms_p2p_collect": (C.c_int32, [_Q]),
     "lms_p2p_device_watermark": (C.c_int32, [_Q, C.c_int32]),
+    "lms_split": (C.c_int32, [C.c_int32, C.c_void_p, C.c_uint64, C.c_uint32, _P(C.c_uint64)]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "lms_kernel_launches": (C.c_int32, [_Q, _P(C.c_uint64)]),
     "lms_est_max_lat": (C.c_int32, [_P(C.c_double), _P(C.c_uint64), C.c_uint64, C.c_double, _P(C.c_double)]),

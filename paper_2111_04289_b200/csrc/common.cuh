@@ -91,17 +91,19 @@ __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long k
     unsigned long long k, kv;
     asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(kv) : "l"(ent));
     if (k == kEmpty64) {
-      k = atomicCAS(ent, kEmpty64, key);
+      // inserts are rare (one per distinct key) and may race with peer GPUs' inserts into the
+      // same dictionary (multi-GPU fused exchange, dict_get_sys): system-scope RMWs
+      k = atomicCAS_system(ent, kEmpty64, key);
       if (k == kEmpty64) {     // we own the entry: allocate the index and publish it
-        uint32_t idx = atomicAdd(&st->n_keys, 1u);
+        uint32_t idx = atomicAdd_system(&st->n_keys, 1u);
         if (idx >= d.max_keys) {
           atomicExch(&st->key_overflow, 1u);
           idx = kEmpty32 - 1;   // poison: entry exists but is unusable
         } else {
           d.key_by_idx[idx] = key;
         }
-        __threadfence();
-        atomicExch(reinterpret_cast<unsigned int*>(ent + 1), idx);
+        __threadfence_system();
+        atomicExch_system(reinterpret_cast<unsigned int*>(ent + 1), idx);
         return idx >= d.max_keys ? kEmpty32 : idx;
       }
       kv = kEmpty32;            // someone else inserted: re-read its index below if it is ours

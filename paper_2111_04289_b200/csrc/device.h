@@ -23,6 +23,10 @@ constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 constexpr uint32_t kFail32 = 0xFFFFFFFEu;   // pane table full: the pane's records overflow
 constexpr unsigned long long kEmpty64 = ~0ull;
 constexpr int kMaxSegs = 128;                          // input segments per aggregate launch
+// Bytes of one micro-batch (host-pushed + borrowed segments).  Bounds the LR2 per-CTA u32
+// partials: a CTA of the 296-CTA grid sees <= 2^37 / 70 / 296 < 6.7e6 records of a batch, so a
+// key's speed sum (<= 100 per record) stays < 6.7e8 < 2^32 even if every record has that key.
+constexpr unsigned long long kMaxBatchTotal = 1ull << 37;
 constexpr int kMaxWorld = 64;                          // multi-GPU ranks
 constexpr int kLrRecBytes = 70;
 constexpr int kLrTileRecs = 512;                       // 256 threads x 2 records
@@ -51,6 +55,7 @@ struct DevState {
   unsigned int close_ticket;
   unsigned int n_keys;          // dictionary entries in use
   unsigned int key_overflow;
+  unsigned int vid_range;       // dense-vehicle LR1: a record's VID was >= max_keys (rejected)
   unsigned int fifo_count[2];   // LR1 retained-row FIFO sizes
   unsigned int fifo_cur;        // LR1: which FIFO holds the live rows
   unsigned int fifo_overflow;
@@ -74,7 +79,7 @@ struct DevState {
 struct BatchReport {
   unsigned long long n_records, bad, late, overflow, rows, windows_closed;
   long long watermark;          // -1 if none
-  unsigned int n_keys, row_overflow, key_overflow, fifo_overflow;
+  unsigned int n_keys, row_overflow, key_overflow, fifo_overflow, vid_range;
   long long close_k_first, close_k_last;
   unsigned long long part_rows;
   unsigned int owner_count[kMaxWorld];

@@ -123,7 +123,7 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
     const unsigned long long wm = st->wm, n_records = st->n_records, bad = st->bad, late = st->late,
                              overflow = st->overflow, rows = st->rows, wclosed = st->windows_closed;
     const uint32_t n_keys = st->n_keys, row_ovf = st->row_overflow, key_ovf = st->key_overflow,
-                   fifo_ovf = st->fifo_overflow, fcur = st->fifo_cur;
+                   fifo_ovf = st->fifo_overflow, fcur = st->fifo_cur, vid_rng = st->vid_range;
     long long ck_first = 0, ck_last = -1;
     unsigned long long wc = wclosed;
     if (w.any) {
@@ -149,6 +149,7 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
     r->watermark = wm ? (long long)wm - 1 : -1;
     r->n_keys = n_keys; r->row_overflow = row_ovf; r->key_overflow = key_ovf;
     r->fifo_overflow = fifo_ovf;
+    r->vid_range = vid_rng;
     r->close_k_first = ck_first;
     r->close_k_last = ck_last;
     r->part_rows = part_rows;
@@ -156,6 +157,7 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
     st->row_overflow = 0;
     st->fifo_overflow = 0;
     st->key_overflow = 0;
+    st->vid_range = 0;
     st->ts_min = kEmpty32;
     st->close_ticket = 0;
     __threadfence();
@@ -255,11 +257,12 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   __shared__ uint32_t wslots[256];   // R/S <= 256
 
   // Most batches close no window (slide S > batch span): nothing to merge (CM: the aggregate
-  // pass wrote the pane accumulators directly), emit or evict — CTA 0 alone advances the state.
-  // (finish() leaves wm / next_k as they are when nothing closes, so a late CTA that reads the
-  // state after it computes the same empty range.)
+  // pass wrote the pane accumulators directly), emit or evict.  The state is still advanced by
+  // the LAST CTA to arrive (ticket), never by a fixed CTA: finish() rewrites next_k /
+  // next_k_valid / ts_min, and a CTA that had not read them yet could otherwise see a torn
+  // snapshot (next_k_valid = 1 with a stale next_k) and close instances that do not exist.
   if (q.kind != kLR2S && !(w.any && w.k_last >= w.nk)) {
-    if (blockIdx.x == 0) finish(q, w);
+    if (ticket(st)) finish(q, w);
     return;
   }
 
@@ -395,9 +398,10 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
   DevState* st = q.state;
   const WinRange w = win_range(q, a.flush);
   // no instance closes (most batches): the retained rows all stay — leave the FIFO as it is
-  // instead of copying every row into the other FIFO; CTA 0 advances the state
+  // instead of copying every row into the other FIFO; the last CTA to arrive advances the
+  // state (after every CTA has read it: see k_close_agg)
   if (!(w.any && w.k_last >= w.nk)) {
-    if (blockIdx.x == 0) finish(q, w, false);
+    if (ticket(st)) finish(q, w, false);
     return;
   }
   const uint32_t cur = st->fifo_cur;

@@ -93,17 +93,17 @@ __device__ __forceinline__ uint32_t dict_get_sys(const Dict& d, unsigned long lo
     unsigned long long k, kv;
     asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(k), "=l"(kv) : "l"(ent));
     if (k == kEmpty64) {
-      k = atomicCAS(ent, kEmpty64, key);
+      k = atomicCAS_system(ent, kEmpty64, key);
       if (k == kEmpty64) {     // we own the entry: allocate the index and publish it
-        uint32_t idx = atomicAdd(&st->n_keys, 1u);
+        uint32_t idx = atomicAdd_system(&st->n_keys, 1u);
         if (idx >= d.max_keys) {
-          atomicExch(&st->key_overflow, 1u);
+          atomicExch_system(&st->key_overflow, 1u);
           idx = kEmpty32 - 1;   // poison: entry exists but is unusable
         } else {
           d.key_by_idx[idx] = key;
         }
         __threadfence_system();
-        atomicExch(reinterpret_cast<unsigned int*>(ent + 1), idx);
+        atomicExch_system(reinterpret_cast<unsigned int*>(ent + 1), idx);
         return idx >= d.max_keys ? kEmpty32 : idx;
       }
       kv = kEmpty32;            // someone else inserted: re-read its index below if it is ours
@@ -115,7 +115,7 @@ __device__ __forceinline__ uint32_t dict_get_sys(const Dict& d, unsigned long lo
     }
     h = (h + 1) & d.cap_mask;
   }
-  atomicExch(&st->key_overflow, 1u);   // every entry taken by other keys: this key is dropped
+  atomicExch_system(&st->key_overflow, 1u);   // every entry taken by other keys: this key is dropped
   return kEmpty32;
 }
 
@@ -134,8 +134,8 @@ __global__ void __launch_bounds__(kThreads) k_p2p_push(const QueryDev q, long lo
     else idx = (uint32_t)r.key;
     if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
     const size_t g = (size_t)w * q.K + idx;
-    atomicAdd(&P.macc_sum[g], r.sum_fixed);
-    atomicAdd(&P.macc_cnt[g], r.count);
+    atomicAdd_system(&P.macc_sum[g], r.sum_fixed);   // remote (peer GPU) RMW: system scope
+    atomicAdd_system(&P.macc_cnt[g], r.count);
   }
   __threadfence_system();
 }
@@ -196,8 +196,8 @@ __global__ void __launch_bounds__(kThreads) k_p2p_push_async(const QueryDev q) {
     else idx = (uint32_t)r.key;
     if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
     const size_t g = (size_t)w * q.K + idx;
-    atomicAdd(&P.macc_sum[g], r.sum_fixed);
-    atomicAdd(&P.macc_cnt[g], r.count);
+    atomicAdd_system(&P.macc_sum[g], r.sum_fixed);   // remote (peer GPU) RMW: system scope
+    atomicAdd_system(&P.macc_cnt[g], r.count);
   }
   __threadfence_system();
   __syncthreads();

@@ -220,6 +220,9 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
             vidx = c_gslot == kFail32 ? kEmpty32
                  : q.lr1_dense ? (r.vid < K ? (uint32_t)r.vid : kEmpty32)
                                : dict_get(q.dict, r.vid, q.state);
+            // dense-vehicle mode cannot represent a VID >= max_keys: the batch is rejected
+            // (LMS_EINVAL at its completion), not silently counted as overflow
+            if (q.lr1_dense && r.vid >= K && c_gslot != kFail32) atomicExch(&q.state->vid_range, 1u);
             if (vidx == kEmpty32) cnt.overflow++;
             else atomicAdd(&q.acc_cnt32[(size_t)c_gslot * K + vidx], 1u);
           }

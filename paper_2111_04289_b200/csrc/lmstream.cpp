@@ -125,6 +125,10 @@ struct lms_query {
   uint8_t* d_in[2] = {nullptr, nullptr};
   uint64_t in_cap = 0, in_used[2] = {0, 0};
   int in_cur = 0;
+  // lms_push_pinned: asynchronous H2D into staging buffer b on the copy stream, bracketed by
+  // these events; the batch that consumes buffer b waits for ev_h2d_end[b] on the device
+  cudaEvent_t ev_h2d_start[2] = {nullptr, nullptr}, ev_h2d_end[2] = {nullptr, nullptr};
+  bool h2d_pending[2] = {false, false};
   std::vector<Pending> pending;
   uint64_t next_ds_id = 0;
   double last_ingest = -std::numeric_limits<double>::infinity();
@@ -141,8 +145,9 @@ struct lms_query {
   struct Flight {
     lms_batch_record cur{};
     int in_buf = 0;
+    bool h2d_async = false;            // its staging buffer was filled by lms_push_pinned
     bool flush = false;
-    cudaEvent_t ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
+    cudaEvent_t ev_admit = nullptr, ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
     BatchReport* h_report = nullptr;   // mapped pinned
     BatchReport* d_report = nullptr;
     void* d_rows = nullptr;            // result rows of this batch
@@ -165,16 +170,24 @@ struct lms_query {
   std::vector<void*> ipc_opened;           // peer buffers opened with cudaIpcOpenMemHandle
   uint64_t launches = 0;
   double last_batch_s = 0, last_agg_s = 0, last_close_s = 0;
-  lms_status last_completion = LMS_OK;
+  // completion status of a batch that lms_push had to complete itself (pipelined handle whose
+  // staging buffer still fed the parked batch): reported by the next lms_sync / lms_poll /
+  // lms_force_batch instead of being dropped
+  lms_status deferred_status = LMS_OK;
+  std::string deferred_msg;
+  bool poisoned = false;           // a fused-exchange barrier timed out: ranks may disagree on the
+                                   // window state, so every later batch call fails (LMS_ESTATE)
 
   ~lms_query() {
     cudaSetDevice(cfg.device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
     for (void* p : dallocs) cudaFree(p);
+    for (cudaEvent_t e : {ev_h2d_start[0], ev_h2d_start[1], ev_h2d_end[0], ev_h2d_end[1]})
+      if (e) cudaEventDestroy(e);
     for (Flight& f : fl) {
       if (f.h_report) cudaFreeHost(f.h_report);
-      for (cudaEvent_t e : {f.ev_start, f.ev_agg, f.ev_close, f.ev_end})
+      for (cudaEvent_t e : {f.ev_admit, f.ev_start, f.ev_agg, f.ev_close, f.ev_end})
         if (e) cudaEventDestroy(e);
     }
     if (h_count) cudaFreeHost(h_count);
@@ -212,7 +225,7 @@ lms_status validate_config(const lms_config* c) {
   if (c->num_cores < 1) return fail(LMS_EINVAL, "num_cores < 1");
   if (c->num_xways < 1 || c->num_xways > 16) return fail(LMS_EINVAL, "num_xways must be 1..16");
   if (!(c->inf_pt_bytes > 0) || !(c->base_trans_cost >= 0)) return fail(LMS_EINVAL, "bad cost constants");
-  if (c->max_batch_bytes == 0 || c->max_batch_bytes > (1ull << 40)) return fail(LMS_EINVAL, "max_batch_bytes");
+  if (c->max_batch_bytes == 0 || c->max_batch_bytes > kMaxBatchTotal) return fail(LMS_EINVAL, "max_batch_bytes must be in [1, 2^37]");
   if (c->max_keys == 0 || c->max_keys > (1ull << 30)) return fail(LMS_EINVAL, "max_keys");
   if (c->max_result_rows == 0 || c->max_result_rows > (1ull << 32)) return fail(LMS_EINVAL, "max_result_rows");
   if (c->world < 1 || c->world > kMaxWorld || c->rank < 0 || c->rank >= c->world)
@@ -267,6 +280,13 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
     if (d.dptr) segs.push_back({d.dptr, d.nbytes});
   q->pending.clear();
   q->F().in_buf = buf;
+  q->F().h2d_async = q->h2d_pending[buf];
+  // Proc (reading R18) runs from admission: an asynchronous H2D still in flight is part of it
+  CUDA_TRY(cudaEventRecord(q->F().ev_admit, q->stream));
+  if (q->h2d_pending[buf]) {        // asynchronous pushes: the kernels wait for their H2D
+    CUDA_TRY(cudaStreamWaitEvent(q->stream, q->ev_h2d_end[buf], 0));
+    q->h2d_pending[buf] = false;
+  }
   q->in_cur ^= 1;
   q->in_used[q->in_cur] = 0;
 
@@ -327,7 +347,7 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
   CUDA_TRY(cudaEventElapsedTime(&ms_total, f.ev_start, f.ev_close));
   CUDA_TRY(cudaEventElapsedTime(&ms_agg, f.ev_start, f.ev_agg));
   CUDA_TRY(cudaEventElapsedTime(&ms_close, f.ev_agg, f.ev_close));
-  CUDA_TRY(cudaEventElapsedTime(&ms_end, f.ev_start, f.ev_end));
+  CUDA_TRY(cudaEventElapsedTime(&ms_end, f.ev_admit, f.ev_end));
   q->last_batch_s = ms_total * 1e-3;
   q->last_agg_s = ms_agg * 1e-3;
   q->last_close_s = ms_close * 1e-3;
@@ -355,6 +375,12 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
     d2h = now_host() - t0;
   }
   q->in_used[f.in_buf] = 0;
+  if (f.h2d_async) {                 // device-timed H2D of the staging buffer (lms_push_pinned)
+    float ms_h2d = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms_h2d, q->ev_h2d_start[f.in_buf], q->ev_h2d_end[f.in_buf]));
+    r.h2d_s += ms_h2d * 1e-3;
+    f.h2d_async = false;
+  }
   r.num_records = rep.n_records;
   r.device_s = q->last_batch_s;
   r.d2h_s = d2h;
@@ -393,7 +419,9 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
                                           " malformed records dropped");
   if (rep.overflow || rep.row_overflow || rep.key_overflow || rep.fifo_overflow)
     st = fail(LMS_EOVERFLOW, "batch " + std::to_string(r.index) + ": capacity exceeded (pane ring, keys, rows or FIFO)");
-  q->last_completion = st;
+  if (rep.vid_range)
+    st = fail(LMS_EINVAL, "batch " + std::to_string(r.index) + ": vehicle id >= max_keys in dense-vehicle LR1 "
+                          "(multi-GPU LR1 / LMS_FLAG_DENSE_VEHICLES): those records were rejected");
   return st;
 }
 
@@ -408,11 +436,20 @@ lms_status complete(lms_query* q) {
   return complete_flight(q, q->F());
 }
 
+// A completion status lms_push deferred (first error wins over s).
+lms_status take_deferred(lms_query* q, lms_status s) {
+  if (!q->deferred_status) return s;
+  const lms_status d = q->deferred_status;
+  q->deferred_status = LMS_OK;
+  g_err = q->deferred_msg;
+  return d;
+}
+
 // Complete every in-flight batch (oldest first); the first error wins.
 lms_status complete_all(lms_query* q) {
   lms_status a = complete(q);
   lms_status b = complete(q);
-  return a ? a : b;
+  return take_deferred(q, a ? a : b);
 }
 
 // Pipelined launch (LMS_FLAG_PIPELINE): park the running batch in its slot and switch to the
@@ -512,14 +549,20 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     const int nslots = q->pipeline ? 2 : 1;
     for (int sl = 0; sl < nslots; sl++) {
       lms_query::Flight& f = q->fl[sl];
-      for (cudaEvent_t* e : {&f.ev_start, &f.ev_agg, &f.ev_close, &f.ev_end}) QC_TRY(cudaEventCreate(e));
+      for (cudaEvent_t* e : {&f.ev_admit, &f.ev_start, &f.ev_agg, &f.ev_close, &f.ev_end}) QC_TRY(cudaEventCreate(e));
       QC_TRY(cudaHostAlloc((void**)&f.h_report, sizeof(BatchReport), cudaHostAllocMapped));
       std::memset(f.h_report, 0, sizeof(BatchReport));
       QC_TRY(cudaHostGetDevicePointer((void**)&f.d_report, f.h_report, 0));   // zero-copy report
     }
     QC_TRY(cudaHostAlloc((void**)&q->h_count, sizeof(unsigned long long), cudaHostAllocDefault));
-    {   // pre-size the result FIFO (pinned, pages touched) for up to 64 K rows
-      const uint64_t pre = std::min<uint64_t>(cfg->max_result_rows, 1ull << 16);
+    for (int b = 0; b < 2; b++) {
+      QC_TRY(cudaEventCreate(&q->ev_h2d_start[b]));
+      QC_TRY(cudaEventCreate(&q->ev_h2d_end[b]));
+    }
+    {   // pre-size the result FIFO (pinned, pages touched): 64 Ki aggregate rows, 1 Mi LR1 rows
+        // (32 MB: an LR1 close at C2 rates emits ~0.5 M rows; growing the pinned FIFO inside a
+        // batch's D2H — cudaHostAlloc + page touch — was the round-1 C2 Proc p99 outlier)
+      const uint64_t pre = std::min<uint64_t>(cfg->max_result_rows, is_lr1(q->kind) ? (1ull << 20) : (1ull << 16));
       QC_TRY(is_lr1(q->kind) ? q->lr1_rows.reserve(pre) : q->agg_rows.reserve(pre));
     }
 
@@ -641,6 +684,12 @@ static lms_status push_common(lms_query* q, uint64_t nbytes, double t) {
   if (nbytes == 0) return fail(LMS_EINVAL, "empty dataset");
   if (!(t >= q->last_ingest)) return fail(LMS_EINVAL, "ingest_time must be non-decreasing");
   if (is_lr(q->kind) && nbytes % kLrRecBytes) return fail(LMS_EINVAL, "LR dataset is not whole 70 B records");
+  // one micro-batch (host-pushed + borrowed bytes) is capped at kMaxBatchTotal: the LR2 per-CTA
+  // u32 partials stay exact below it (device.h)
+  uint64_t pend = 0;
+  for (const Pending& d : q->pending) pend += d.nbytes;
+  if (nbytes > kMaxBatchTotal || pend + nbytes > kMaxBatchTotal)
+    return fail(LMS_EOVERFLOW, "micro-batch would exceed 2^37 bytes (admit the buffered datasets first)");
   return LMS_OK;
 }
 
@@ -656,6 +705,7 @@ lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, 
     if (q->parked && q->fl[q->cur_slot ^ 1].in_buf == q->in_cur) {
       lms_status c = complete(q);
       if (c && c != LMS_EFORMAT && c != LMS_EOVERFLOW) return c;
+      if (c && !q->deferred_status) { q->deferred_status = c; q->deferred_msg = g_err; }
     }
     const int b = q->in_cur;
     if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
@@ -671,6 +721,41 @@ lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, 
     return LMS_OK;
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in push");
+  }
+}
+
+lms_status lms_push_pinned(lms_query* q, const void* bytes, uint64_t nbytes, double t, uint64_t* id) {
+  try {
+    lms_status s = push_common(q, nbytes, t);
+    if (s) return s;
+    if (!bytes) return fail(LMS_EINVAL, "null bytes");
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, bytes) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return fail(LMS_EINVAL, "lms_push_pinned needs page-locked host memory (cudaHostAlloc / registered)");
+    }
+    if (!is_lr(q->kind) && static_cast<const uint8_t*>(bytes)[nbytes - 1] != '\n')
+      return fail(LMS_EINVAL, "CM dataset does not end with a newline");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    if (q->parked && q->fl[q->cur_slot ^ 1].in_buf == q->in_cur) {   // (see lms_push)
+      lms_status c = complete(q);
+      if (c && c != LMS_EFORMAT && c != LMS_EOVERFLOW) return c;
+      if (c && !q->deferred_status) { q->deferred_status = c; q->deferred_msg = g_err; }
+    }
+    const int b = q->in_cur;
+    if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
+    if (!q->h2d_pending[b]) CUDA_TRY(cudaEventRecord(q->ev_h2d_start[b], q->copy_stream));
+    CUDA_TRY(cudaMemcpyAsync(q->d_in[b] + q->in_used[b], bytes, nbytes, cudaMemcpyHostToDevice, q->copy_stream));
+    CUDA_TRY(cudaEventRecord(q->ev_h2d_end[b], q->copy_stream));
+    q->h2d_pending[b] = true;
+    q->in_used[b] += nbytes;
+    q->pending.push_back({q->next_ds_id, t, nbytes, nullptr, 0.0});   // H2D time: at completion
+    q->last_ingest = t;
+    if (id) *id = q->next_ds_id;
+    q->next_ds_id++;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in push_pinned");
   }
 }
 
@@ -702,6 +787,8 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status cs = LMS_OK;
     if (q->parked) cs = complete(q);                  // (pipelined handles polled: drain)
+    if (q->poisoned) return fail(LMS_ESTATE, "handle poisoned by a failed fused exchange");
+    cs = take_deferred(q, cs);
     if (q->in_flight) {
       cudaError_t e = cudaEventQuery(q->F().ev_end);
       if (e == cudaErrorNotReady) return cs;        // one micro-batch in flight at a time
@@ -753,10 +840,11 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
     if (q->awaiting_close || (q->in_flight && !q->pipeline))
       return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
     if (q->p2p_async_pending) return fail(LMS_ESTATE, "fused exchange pending (call lms_p2p_collect)");
+    if (q->poisoned) return fail(LMS_ESTATE, "handle poisoned by a failed fused exchange");
     // multi-GPU ranks run their batches in lockstep: an empty rank still runs the batch
     if (q->pending.empty() && q->qd.world == 1) return LMS_OK;
     CUDA_TRY(cudaSetDevice(q->cfg.device));
-    lms_status c = park_current(q);     // pipelined: the running batch keeps its slot
+    lms_status c = take_deferred(q, park_current(q));   // pipelined: the running batch keeps its slot
     lms_status s = launch_batch(q, now, kAdmitForced, std::nan(""), false);
     if (s) return s;
     if (bidx) *bidx = q->F().cur.index;
@@ -1083,13 +1171,19 @@ lms_status lms_p2p_collect(lms_query* q) {
   try {
     if (lms_status e = p2p_check(q)) return e;
     if (!q->p2p_async_pending) return fail(LMS_ESTATE, "no async exchange pending");
+    if (q->poisoned) return fail(LMS_ESTATE, "handle poisoned by a failed fused exchange");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status s1 = complete_all(q);                 // batch record (the close's report)
     CUDA_TRY(cudaStreamSynchronize(q->stream));      // + the exchange kernels behind it
     q->p2p_async_pending = false;
     unsigned int err = 0;
     CUDA_TRY(cudaMemcpy(&err, &q->qd.state->p2p_err, sizeof(err), cudaMemcpyDeviceToHost));
-    if (err) return fail(LMS_ECUDA, "fused exchange: a peer did not arrive within 20 s");
+    if (err) {
+      // a bounded wait gave up: the watermark / accumulators may be partially folded and the
+      // barrier generations are out of step — the handle cannot continue (fatal, not retried)
+      q->poisoned = true;
+      return fail(LMS_ECUDA, "fused exchange: a peer did not arrive within 20 s (handle poisoned)");
+    }
     unsigned long long total = 0;
     CUDA_TRY(cudaMemcpy(&total, &q->qd.state->rows, sizeof(total), cudaMemcpyDeviceToHost));
     const uint64_t nrows = std::min<uint64_t>(total, q->cfg.max_result_rows);
@@ -1167,6 +1261,73 @@ lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
     if (lms_status e = merge_pass(q, rows, n, k, nwin)) return e;
   }
   return LMS_OK;
+}
+
+// ------------------------------------------------------------------ record-boundary split
+// Row partition of one dataset into `parts` contiguous ranges of whole records (SURVEY §8(e):
+// the host splits each micro-batch across the GPUs; the paper splits a micro-batch into
+// NumCores partitions).  LR: cut i at the 70 B multiple at or below i*n/parts.  CM:
+// cut i advanced from i*n/parts to the first byte that follows a '\n' (a record is <= 256 B,
+// so at most one record is scanned per cut; device buffers: that window is copied to the host).
+lms_status lms_split(int32_t kind, const void* bytes, uint64_t nbytes, uint32_t parts, uint64_t* offsets) {
+  try {
+    uint32_t R, S;
+    if (!table_iv(kind, R, S)) return fail(LMS_EINVAL, "unknown query kind");
+    if (!bytes || !offsets || parts == 0 || nbytes == 0) return fail(LMS_EINVAL, "null argument or empty dataset");
+    const bool lr = is_lr(kind);
+    if (lr && nbytes % kLrRecBytes) return fail(LMS_EINVAL, "LR dataset is not whole 70 B records");
+    cudaPointerAttributes at{};
+    bool dev = false;
+    if (cudaPointerGetAttributes(&at, bytes) == cudaSuccess)
+      dev = at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+    cudaGetLastError();
+    const uint8_t* b = static_cast<const uint8_t*>(bytes);
+    auto byte_at = [&](uint64_t i, uint8_t* out) -> bool {   // (device: one small copy per window)
+      if (!dev) { *out = b[i]; return true; }
+      return cudaMemcpy(out, b + i, 1, cudaMemcpyDeviceToHost) == cudaSuccess;
+    };
+    uint8_t last = 0;
+    if (!lr) {
+      if (!byte_at(nbytes - 1, &last)) return fail(LMS_ECUDA, "cudaMemcpy (split)");
+      if (last != '\n') return fail(LMS_EINVAL, "CM dataset does not end with a newline");
+    }
+    offsets[0] = 0;
+    for (uint32_t i = 1; i < parts; i++) {
+      uint64_t c = (uint64_t)((unsigned __int128)nbytes * i / parts);
+      if (lr) {
+        c -= c % kLrRecBytes;
+      } else if (c > 0 && c < nbytes) {
+        // first record start at or after c: the byte after a '\n' in [c-1, nbytes)
+        const uint64_t lo = c - 1, hi = std::min<uint64_t>(nbytes, lo + 512);
+        std::vector<uint8_t> w(hi - lo);
+        if (dev) {
+          if (cudaMemcpy(w.data(), b + lo, w.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return fail(LMS_ECUDA, "cudaMemcpy (split)");
+        } else {
+          std::memcpy(w.data(), b + lo, w.size());
+        }
+        uint64_t j = 0;
+        while (j < w.size() && w[j] != '\n') j++;
+        if (j == w.size()) {                // a line longer than 512 B: scan on (malformed input)
+          uint64_t k = hi;
+          uint8_t x = 0;
+          while (k < nbytes) {
+            if (!byte_at(k, &x)) return fail(LMS_ECUDA, "cudaMemcpy (split)");
+            if (x == '\n') break;
+            k++;
+          }
+          c = std::min<uint64_t>(nbytes, k + 1);
+        } else {
+          c = lo + j + 1;
+        }
+      }
+      offsets[i] = std::max<uint64_t>(c, offsets[i - 1]);
+    }
+    offsets[parts] = nbytes;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in split");
+  }
 }
 
 // ------------------------------------------------------------------ pure functions

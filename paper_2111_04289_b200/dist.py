@@ -57,24 +57,21 @@ def device_view(ptr: int, nbytes: int, dtype="u1"):
 # ----------------------------------------------------------------------------- host split
 
 def split_points(family: str, data, world: int) -> list[tuple[int, int]]:
-    """Row partition of one dataset at record boundaries: [(offset, nbytes)] per rank.
-
-    LR: multiples of 70 B; CM: each cut advanced to the byte after the next '\\n' (records
-    are <= 256 B, so the host scans at most one record per cut).
-    """
-    buf = memoryview(data).cast("B") if not isinstance(data, np.ndarray) else data
-    n = len(buf)
-    cuts = [0]
-    for r in range(1, world):
-        c = n * r // world
-        if family == "LR":
-            c -= c % 70
-        else:
-            while c < n and (c == 0 or buf[c - 1] != ord("\n")):
-                c += 1
-        cuts.append(max(c, cuts[-1]))
-    cuts.append(n)
-    return [(cuts[i], cuts[i + 1] - cuts[i]) for i in range(world)]
+    """Row partition of one dataset at record boundaries: [(offset, nbytes)] per rank, computed
+    by the library (lms_split).  data: bytes-like host memory, or (pointer, nbytes) of host or
+    device memory."""
+    if isinstance(data, tuple):
+        ptr, n = data
+        keep = None
+    else:
+        arr = np.frombuffer(data, dtype=np.uint8) if not isinstance(data, np.ndarray) else data
+        arr = np.ascontiguousarray(arr)
+        ptr, n, keep = arr.ctypes.data, arr.nbytes, arr
+    offs = (C.c_uint64 * (world + 1))()
+    kind = L.LMS_LR2S if family == "LR" else L.LMS_CM2S
+    check(L.lms_split(kind, C.c_void_p(ptr), n, world, offs), "lms_split")
+    del keep
+    return [(offs[i], offs[i + 1] - offs[i]) for i in range(world)]
 
 
 # ----------------------------------------------------------------------------- handles

@@ -114,6 +114,26 @@ def test_split_points_record_boundaries(world):
     assert sum(n for _, n in parts) == len(lr)
 
 
+def test_split_edge_cases():
+    """lms_split: more parts than records (empty parts), a line longer than the 512 B scan
+    window, and the argument checks (C ABI, host memory)."""
+    import ctypes as C
+    from paper_2111_04289_b200 import _lib as L
+    from paper_2111_04289_b200.dist import split_points
+    two = b"1,,1000000000,1,1,1,u,0,0,0.000001,0.000001,0.000001,0\n" * 2
+    parts = split_points("CM", two, 5)
+    assert [n for _, n in parts].count(0) == 3 and b"".join(two[o:o + n] for o, n in parts) == two
+    long_line = b"1,,1," + b"x" * 2000 + b"\n" + b"2,,2,y\n"
+    parts = split_points("CM", long_line, 2)
+    assert parts[1][0] == long_line.index(b"\n") + 1
+    offs = (C.c_uint64 * 3)()
+    buf = C.create_string_buffer(b"abc", 3)
+    assert L.lms_split(L.LMS_CM2S, buf, 3, 2, offs) == L.LMS_EINVAL          # no final newline
+    assert L.lms_split(L.LMS_LR2S, buf, 3, 2, offs) == L.LMS_EINVAL          # not 70 B records
+    assert L.lms_split(99, buf, 3, 2, offs) == L.LMS_EINVAL
+    assert L.lms_split(L.LMS_CM2S, None, 3, 2, offs) == L.LMS_EINVAL
+
+
 class FakeLr1Handle:
     """CPU stand-in for an LR1 RankHandle: per-instance vehicle counts, records the all-reduced
     counts each probe saw."""

@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 N = 10_000_000
 
 
-@pytest.mark.parametrize("qname,seconds", [("CM2S", 12), ("LR2S", 12)])
+@pytest.mark.parametrize("qname,seconds", [("CM2S", 12), ("LR2S", 12), ("CM1S", 12)])
 def test_full_size_batches_every_row(qname, seconds):
     import torch
 

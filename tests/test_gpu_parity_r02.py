@@ -1,0 +1,152 @@
+"""GPU parity, round 2: the paths round 1 left unchecked (VERDICT r01 "What's weak" 2).
+
+- LR1S at BASELINE config C2 scale: U(100) traffic (~10^5 records/s), V = 10^6 vehicles (the
+  key dictionary near its 2^20 capacity), 5-second micro-batches (~0.5M records, what Alg. 1
+  forms at C2), >= 3 closing instances; every row of every batch against the column-form LR1
+  oracle (oracle/bulk.py BulkLr1Replay, pinned to the brute-force self-join on small streams by
+  tests/test_oracle_bulk.py).  Dictionary and dense-vehicle modes.
+- LR1 with R/S > 8 panes per window (the closing probe's looped tail) and a flush whose
+  closing instances span > 1024 panes (the probe's uncached pane lookups), against the
+  brute-force oracle (oracle/queries.py).
+- Dense-vehicle LR1 with VIDs >= max_keys: rejected (LMS_EINVAL), not silently dropped.
+- lms_push_pinned (asynchronous H2D from page-locked memory) equals lms_push.
+Paper anchor: Table IV LR1; reading R8.
+"""
+import numpy as np
+import pytest
+
+import lmsgen as g
+from lmsgen import vec
+from oracle import bulk as B
+from oracle import queries as Q
+from tests.helpers import compare_run, oracle_rows, product_run
+
+pytestmark = pytest.mark.gpu
+
+SEED = 211104289
+
+
+def _prod_lr1_sorted(rows):
+    out = np.zeros(len(rows), B.LR1_DTYPE)
+    out["win_start"], out["ts"], out["vehicle"] = rows["win_start_s"], rows["ts"], rows["vehicle"]
+    out["speed"], out["xway"], out["lane"] = rows["speed"], rows["xway"], rows["lane"]
+    out["dir"], out["seg"], out["m"] = rows["dir"], rows["segment"], rows["multiplicity"]
+    return np.sort(out)
+
+
+def _check_lr1(rows, want):
+    got = _prod_lr1_sorted(rows)
+    want = np.sort(want)
+    assert len(got) == len(want), (len(got), len(want))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("flags", [0, 4])      # key dictionary; LMS_FLAG_DENSE_VEHICLES
+def test_lr1s_c2_scale_every_row(flags):
+    import torch
+
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    from lmsgen import cuda as gcu
+    tr = g.Traffic.parse("U(100)")
+    secs, bsz = 45, 5
+    q = Q.query_spec("LR1S")
+    rp = B.BulkLr1Replay(q)
+    closing = 0
+    n_total = 0
+    with P.Query("LR1S", mode="manual", flags=flags) as dq:
+        for b0 in range(0, secs, bsz):
+            keep, seconds = [], []
+            for t in range(b0, b0 + bsz):
+                n = tr.count(t, SEED)
+                buf, nb = gcu.second_tensor("LR", t, n, seed=SEED)
+                keep.append(buf)
+                dq.push_device(buf.data_ptr(), nb, float(t))
+                seconds.append((t, vec.lr_columns(SEED, t, n)))
+                n_total += n
+            dq.force(float(b0 + bsz))
+            assert dq.sync() == L.LMS_OK
+            rec = dq.record(dq.num_batches() - 1)
+            assert rec["bad_records"] == 0 and rec["overflow_records"] == 0
+            want = rp.batch(seconds)
+            closing += rec["windows_closed"]
+            _check_lr1(dq.read_lr1(), want)
+            del keep
+            torch.cuda.empty_cache()
+        dq.flush(float(secs + 1))
+        _check_lr1(dq.read_lr1(), rp.flush())
+        assert dq.record(dq.num_batches() - 1)["rows_emitted"] > 0
+    assert closing >= 3
+    assert n_total > 3_500_000
+
+
+def test_lr1_more_than_8_panes_per_window():
+    data = [d for _, d in g.stream_datasets("LR", "B(0.3)", 48, seed=17, params=g.LRParams(num_vehicles=60))]
+    batches = [data[i:i + 4] for i in range(0, len(data), 4)]
+    for qname, R, S in (("LR1S", 20, 2), ("LR1S", 12, 1)):          # R/S = 10, 12
+        compare_run(qname, product_run(qname, batches, range_s=R, slide_s=S),
+                    oracle_rows(qname, batches, range_s=R, slide_s=S))
+
+
+def test_lr1_flush_spanning_more_than_1024_panes():
+    """One batch holding seconds 0-9 and 1200-1209 (R = 2, S = 1): its close emits ~1210
+    instances, so the probe resolves panes outside its 1024-pane cache."""
+    p = g.LRParams(num_vehicles=25)
+    a = [d for _, d in g.stream_datasets("LR", "B(0.03)", 10, seed=5, params=p)]
+    b = [d for _, d in g.stream_datasets("LR", "B(0.03)", 10, seed=5, params=p, t0=1200)]
+    batches = [a + b]
+    for qname in ("LR1S",):
+        compare_run(qname, product_run(qname, batches, range_s=2, slide_s=1),
+                    oracle_rows(qname, batches, range_s=2, slide_s=1))
+    batches = [a, b]                                                  # the gap between batches
+    compare_run("LR1S", product_run("LR1S", batches, range_s=2, slide_s=1),
+                oracle_rows("LR1S", batches, range_s=2, slide_s=1))
+
+
+def test_dense_vehicle_id_out_of_range_is_rejected():
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    p = g.LRParams(num_vehicles=4000)
+    data = [d for _, d in g.stream_datasets("LR", "B(0.5)", 3, seed=9, params=p)]
+    big = sum(1 for d in data for i in range(0, len(d), 70) if int(d[i + 9:i + 19]) >= 1024)
+    assert big > 0
+    with P.Query("LR1S", mode="manual", flags=L.LMS_FLAG_DENSE_VEHICLES, max_keys=1024) as q:
+        for t, d in enumerate(data):
+            q.push(d, float(t))
+        q.force(3.0)
+        assert q.sync(ok=(L.LMS_EINVAL,)) == L.LMS_EINVAL
+        assert b"vehicle id" in L.lms_last_error()
+        assert q.record(0)["overflow_records"] == big
+
+
+def test_push_pinned_equals_push():
+    import torch
+
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    data = [d for _, d in g.stream_datasets("CM", "B(1.2)", 24, seed=3)]
+    batches = [data[i:i + 6] for i in range(0, len(data), 6)]
+    want = product_run("CM2S", batches)
+    got, keep = [], []
+    with P.Query("CM2S", mode="manual") as q:
+        t = 0.0
+        for b in batches:
+            for d in b:
+                h = torch.empty(len(d), dtype=torch.uint8, pin_memory=True)
+                h.copy_(torch.frombuffer(bytearray(d), dtype=torch.uint8))
+                keep.append(h)
+                q.push_pinned(h.data_ptr(), len(d), t)
+                t += 1.0
+            q.force(t)
+            st = q.sync()
+            rec = q.record(q.num_batches() - 1)
+            assert rec["h2d_s"] > 0
+            got.append((q.read_agg(), rec, st))
+        q.flush(t)
+        got.append((q.read_agg(), q.record(q.num_batches() - 1), L.LMS_OK))
+        with pytest.raises(P.LmsError):                       # pageable memory is refused
+            arr = np.frombuffer(data[0], dtype=np.uint8).copy()
+            q.push_pinned(arr.ctypes.data, arr.nbytes, t + 1)
+    compare_run("CM2S", got, oracle_rows("CM2S", batches))
+    for (gr, _, _), (wr, _, _) in zip(got, want):
+        assert sorted(map(bytes, gr)) == sorted(map(bytes, wr))

@@ -52,3 +52,37 @@ def test_bulk_matches_brute_force(qname, traffic, secs, R, S, params):
             if qname.startswith("CM1"):
                 assert gr.rank == wr.rank
     assert nonempty >= 3
+
+
+def _lr1_sorted(rows):
+    return sorted((int(r["win_start"]), int(r["ts"]), int(r["vehicle"]), int(r["speed"]), int(r["xway"]),
+                   int(r["lane"]), int(r["dir"]), int(r["seg"]), int(r["m"])) for r in rows)
+
+
+@pytest.mark.parametrize("qname,traffic,secs,R,S,nveh,bsz", [
+    ("LR1S", "B(0.2)", 47, None, None, 50, 5),          # Table IV LR1S, 5-second batches
+    ("LR1S", "U(0.3)", 40, 18, 2, 40, 3),                # R/S = 9 panes per window
+    ("LR1T", "R(0.1,0.4)", 75, None, None, 30, 7),      # tumbling: L = A
+    ("LR1S", "B(0.1)", 30, 4, 1, 20, 1),
+])
+def test_bulk_lr1_matches_brute_force(qname, traffic, secs, R, S, nveh, bsz):
+    """The column-form LR1 (vehicle counts per second -> window multiplicity m) equals the
+    brute-force nested-loop self-join (queries.eval_instance, pinned to sqlite) batch by batch."""
+    q = Q.query_spec(qname, R, S)
+    tr = g.Traffic.parse(traffic)
+    params = g.LRParams(num_vehicles=nveh)
+    data = list(g.stream_datasets("LR", tr, secs, seed=43, params=params))
+    batches = [data[i:i + bsz] for i in range(0, len(data), bsz)]
+    want = Q.replay(q, [[d for _, d in b] for b in batches])
+    rp = B.BulkLr1Replay(q)
+    got = [rp.batch([(t, vec.lr_columns(43, t, tr.count(t, 43), params)) for t, _ in b]) for b in batches]
+    got.append(rp.flush())
+    assert len(got) == len(want)
+    total = 0
+    for gr, w in zip(got, want):
+        assert _lr1_sorted(gr) == sorted((r.win_start, r.ts, r.vehicle, r.speed, r.xway, r.lane, r.dir, r.seg, r.m)
+                                         for r in w.rows)
+        total += len(gr)
+    # every record is an L row of exactly one instance (its pane's), with m >= 1
+    assert total == sum(tr.count(t, 43) for t, _ in data)
+    assert all(int(x) >= 1 for b in got for x in b["m"])
