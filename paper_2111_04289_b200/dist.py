@@ -19,10 +19,10 @@ LR1 (self-join, no owner exchange): after step 2, for every instance the batch c
 ranks' vehicle-indexed window counts are all-reduced (SUM, 4 B per vehicle) and each rank
 probes its own newest-slide rows against the global counts (lms_lr1_* calls).
 
-`Exchange` implementations: TorchDistExchange (one handle per process, any torch.distributed
-backend: NCCL on GPUs, gloo for the CPU protocol tests) and LocalExchange (several handles on
-one GPU in one process — "virtual shards", used to test the kernels of the protocol on a
-single GPU).  run_batch(p2p=True) uses the fused exchange instead: each rank
+`Exchange` implementation: TorchDistExchange (one handle per process, any torch.distributed
+backend: NCCL on GPUs, gloo for the CPU protocol tests).  The tests' LocalExchange
+(tests/local_exchange.py: several handles on one GPU in one process, "virtual shards") drives
+the same protocol without a process group.  run_batch(p2p=True) uses the fused exchange instead: each rank
 adds its partials straight into the owners' accumulators through peer-mapped memory (CUDA IPC
 over NVLink; lms_p2p_*), then barrier + owner finalize — no all-to-all, no merge copy.
 """
@@ -213,15 +213,13 @@ class TorchDistExchange:
         return torch.cuda.stream(torch.cuda.ExternalStream(h.stream_ptr))
 
     def allreduce_watermarks(self, handles):
-        """One MAX all-reduce of [wm, -ts_min] (global watermark and first-batch ts_min)."""
-        import torch
+        """In place on the library's state: MAX all-reduce of the watermark, MIN of the batch's
+        first ts (reading R7) — collectives only, no compute outside the library."""
         (h,) = handles
         wm, tsmin = h.watermark_tensors()
         with self._on(h):
-            both = torch.cat([wm, -tsmin])
-            self._all_reduce(both, self.dist.ReduceOp.MAX)
-            wm.copy_(both[:1])
-            tsmin.copy_(-both[1:])
+            self._all_reduce(wm, self.dist.ReduceOp.MAX)
+            self._all_reduce(tsmin, self.dist.ReduceOp.MIN)
 
     def setup_p2p(self, handles, device_watermark: bool = False):
         """Fused exchange: every rank maps every rank's owner state (CUDA IPC handles sent with
@@ -256,53 +254,6 @@ class TorchDistExchange:
             recv = torch.empty(sum(rc) * ROW_BYTES, dtype=torch.uint8, device=dev)
             self._a2a(recv, rows, [c * ROW_BYTES for c in rc], [c * ROW_BYTES for c in counts])
         return [recv]
-
-
-class LocalExchange:
-    """All ranks' handles in one process (virtual shards on one GPU)."""
-
-    def setup_p2p(self, handles, device_watermark: bool = False):
-        for h in handles:
-            for o in handles:
-                h.p2p_import_local(o)
-        if device_watermark:
-            for h in handles:
-                h.p2p_device_watermark(True)
-
-    def barrier(self, handles):
-        pass                        # pushes are synchronous: nothing in flight
-
-    def allreduce_watermarks(self, handles):
-        import torch
-        torch.cuda.synchronize()
-        wms, tss = zip(*(h.watermark_tensors() for h in handles))
-        wm = torch.stack(list(wms)).max(0).values
-        ts = torch.stack(list(tss)).min(0).values
-        for a, b in zip(wms, tss):
-            a.copy_(wm)
-            b.copy_(ts)
-        torch.cuda.synchronize()
-
-    def allreduce_sum(self, handles, tensors):
-        import torch
-        torch.cuda.synchronize()
-        tot = torch.stack(list(tensors)).sum(0, dtype=tensors[0].dtype)
-        for t in tensors:
-            t.copy_(tot)
-        torch.cuda.synchronize()
-
-    def all_to_all(self, handles, sends):
-        import torch
-        world = len(handles)
-        out = []
-        for d in range(world):
-            parts = []
-            for rows, counts in sends:
-                off = sum(counts[:d]) * ROW_BYTES
-                parts.append(rows[off:off + counts[d] * ROW_BYTES])
-            out.append(torch.cat(parts) if parts else torch.empty(0, dtype=torch.uint8, device="cuda"))
-        torch.cuda.synchronize()
-        return out
 
 
 class _Null:

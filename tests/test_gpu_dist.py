@@ -13,7 +13,8 @@ pytestmark = pytest.mark.gpu
 
 def sharded_run(qname, batches, world, p2p=False, **cfg):
     import paper_2111_04289_b200 as P
-    from paper_2111_04289_b200.dist import LocalExchange, RankHandle, run_batch, split_points
+    from paper_2111_04289_b200.dist import RankHandle, run_batch, split_points
+    from tests.local_exchange import LocalExchange
     fam = qname[:2]
     hs = [RankHandle(P.Query(qname, mode="manual", rank=r, world=world, **cfg)) for r in range(world)]
     ex = LocalExchange()

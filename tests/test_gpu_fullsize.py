@@ -48,7 +48,7 @@ def test_full_size_batches_every_row(qname, seconds):
         want = rp.flush()
         compare_agg(qname, rows, want)
         emitted += len(want)
-    assert emitted > 1000
+    assert emitted > (20 if qname.startswith("CM1") else 1000)     # CM1: 4 categories per instance
 
 
 def test_full_size_pipelined_as_bench_runs_it():
