@@ -300,8 +300,9 @@ typedef struct {
   uint64_t dict_cap_mask;
   uint32_t dict_max_keys, present;   /* present: bit i = ipc[i] is valid                  */
   uint8_t  ipc[6][64];               /* cudaIpcMemHandle_t of: merge sums, merge counts,
-                                        dictionary {key, index} entries, (unused: ipc[3]
-                                        is never present), keys by index, state            */
+                                        dictionary {key, index} entries, dictionary free-
+                                        index stack, keys by index, state (CM2 only: the
+                                        dictionary slots ipc[2..4])                        */
 } lms_p2p_handle;
 lms_status  lms_p2p_export(lms_query* q, lms_p2p_handle* out);
 lms_status  lms_p2p_import(lms_query* q, const lms_p2p_handle* peer);

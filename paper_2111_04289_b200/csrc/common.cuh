@@ -82,7 +82,21 @@ __device__ __forceinline__ unsigned long long fmix64(unsigned long long k) {
   return k;
 }
 
-// Dictionary lookup-or-insert: key -> dense index < max_keys; kEmpty32 on overflow.
+// Dense index for a newly inserted key: a recycled one (reclaimed when its key's last pane was
+// evicted, reading R7 eviction) if any, else the next fresh one.  Pops run only while no
+// reclaim runs (reclaims happen in the close kernels, pops in the aggregate / merge kernels).
+__device__ __forceinline__ uint32_t alloc_key_index(const Dict& d, DevState* st) {
+  if (*(volatile int*)&st->kfree_top > 0) {
+    const int t = atomicSub(&st->kfree_top, 1) - 1;
+    if (t >= 0) return d.free_idx[t];
+    atomicAdd(&st->kfree_top, 1);          // lost the race for the last one
+  }
+  return atomicAdd_system(&st->n_keys, 1u);
+}
+
+// Dictionary lookup-or-insert: key -> dense index < max_keys; kEmpty32 on overflow.  Entries of
+// reclaimed keys are tombstones (kTomb64): probes pass over them, inserts only take empty
+// entries (so that two threads inserting the same key cannot end in two entries).
 __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long key, DevState* st) {
   unsigned long long h = fmix64(key) & d.cap_mask;
   for (unsigned long long probes = 0; probes <= d.cap_mask; probes++) {   // bounded: a full
@@ -95,7 +109,7 @@ __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long k
       // same dictionary (multi-GPU fused exchange, dict_get_sys): system-scope RMWs
       k = atomicCAS_system(ent, kEmpty64, key);
       if (k == kEmpty64) {     // we own the entry: allocate the index and publish it
-        uint32_t idx = atomicAdd_system(&st->n_keys, 1u);
+        uint32_t idx = alloc_key_index(d, st);
         if (idx >= d.max_keys) {
           atomicExch(&st->key_overflow, 1u);
           idx = kEmpty32 - 1;   // poison: entry exists but is unusable

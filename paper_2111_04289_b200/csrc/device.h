@@ -22,6 +22,8 @@ namespace lms {
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
 constexpr uint32_t kFail32 = 0xFFFFFFFEu;   // pane table full: the pane's records overflow
 constexpr unsigned long long kEmpty64 = ~0ull;
+constexpr unsigned long long kTomb64 = ~0ull - 1;   // dictionary entry of a reclaimed key (no parsed
+                                                    // key reaches it: <= 19 digits < 2^64 - 2)
 constexpr int kMaxSegs = 128;                          // input segments per aggregate launch
 // Bytes of one micro-batch (host-pushed + borrowed segments).  Bounds the LR2 per-CTA u32
 // partials: a CTA of the 296-CTA grid sees <= 2^37 / 70 / 296 < 6.7e6 records of a batch, so a
@@ -53,7 +55,9 @@ struct DevState {
   unsigned long long n_records, bad, late, overflow, rows, windows_closed;
   unsigned int row_overflow;
   unsigned int close_ticket;
-  unsigned int n_keys;          // dictionary entries in use
+  unsigned int n_keys;          // dictionary indices handed out so far (high-water mark)
+  int kfree_top;                // reclaimed dictionary indices on the free stack (Dict.free_idx)
+  unsigned int n_tomb;          // tombstoned dictionary entries (rehash when > capacity / 4)
   unsigned int key_overflow;
   unsigned int vid_range;       // dense-vehicle LR1: a record's VID was >= max_keys (rejected)
   unsigned int fifo_count[2];   // LR1 retained-row FIFO sizes
@@ -108,7 +112,8 @@ struct Dict {
   unsigned long long* keys;     // [cap][2]: entry h = {key (kEmpty64 = free), index in the low 32
                                 // bits of the second word (kEmpty32 until published)} — one
                                 // 16 B load resolves a key (one L2 round trip, not two)
-  uint32_t* vals;               // unused (kept for the ABI's IPC handle slots)
+  uint32_t* free_idx;           // [max_keys] stack of reclaimed indices (a key whose panes were all
+                                // evicted frees its index; inserts take recycled indices first)
   unsigned long long* key_by_idx;  // [max_keys]
   unsigned long long cap_mask;
   uint32_t max_keys;

@@ -52,11 +52,55 @@ __device__ __forceinline__ WinRange win_range(const QueryDev& q, int flush) {
   return w;
 }
 
-// Resolve the accumulator slots of instance k's panes into smem (kEmpty32: pane never seen).
+// Resolve the accumulator slots of instance k's panes into smem (kEmpty32: pane never seen),
+// and at slots[ppw] the pane just past the instance (the only live pane a key can have beyond
+// the last closing instance: see reclaim below).
 __device__ __forceinline__ void window_slots(const QueryDev& q, long long k, uint32_t* slots) {
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < q.ppw; j += blockDim.x) slots[j] = find_slot(q, k + j);
+  for (uint32_t j = threadIdx.x; j <= q.ppw; j += blockDim.x) slots[j] = find_slot(q, k + j);
   __syncthreads();
+}
+
+// Key-state eviction (dictionary kinds, single GPU): a key whose counts are zero in every pane
+// that is still live after this close has no state left — its dictionary entry becomes a
+// tombstone and its dense index goes on the free stack for the next new key, so the key
+// capacity bounds the keys live in the window, not the keys ever seen (a churning jobId
+// stream).  Runs in the close kernels only, never concurrently with dictionary lookups.
+__device__ void reclaim_key(const QueryDev& q, uint32_t idx) {
+  const unsigned long long key = q.dict.key_by_idx[idx];
+  if (key == kEmpty64) return;                              // already free
+  unsigned long long h = fmix64(key) & q.dict.cap_mask;
+  for (unsigned long long n = 0; n <= q.dict.cap_mask; n++) {
+    unsigned long long* ent = q.dict.keys + 2 * h;
+    const unsigned long long k = *ent;
+    if (k == key) { *ent = kTomb64; break; }
+    if (k == kEmpty64) break;
+    h = (h + 1) & q.dict.cap_mask;
+  }
+  q.dict.key_by_idx[idx] = kEmpty64;
+  q.dict.free_idx[atomicAdd(&q.state->kfree_top, 1)] = idx;
+  atomicAdd(&q.state->n_tomb, 1u);
+}
+
+// Whole CTA: rebuild the dictionary's hash table from the live keys (drops the tombstones;
+// every live key keeps its dense index).
+__device__ void dict_rehash_cta(const QueryDev& q) {
+  const unsigned long long cap = q.dict.cap_mask + 1;
+  for (unsigned long long i = threadIdx.x; i < cap; i += blockDim.x) {
+    q.dict.keys[2 * i] = kEmpty64;
+    q.dict.keys[2 * i + 1] = kEmpty64;
+  }
+  __syncthreads();
+  const uint32_t hwm = min(q.state->n_keys, q.dict.max_keys);
+  for (uint32_t idx = threadIdx.x; idx < hwm; idx += blockDim.x) {
+    const unsigned long long key = q.dict.key_by_idx[idx];
+    if (key == kEmpty64) continue;
+    unsigned long long h = fmix64(key) & q.dict.cap_mask;
+    while (atomicCAS(q.dict.keys + 2 * h, kEmpty64, key) != kEmpty64) h = (h + 1) & q.dict.cap_mask;
+    reinterpret_cast<unsigned int*>(q.dict.keys + 2 * h + 1)[0] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) q.state->n_tomb = 0;
 }
 
 __device__ __forceinline__ unsigned long long row_slot(DevState* st, bool want) {
@@ -112,6 +156,13 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
   if (q.kind == kLR2S)
     for (uint32_t i = threadIdx.x; i < 2 * q.n_agg_ctas; i += blockDim.x) q.part_tag[i] = kEmpty64;
   if (w.any && !lr1) evict_rebuild_cta(q, w.k_last);      // LR1: k_lr1_evict frees the slots
+  {   // tombstones above a quarter of the table: rebuild it (LR1: in k_lr1_evict)
+    __shared__ int s_rehash;
+    if (threadIdx.x == 0)
+      s_rehash = q.kind == kCM2S && q.world == 1 && st->n_tomb > (uint32_t)((q.dict.cap_mask + 1) / 4);
+    __syncthreads();
+    if (s_rehash) dict_rehash_cta(q);
+  }
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < kMaxWorld; i += blockDim.x) {   // bucket counters (multi-GPU)
     st->owner_count[i] = 0;
@@ -122,7 +173,8 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
     // (which may alias as far as the compiler knows) each load would wait for the last one
     const unsigned long long wm = st->wm, n_records = st->n_records, bad = st->bad, late = st->late,
                              overflow = st->overflow, rows = st->rows, wclosed = st->windows_closed;
-    const uint32_t n_keys = st->n_keys, row_ovf = st->row_overflow, key_ovf = st->key_overflow,
+    const uint32_t n_keys = st->n_keys - (uint32_t)max(st->kfree_top, 0),   // live keys
+                   row_ovf = st->row_overflow, key_ovf = st->key_overflow,
                    fifo_ovf = st->fifo_overflow, fcur = st->fifo_cur, vid_rng = st->vid_range;
     long long ck_first = 0, ck_last = -1;
     unsigned long long wc = wclosed;
@@ -254,7 +306,8 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   const uint32_t k0 = (uint32_t)((unsigned long long)K * blockIdx.x / gridDim.x);
   const uint32_t k1 = (uint32_t)((unsigned long long)K * (blockIdx.x + 1) / gridDim.x);
   const uint32_t P = q.P;
-  __shared__ uint32_t wslots[256];   // R/S <= 256
+  __shared__ uint32_t wslots[257];   // R/S <= 256, + the pane after the instance
+  const bool reclaim = q.kind == kCM2S && q.world == 1;
 
   // Most batches close no window (slide S > batch span): nothing to merge (CM: the aggregate
   // pass wrote the pane accumulators directly), emit or evict.  The state is still advanced by
@@ -318,7 +371,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
       // LR2 / CM2: one thread per key of my slice
       for (uint32_t kb = k0; kb < k1; kb += blockDim.x) {
         const uint32_t key = kb + threadIdx.x;
-        unsigned long long s = 0, c = 0;
+        unsigned long long s = 0, c = 0, c_first = 0;
         if (key < k1) {
           for (uint32_t j = 0; j < q.ppw; j++) {
             const uint32_t g = wslots[j];
@@ -328,7 +381,18 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
                 s += q.acc_sum[gi];
                 c += q.acc_cnt[gi];
               }
+            if (j == 0) c_first = c;
           }
+        }
+        // the last closing instance decides key eviction: after this close the live panes are
+        // k_last + 1 .. k_last + ppw (the watermark is below (k_last + 1) S + R)
+        bool dead = false;
+        if (reclaim && k == w.k_last && key < k1) {
+          unsigned long long c_live = c - c_first;
+          const uint32_t gx = wslots[q.ppw];
+          if (gx != kEmpty32)
+            for (uint32_t sp = 0; sp < q.stripes; sp++) c_live += q.acc_cnt[((size_t)gx * q.stripes + sp) * q.K + key];
+          dead = c_live == 0;
         }
         bool want = c > 0;
         double sum, avg;
@@ -358,6 +422,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
             atomicExch(&st->row_overflow, 1u);
           }
         }
+        if (dead) reclaim_key(q, key);          // (after its row: the row reads key_by_idx)
       }
     }
   }
@@ -538,14 +603,36 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   // always past the last emitted instance): every CTA sees the same values and returns
   if (upto <= st->evicted_upto && !st->pane_fail) return;
   const uint32_t nk = q.lr1_dense ? q.K : min(st->n_keys, q.K);
+  __shared__ uint32_t s_live[1024];           // slots of the panes that stay live (P <= 1024)
+  __shared__ uint32_t s_nlive;
+  if (threadIdx.x == 0) s_nlive = 0;
+  __syncthreads();
+  for (uint32_t g = threadIdx.x; g < q.P; g += blockDim.x) {
+    const uint32_t p = q.slot_pane[g];
+    if (p != kEmpty32 && (long long)p > upto) s_live[atomicAdd(&s_nlive, 1u)] = g;
+  }
+  __syncthreads();
+  const bool reclaim = !q.lr1_dense && q.world == 1;
   for (uint32_t g = 0; g < q.P; g++) {
     const uint32_t p = q.slot_pane[g];
     if (p == kEmpty32 || (long long)p > upto) continue;
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += gridDim.x * blockDim.x)
       q.acc_cnt32[(size_t)g * q.K + k] = 0;
   }
+  if (reclaim) {   // key-state eviction: vehicles with no count in any live pane (see reclaim_key)
+    const uint32_t nl = s_nlive;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nk; k += gridDim.x * blockDim.x) {
+      uint32_t c = 0;
+      for (uint32_t i = 0; i < nl && c == 0; i++) c += q.acc_cnt32[(size_t)s_live[i] * q.K + k];
+      if (c == 0) reclaim_key(q, k);
+    }
+  }
   if (ticket(st)) {
     evict_rebuild_cta(q, upto);
+    __shared__ int s_rehash;
+    if (threadIdx.x == 0) s_rehash = reclaim && st->n_tomb > (uint32_t)((q.dict.cap_mask + 1) / 4);
+    __syncthreads();
+    if (s_rehash) dict_rehash_cta(q);
     if (threadIdx.x == 0) { st->evicted_upto = upto; st->close_ticket = 0; __threadfence(); }
   }
 }

@@ -627,7 +627,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       d.dict.cap_mask = cap - 1;
       d.dict.max_keys = (uint32_t)cfg->max_keys;
       Q_TRY(q->dalloc(&d.dict.keys, 2 * cap, 0xFF));   // {key, index} entries of 16 B
-      d.dict.vals = nullptr;
+      Q_TRY(q->dalloc(&d.dict.free_idx, cfg->max_keys, 0));   // reclaimed-index stack
       Q_TRY(q->dalloc(&d.dict.key_by_idx, cfg->max_keys, 0));
     }
     d.row_cap = cfg->max_result_rows;
@@ -1035,7 +1035,7 @@ lms_status lms_p2p_export(lms_query* q, lms_p2p_handle* out) {
     out->kind = q->kind;
     out->dict_cap_mask = q->qd.dict.cap_mask;
     out->dict_max_keys = q->qd.dict.max_keys;
-    void* bufs[6] = {q->qd.macc_sum, q->qd.macc_cnt, q->qd.dict.keys, q->qd.dict.vals, q->qd.dict.key_by_idx,
+    void* bufs[6] = {q->qd.macc_sum, q->qd.macc_cnt, q->qd.dict.keys, q->qd.dict.free_idx, q->qd.dict.key_by_idx,
                      q->qd.state};
     for (int i = 0; i < 6; i++) {
       if (!bufs[i]) continue;                     // no dictionary for LR2 / CM1
@@ -1073,7 +1073,7 @@ lms_status lms_p2p_import(lms_query* q, const lms_p2p_handle* peer) {
       v.macc_sum = static_cast<unsigned long long*>(ptr[0]);
       v.macc_cnt = static_cast<unsigned long long*>(ptr[1]);
       v.dict.keys = static_cast<unsigned long long*>(ptr[2]);
-      v.dict.vals = static_cast<uint32_t*>(ptr[3]);
+      v.dict.free_idx = static_cast<uint32_t*>(ptr[3]);
       v.dict.key_by_idx = static_cast<unsigned long long*>(ptr[4]);
       v.dict.cap_mask = peer->dict_cap_mask;
       v.dict.max_keys = peer->dict_max_keys;
