@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LMS_ABI_VERSION 1u
+#define LMS_ABI_VERSION 2u
 
 typedef struct lms_query lms_query;      /* opaque, library-owned */
 
@@ -108,6 +108,18 @@ typedef struct {
                                 lms_run_close / lms_partials / lms_merge.  world > 1
                                 (LR1S, LR1T): vehicle-indexed counts, window counts
                                 all-reduced per closing instance — lms_lr1_window_counts. */
+  int32_t  num_gpus;         /* single-handle multi-device driver: > 1 -> this
+                                one handle row-partitions every micro-batch over num_gpus devices
+                                of this process (rank / world must stay 0 / 1).  Pushes are split
+                                at record boundaries (lms_split), Alg. 1 / CG(dN) / OS(tN) size the
+                                WHOLE micro-batch once (Eq. 4/5/6 on its total bytes and its Proc =
+                                the slowest device's), the partial aggregates are merged by key
+                                owner through peer memory (the fused exchange, device-side
+                                barriers), and rows / batch records come out of this handle as
+                                from a single GPU.  Devices need peer access to each other (the
+                                same ordinal may repeat: virtual shards on one GPU).  Default 1.  */
+  const int32_t* device_ids; /* [num_gpus] CUDA ordinals (NULL -> 0 .. num_gpus-1); copied at
+                                lms_query_create                                                */
 } lms_config;
 
 #define LMS_FLAG_ONLINE_INFPT 0x1u  /* Eq. 10 online regression of InfPT */

@@ -23,12 +23,19 @@ assert AGG_DTYPE.itemsize == C.sizeof(L.lms_agg_row) and LR1_DTYPE.itemsize == C
 
 
 def config(kind: str | int, **overrides) -> L.lms_config:
+    """lms_config_init defaults + overrides (device_ids: a sequence of CUDA ordinals, kept alive
+    on the returned struct as `_device_ids`; it implies num_gpus = len(device_ids))."""
     cfg = L.lms_config()
     k = KIND[kind.upper()] if isinstance(kind, str) else int(kind)
     check(L.lms_config_init(C.byref(cfg), k), "lms_config_init")
     for name, val in overrides.items():
         if name == "mode" and isinstance(val, str):
             val = MODE[val]
+        if name == "device_ids" and val is not None:
+            arr = (C.c_int32 * len(val))(*val)
+            cfg._device_ids = arr
+            cfg.num_gpus = len(val)
+            val = C.cast(arr, C.POINTER(C.c_int32))
         setattr(cfg, name, val)
     return cfg
 

@@ -17,7 +17,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
-LMS_ABI_VERSION = 1
+LMS_ABI_VERSION = 2
 LMS_OK, LMS_EINVAL, LMS_ENOMEM, LMS_ECUDA, LMS_ENCCL, LMS_EHISTORY, LMS_EPLAN, LMS_EFORMAT, \
     LMS_ESTATE, LMS_EOVERFLOW, LMS_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9, -10
 STATUS_NAMES = {0: "LMS_OK", -1: "LMS_EINVAL", -2: "LMS_ENOMEM", -3: "LMS_ECUDA", -4: "LMS_ENCCL",
@@ -44,7 +44,8 @@ class lms_config(C.Structure):
                 ("range_s", C.c_double), ("slide_s", C.c_double), ("num_cores", C.c_int32),
                 ("num_xways", C.c_int32), ("inf_pt_bytes", C.c_double), ("base_trans_cost", C.c_double),
                 ("max_batch_bytes", C.c_uint64), ("max_keys", C.c_uint64), ("max_result_rows", C.c_uint64),
-                ("pane_slots", C.c_uint32), ("flags", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32)]
+                ("pane_slots", C.c_uint32), ("flags", C.c_uint32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("num_gpus", C.c_int32), ("device_ids", C.POINTER(C.c_int32))]
 
 
 class lms_agg_row(C.Structure):

@@ -180,6 +180,7 @@ cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st);
 cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_lr1_wsum(const QueryDev& q, long long k, cudaStream_t st);
 cudaError_t launch_lr1_probe(const QueryDev& q, long long k, cudaStream_t st);
+cudaError_t launch_sum_u32(uint32_t* dst, const uint32_t* const* srcs, uint32_t G, uint32_t n, cudaStream_t st);
 cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st);

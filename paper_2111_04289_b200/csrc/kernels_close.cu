@@ -703,7 +703,30 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_probe(const QueryDev q, l
   }
 }
 
+// dst[i] = sum over g of src[g][i] (the devices' LR1 window counts, read through peer memory:
+// the single-handle multi-device driver's all-reduce).
+struct SumSrcs {
+  const uint32_t* p[kMaxWorld];
+};
+__global__ void __launch_bounds__(kCloseThreads) k_sum_u32(uint32_t* dst, const SumSrcs src, uint32_t G, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t s = 0;
+    for (uint32_t g = 0; g < G; g++) s += __ldcg(src.p[g] + i);
+    dst[i] = s;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_sum_u32(uint32_t* dst, const uint32_t* const* srcs, uint32_t G, uint32_t n, cudaStream_t st) {
+  SumSrcs a{};
+  for (uint32_t g = 0; g < G && g < (uint32_t)kMaxWorld; g++) a.p[g] = srcs[g];
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  k_sum_u32<<<2 * nsm, kCloseThreads, 0, st>>>(dst, a, G, n);
+  return cudaGetLastError();
+}
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily, at first launch, and a
 // lazy load waits for the device: a first launch behind a running spin-wait kernel of another
@@ -716,6 +739,7 @@ void preload_close_kernels() {
   cudaFuncGetAttributes(&fa, k_lr1_evict);
   cudaFuncGetAttributes(&fa, k_lr1_wsum);
   cudaFuncGetAttributes(&fa, k_lr1_probe);
+  cudaFuncGetAttributes(&fa, k_sum_u32);
 }
 
 int close_ctas(const QueryDev& q) {

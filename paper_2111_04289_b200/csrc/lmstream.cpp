@@ -177,8 +177,20 @@ struct lms_query {
   std::string deferred_msg;
   bool poisoned = false;           // a fused-exchange barrier timed out: ranks may disagree on the
                                    // window state, so every later batch call fails (LMS_ESTATE)
+  // single-handle multi-device driver (cfg.num_gpus > 1): one sub-handle (rank g of G) per device;
+  // this handle keeps the host side (pending datasets, Alg. 1 / Eq. 4-6 / Eq. 10 history, batch
+  // records, row FIFOs) of the whole, row-partitioned micro-batch
+  std::vector<lms_query*> subs;
+  std::vector<cudaEvent_t> g_end;          // per sub: after the batch's last kernel (its stream)
+  std::vector<uint32_t*> g_lr1_w;          // LR1: per sub, the device-summed window counts
+  lms_batch_record g_cur{};
+  bool g_in_flight = false;
 
   ~lms_query() {
+    for (size_t g = 0; g < subs.size(); g++) {
+      if (g < g_end.size() && g_end[g]) { cudaSetDevice(subs[g]->cfg.device); cudaEventDestroy(g_end[g]); }
+      delete subs[g];
+    }
     cudaSetDevice(cfg.device);
     if (stream) cudaStreamSynchronize(stream);
     for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
@@ -232,10 +244,80 @@ lms_status validate_config(const lms_config* c) {
     return fail(LMS_EINVAL, "need 0 <= rank < world <= 64");
   if (c->world > 1 && c->mode != LMS_MODE_MANUAL)
     return fail(LMS_EINVAL, "multi-GPU handles use LMS_MODE_MANUAL (the caller forms batches in lockstep)");
+  if (c->num_gpus < 1 || c->num_gpus > kMaxWorld) return fail(LMS_EINVAL, "num_gpus must be 1..64");
+  if (c->num_gpus > 1 && (c->world != 1 || c->rank != 0))
+    return fail(LMS_EINVAL, "num_gpus > 1 drives all devices from one handle: rank / world stay 0 / 1");
   return LMS_OK;
 }
 
 lms_status launch_close_stage(lms_query* q);
+
+// Alg. 2 labels of a batch (report-only): Part = batch bytes / NumCores.
+void plan_labels(lms_query* q, lms_batch_record& r) {
+  const double t0 = now_host();
+  std::vector<uint8_t> dev;
+  const double part = (double)r.batch_bytes / (double)q->cfg.num_cores;
+  if (part > 0 && map_device(q->dag, part, q->infpt, q->cfg.base_trans_cost, dev)) {
+    for (size_t o = 0; o < dev.size(); o++) {
+      if (dev[o]) { r.n_gpu_ops++; r.plan_mask |= 1u << o; }
+      else r.n_cpu_ops++;
+    }
+  }
+  r.plan_overhead_s = now_host() - t0;
+}
+
+// Alg. 1 for one poll at `now` on the handle's buffered datasets (modes LMSTREAM / DEADLINE /
+// TRIGGER; MANUAL never admits here).
+void alg1_decide(lms_query* q, double now, bool& admit, int32_t& reason, double& est) {
+  const Mode mode = (Mode)q->cfg.mode;
+  admit = false;
+  reason = kBuffer;
+  est = std::nan("");
+  if (mode == Mode::Trigger) {
+    if (now >= q->next_trigger) {                 // OS(tN): trigger instants N, 2N, ...
+      q->next_trigger = (std::floor(now / q->cfg.trigger_s) + 1.0) * q->cfg.trigger_s;
+      if (!q->pending.empty()) { admit = true; reason = kAdmitTrigger; }
+    }
+  } else if (mode == Mode::LMStream || mode == Mode::Deadline) {
+    const size_t n = q->pending.size();
+    std::vector<double> ing(n);
+    std::vector<uint64_t> by(n);
+    for (size_t j = 0; j < n; j++) { ing[j] = q->pending[j].ingest; by[j] = q->pending[j].nbytes; }
+    const double thp = q->cum_proc > 0 ? q->cum_bytes / q->cum_proc : 0.0;
+    const double slide = is_tumbling(q->kind) ? 0.0 : (double)q->S;   // SlideTime (Table I)
+    AdmitResult ar = admit_decision(mode, slide, q->cfg.deadline_s, now, ing.data(), by.data(), n, thp,
+                                    q->maxlat_hist.data(), q->maxlat_hist.size());
+    admit = ar.admit;
+    reason = ar.reason;
+    est = ar.est;
+  }
+}
+
+// Eq. 4 / Eq. 5 bookkeeping of a completed batch, and the optional Eq. 10 refit.
+void account_batch(lms_query* q, lms_batch_record& r) {
+  r.max_lat_s = r.max_buff_s + r.proc_s;                     // Eq. 5
+  q->cum_bytes += (double)r.batch_bytes;                     // Eq. 4
+  q->cum_proc += r.proc_s;
+  r.avg_thput_Bps = q->cum_proc > 0 ? q->cum_bytes / q->cum_proc : 0;
+  if (r.num_datasets > 0) q->maxlat_hist.push_back(r.max_lat_s);
+  q->records.push_back(r);
+  if ((q->cfg.flags & LMS_FLAG_ONLINE_INFPT) && r.num_datasets > 0) {
+    q->reg_hist.push_back({r.avg_thput_Bps, r.max_lat_s, r.inf_pt_bytes});
+    if (q->reg_hist.size() > 256) q->reg_hist.pop_front();
+    std::vector<double> th, la, ip;
+    double tmax = 0, lsum = 0;
+    for (auto& h : q->reg_hist) {
+      th.push_back(h[0]); la.push_back(h[1]); ip.push_back(h[2]);
+      tmax = std::max(tmax, h[0]);
+      lsum += h[1];
+    }
+    double b[3];
+    if (infpt_fit(th.data(), la.data(), ip.data(), th.size(), b)) {
+      const double tl = is_tumbling(q->kind) ? lsum / (double)q->reg_hist.size() : (double)q->S;
+      q->infpt = infpt_predict(b, tmax, tl);
+    }
+  }
+}
 
 lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bool flush) {
   // the slot's report / rows buffers are what this batch's kernels write
@@ -259,19 +341,7 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
   r.est_max_lat_s = est;
   r.admit_reason = (uint32_t)reason;
   r.inf_pt_bytes = q->infpt;
-  // ---- Alg. 2 labels (report-only)
-  {
-    const double t0 = now_host();
-    std::vector<uint8_t> dev;
-    const double part = (double)r.batch_bytes / (double)q->cfg.num_cores;
-    if (part > 0 && map_device(q->dag, part, q->infpt, q->cfg.base_trans_cost, dev)) {
-      for (size_t o = 0; o < dev.size(); o++) {
-        if (dev[o]) { r.n_gpu_ops++; r.plan_mask |= 1u << o; }
-        else r.n_cpu_ops++;
-      }
-    }
-    r.plan_overhead_s = now_host() - t0;
-  }
+  plan_labels(q, r);
   // ---- input segments
   std::vector<Segment> segs;
   const int buf = q->in_cur;
@@ -385,35 +455,13 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
   r.device_s = q->last_batch_s;
   r.d2h_s = d2h;
   r.proc_s = ms_end * 1e-3 + d2h;                            // Proc_i (reading R18)
-  r.max_lat_s = r.max_buff_s + r.proc_s;                     // Eq. 5
-  q->cum_bytes += (double)r.batch_bytes;                     // Eq. 4
-  q->cum_proc += r.proc_s;
-  r.avg_thput_Bps = q->cum_proc > 0 ? q->cum_bytes / q->cum_proc : 0;
   r.windows_closed = rep.windows_closed;
   r.rows_emitted = rep.rows;
   r.late_records = rep.late;
   r.bad_records = rep.bad;
   r.overflow_records = rep.overflow;
   r.watermark = rep.watermark;
-  if (r.num_datasets > 0) q->maxlat_hist.push_back(r.max_lat_s);
-  q->records.push_back(r);
-  // Eq. 10: online inflection point, optional
-  if ((q->cfg.flags & LMS_FLAG_ONLINE_INFPT) && r.num_datasets > 0) {
-    q->reg_hist.push_back({r.avg_thput_Bps, r.max_lat_s, r.inf_pt_bytes});
-    if (q->reg_hist.size() > 256) q->reg_hist.pop_front();
-    std::vector<double> th, la, ip;
-    double tmax = 0, lsum = 0;
-    for (auto& h : q->reg_hist) {
-      th.push_back(h[0]); la.push_back(h[1]); ip.push_back(h[2]);
-      tmax = std::max(tmax, h[0]);
-      lsum += h[1];
-    }
-    double b[3];
-    if (infpt_fit(th.data(), la.data(), ip.data(), th.size(), b)) {
-      const double tl = is_tumbling(q->kind) ? lsum / (double)q->reg_hist.size() : (double)q->S;
-      q->infpt = infpt_predict(b, tmax, tl);
-    }
-  }
+  account_batch(q, r);                                       // Eq. 4 / 5 (/ 10)
   lms_status st = LMS_OK;
   if (rep.bad) st = fail(LMS_EFORMAT, "batch " + std::to_string(r.index) + ": " + std::to_string(rep.bad) +
                                           " malformed records dropped");
@@ -466,6 +514,353 @@ lms_status park_current(lms_query* q) {
 
 }  // namespace
 
+
+static lms_status push_common(lms_query* q, uint64_t nbytes, double t) {
+  if (!q) return fail(LMS_EINVAL, "null query");
+  if (nbytes == 0) return fail(LMS_EINVAL, "empty dataset");            // S:76
+  if (!(t >= q->last_ingest)) return fail(LMS_EINVAL, "ingest_time must be non-decreasing");
+  if (is_lr(q->kind) && nbytes % kLrRecBytes) return fail(LMS_EINVAL, "LR dataset is not whole 70 B records");
+  // one micro-batch (host-pushed + borrowed bytes) is capped at kMaxBatchTotal: the LR2 per-CTA
+  // u32 partials stay exact below it (device.h)
+  uint64_t pend = 0;
+  for (const Pending& d : q->pending) pend += d.nbytes;
+  if (nbytes > kMaxBatchTotal || pend + nbytes > kMaxBatchTotal)
+    return fail(LMS_EOVERFLOW, "micro-batch would exceed 2^37 bytes (admit the buffered datasets first)");
+  return LMS_OK;
+}
+
+// =====================================================================================
+// Single-handle multi-device driver (cfg.num_gpus > 1; SURVEY §8(b) num_gpus / device_ids,
+// §8(e) "a single process with G devices behind one lms_query handle").  The handle owns one
+// sub-handle per device (rank g of G, MANUAL) and drives the multi-GPU protocol itself:
+//   push        split at record boundaries (lms_split, P:417 partitions) -> each device's part
+//   Alg. 1      on the whole micro-batch (total bytes; AvgThPut / MaxLat of the whole job)
+//   launch      every device: aggregate pass -> device-side watermark exchange (peer memory)
+//               -> close (partial rows by key owner) -> fused push into the owners'
+//               accumulators -> device barrier -> owner finalize; all enqueued, no host sync
+//   complete    one collect per device; the owners' rows -> this handle's FIFO; Eq. 4 / 5 with
+//               Proc = the slowest device's admit -> last kernel (+ row copies)
+// LR1 (self-join): watermark folded across the devices, then per closing instance every
+// device's vehicle counts are summed over all devices by a peer-reading kernel and each device
+// probes its own rows against the sum (no rows move); this part is host-sequenced.
+namespace {
+
+lms_status push_staged(lms_query* q, const void* src, uint64_t nbytes, double t) {
+  // device (or any UVA) bytes copied into the handle's staging buffer (copy semantics)
+  lms_status s = push_common(q, nbytes, t);
+  if (s) return s;
+  CUDA_TRY(cudaSetDevice(q->cfg.device));
+  const int b = q->in_cur;
+  if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
+  const double t0 = now_host();
+  CUDA_TRY(cudaMemcpyAsync(q->d_in[b] + q->in_used[b], src, nbytes, cudaMemcpyDefault, q->copy_stream));
+  CUDA_TRY(cudaStreamSynchronize(q->copy_stream));
+  q->in_used[b] += nbytes;
+  q->pending.push_back({q->next_ds_id, t, nbytes, nullptr, now_host() - t0});
+  q->last_ingest = t;
+  q->next_ds_id++;
+  return LMS_OK;
+}
+
+lms_status group_create(const lms_config* cfg, lms_query** out) {
+  lms_query* q = new (std::nothrow) lms_query();
+  if (!q) return fail(LMS_ENOMEM, "host alloc");
+  auto bail = [&](lms_status st) { delete q; return st; };
+  q->cfg = *cfg;
+  q->cfg.device_ids = nullptr;
+  q->kind = cfg->kind;
+  table_iv(q->kind, q->R, q->S);
+  if (cfg->range_s > 0) q->R = (uint32_t)cfg->range_s;
+  if (is_tumbling(q->kind)) q->S = q->R;
+  else if (cfg->slide_s > 0) q->S = (uint32_t)cfg->slide_s;
+  if (q->S == 0 || q->S > q->R || q->R % q->S) return bail(fail(LMS_EINVAL, "window needs 0 < S <= R, S | R"));
+  q->ppw = q->R / q->S;
+  q->infpt = cfg->inf_pt_bytes;
+  q->next_trigger = cfg->trigger_s;
+  q->dag = query_dag(q->kind);
+  q->cfg.device = cfg->device_ids ? cfg->device_ids[0] : 0;
+  const int G = cfg->num_gpus;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return bail(fail(LMS_ECUDA, "no CUDA device"));
+  std::vector<int> ids(G);
+  for (int g = 0; g < G; g++) {
+    ids[g] = cfg->device_ids ? cfg->device_ids[g] : g;
+    if (ids[g] < 0 || ids[g] >= ndev) return bail(fail(LMS_EINVAL, "bad device ordinal in device_ids"));
+  }
+  for (int a = 0; a < G; a++)          // peer access between every pair of distinct devices
+    for (int b = 0; b < G; b++) {
+      if (ids[a] == ids[b]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, ids[a], ids[b]);
+      if (!can) return bail(fail(LMS_ECUDA, "devices without peer access (NVLink / NVSwitch needed)"));
+      if (cudaSetDevice(ids[a]) != cudaSuccess) return bail(fail(LMS_ECUDA, "cudaSetDevice"));
+      const cudaError_t e = cudaDeviceEnablePeerAccess(ids[b], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return bail(fail(LMS_ECUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e)));
+      cudaGetLastError();
+    }
+  for (int g = 0; g < G; g++) {
+    lms_config c = *cfg;
+    c.num_gpus = 1;
+    c.device_ids = nullptr;
+    c.device = ids[g];
+    c.rank = g;
+    c.world = G;
+    c.mode = LMS_MODE_MANUAL;                      // this handle forms the batches
+    c.flags &= ~(LMS_FLAG_PIPELINE | LMS_FLAG_ONLINE_INFPT);
+    lms_query* sub = nullptr;
+    if (lms_status st = lms_query_create(&c, &sub)) return bail(st);
+    q->subs.push_back(sub);
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return bail(fail(LMS_ECUDA, "cudaEventCreate"));
+    q->g_end.push_back(e);
+  }
+  if (!is_lr1(q->kind)) {                          // fused exchange + device-side watermark exchange
+    for (lms_query* a : q->subs)
+      for (lms_query* b : q->subs)
+        if (lms_status st = lms_p2p_import_local(a, b)) return bail(st);
+    for (lms_query* a : q->subs)
+      if (lms_status st = lms_p2p_device_watermark(a, 1)) return bail(st);
+  } else {
+    for (lms_query* a : q->subs) {
+      uint32_t* w = nullptr;
+      if (cudaSetDevice(a->cfg.device) != cudaSuccess) return bail(fail(LMS_ECUDA, "cudaSetDevice"));
+      if (lms_status st = a->dalloc(&w, a->qd.K, 0)) return bail(st);
+      q->g_lr1_w.push_back(w);
+    }
+  }
+  const uint64_t pre = std::min<uint64_t>(cfg->max_result_rows, is_lr1(q->kind) ? (1ull << 20) : (1ull << 16));
+  if (cudaSetDevice(q->cfg.device) != cudaSuccess) return bail(fail(LMS_ECUDA, "cudaSetDevice"));
+  if ((is_lr1(q->kind) ? q->lr1_rows.reserve(pre) : q->agg_rows.reserve(pre)) != cudaSuccess)
+    return bail(fail(LMS_ENOMEM, "pinned row FIFO"));
+  *out = q;
+  return LMS_OK;
+}
+
+// how: 0 host bytes (copied), 1 page-locked host bytes (asynchronous H2D), 2 device bytes
+lms_status group_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, uint64_t* id, int how) {
+  if (nbytes == 0) return fail(LMS_EINVAL, "empty dataset");
+  if (!bytes) return fail(LMS_EINVAL, "null bytes");
+  if (!(t >= q->last_ingest)) return fail(LMS_EINVAL, "ingest_time must be non-decreasing");
+  uint64_t pend = 0;
+  for (const Pending& d : q->pending) pend += d.nbytes;
+  if (nbytes > kMaxBatchTotal || pend + nbytes > kMaxBatchTotal)
+    return fail(LMS_EOVERFLOW, "micro-batch would exceed 2^37 bytes (admit the buffered datasets first)");
+  const uint32_t G = (uint32_t)q->subs.size();
+  std::vector<uint64_t> offs(G + 1);
+  if (lms_status st = lms_split(q->kind, bytes, nbytes, G, offs.data())) return st;
+  int src_dev = -1;
+  if (how == 2) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, bytes) != cudaSuccess || at.type != cudaMemoryTypeDevice) {
+      cudaGetLastError();
+      return fail(LMS_EINVAL, "not device memory");
+    }
+    src_dev = at.device;
+  }
+  for (uint32_t g = 0; g < G; g++) {
+    const uint64_t m = offs[g + 1] - offs[g];
+    if (!m) continue;                              // (a device may get no records of a dataset)
+    const uint8_t* part = static_cast<const uint8_t*>(bytes) + offs[g];
+    lms_query* sub = q->subs[g];
+    lms_status st;
+    if (how == 0) {
+      st = lms_push(sub, part, m, t, nullptr);
+    } else if (how == 1) {
+      st = lms_push_pinned(sub, part, m, t, nullptr);
+      if (st == LMS_EINVAL) st = lms_push(sub, part, m, t, nullptr);   // not pinned for that device
+    } else if (src_dev == sub->cfg.device && !(reinterpret_cast<uintptr_t>(part) & 15u)) {
+      st = lms_push_device(sub, part, m, t, nullptr);                  // borrowed in place
+    } else {
+      st = push_staged(sub, part, m, t);           // another device's (or unaligned) part: copy
+    }
+    if (st) return st;
+  }
+  q->pending.push_back({q->next_ds_id, t, nbytes, nullptr, 0.0});
+  q->last_ingest = t;
+  if (id) *id = q->next_ds_id;
+  q->next_ds_id++;
+  return LMS_OK;
+}
+
+lms_status group_launch(lms_query* q, double now, int32_t reason, double est, bool flush) {
+  lms_batch_record& r = q->g_cur;
+  r = lms_batch_record{};
+  r.index = q->records.size();
+  r.num_datasets = q->pending.size();
+  r.admit_time_s = now;
+  for (size_t j = 0; j < q->pending.size(); j++) {
+    r.batch_bytes += q->pending[j].nbytes;
+    r.max_buff_s = j == 0 ? now - q->pending[j].ingest : std::max(r.max_buff_s, now - q->pending[j].ingest);
+  }
+  r.est_max_lat_s = est;
+  r.admit_reason = (uint32_t)reason;
+  r.inf_pt_bytes = q->infpt;
+  plan_labels(q, r);
+  q->pending.clear();
+  lms_status bad = LMS_OK;
+  for (lms_query* sub : q->subs) {
+    const lms_status st = flush ? lms_flush(sub, now) : lms_force_batch(sub, now, nullptr);
+    if (st && st != LMS_EFORMAT && st != LMS_EOVERFLOW && st != LMS_EINVAL) return st;
+    if (st && !bad) bad = st;
+  }
+  const size_t G = q->subs.size();
+  if (!is_lr1(q->kind)) {
+    for (lms_query* sub : q->subs)
+      if (lms_status st = lms_p2p_exchange_async(sub)) return st;
+  } else {
+    for (lms_query* sub : q->subs) {               // aggregate passes done
+      CUDA_TRY(cudaSetDevice(sub->cfg.device));
+      CUDA_TRY(cudaStreamSynchronize(sub->stream));
+    }
+    // one global watermark / first ts (reading R7): folded across the devices' states
+    unsigned long long wm = 0, tsmin = 0xFFFFFFFFull;
+    for (lms_query* sub : q->subs) {
+      unsigned long long v[2];
+      CUDA_TRY(cudaSetDevice(sub->cfg.device));
+      CUDA_TRY(cudaMemcpy(&v[0], &sub->qd.state->wm, 8, cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(&v[1], &sub->qd.state->ts_min, 8, cudaMemcpyDeviceToHost));
+      wm = std::max(wm, v[0]);
+      tsmin = std::min(tsmin, v[1]);
+    }
+    for (lms_query* sub : q->subs) {
+      CUDA_TRY(cudaSetDevice(sub->cfg.device));
+      CUDA_TRY(cudaMemcpy(&sub->qd.state->wm, &wm, 8, cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMemcpy(&sub->qd.state->ts_min, &tsmin, 8, cudaMemcpyHostToDevice));
+    }
+    int64_t k0 = 0, k1 = -1;
+    if (lms_status st = lms_close_range(q->subs[0], &k0, &k1)) return st;
+    std::vector<const uint32_t*> srcs(G);
+    for (int64_t k = k0; k <= k1; k++) {
+      for (size_t g = 0; g < G; g++) {
+        void* p = nullptr;
+        uint64_t n = 0;
+        if (lms_status st = lms_lr1_window_counts(q->subs[g], k, &p, &n)) return st;
+        srcs[g] = static_cast<const uint32_t*>(p);
+      }
+      for (lms_query* sub : q->subs) {             // every device's counts of instance k written
+        CUDA_TRY(cudaSetDevice(sub->cfg.device));
+        CUDA_TRY(cudaStreamSynchronize(sub->stream));
+      }
+      for (size_t g = 0; g < G; g++) {             // sum over the devices (peer reads), then probe
+        lms_query* sub = q->subs[g];
+        CUDA_TRY(cudaSetDevice(sub->cfg.device));
+        CUDA_TRY(launch_sum_u32(q->g_lr1_w[g], srcs.data(), (uint32_t)G, sub->qd.K, sub->stream));
+        QueryDev d = sub->qd;
+        d.lr1_w = q->g_lr1_w[g];
+        CUDA_TRY(launch_lr1_probe(d, (long long)k, sub->stream));
+        sub->launches += 2;
+      }
+      for (lms_query* sub : q->subs) {             // before the next instance rewrites the counts
+        CUDA_TRY(cudaSetDevice(sub->cfg.device));
+        CUDA_TRY(cudaStreamSynchronize(sub->stream));
+      }
+    }
+    for (lms_query* sub : q->subs)
+      if (lms_status st = lms_run_close(sub)) return st;
+  }
+  for (size_t g = 0; g < G; g++) {
+    CUDA_TRY(cudaSetDevice(q->subs[g]->cfg.device));
+    CUDA_TRY(cudaEventRecord(q->g_end[g], q->subs[g]->stream));
+  }
+  q->g_in_flight = true;
+  return bad;
+}
+
+lms_status group_complete(lms_query* q) {
+  if (!q->g_in_flight) return LMS_OK;
+  q->g_in_flight = false;
+  lms_status first = LMS_OK;
+  std::string first_msg;
+  const bool lr1 = is_lr1(q->kind);
+  for (lms_query* sub : q->subs) {
+    const lms_status st = lr1 ? lms_sync(sub) : lms_p2p_collect(sub);
+    if (st && !first) { first = st; first_msg = g_err; }
+    if (st && st != LMS_EFORMAT && st != LMS_EOVERFLOW && st != LMS_EINVAL) return st;
+  }
+  if (!lr1) {   // a long flush: the instances beyond one merge window in host-driven passes
+    int64_t k0 = 0, k1 = -1;
+    if (lms_status st = lms_last_close_range(q->subs[0], &k0, &k1)) return st;
+    const int64_t W = q->subs[0]->qd.Wmerge;
+    for (int64_t k = k0 + W; k <= k1; k += W) {
+      const uint32_t nwin = (uint32_t)std::min<int64_t>(W, k1 - k + 1);
+      for (lms_query* sub : q->subs)
+        if (lms_status st = lms_p2p_push(sub, k, nwin)) return st;
+      for (lms_query* sub : q->subs) {
+        const lms_status st = lms_p2p_finalize(sub, k, nwin);
+        if (st && st != LMS_EOVERFLOW) return st;
+        if (st && !first) { first = st; first_msg = g_err; }
+      }
+    }
+  }
+  lms_batch_record& r = q->g_cur;
+  double proc = 0, rows_s = 0;
+  const double t0 = now_host();
+  for (size_t g = 0; g < q->subs.size(); g++) {
+    lms_query* sub = q->subs[g];
+    const lms_batch_record& sr = sub->records.back();
+    r.num_records += sr.num_records;
+    r.late_records += sr.late_records;
+    r.bad_records += sr.bad_records;
+    r.overflow_records += sr.overflow_records;
+    r.device_s = std::max(r.device_s, sr.device_s);
+    r.h2d_s = std::max(r.h2d_s, sr.h2d_s);
+    r.d2h_s += sr.d2h_s;
+    if (g == 0) { r.windows_closed = sr.windows_closed; r.watermark = sr.watermark; }
+    float ms = 0;
+    CUDA_TRY(cudaSetDevice(sub->cfg.device));
+    CUDA_TRY(cudaEventElapsedTime(&ms, sub->F().ev_admit, q->g_end[g]));
+    proc = std::max(proc, ms * 1e-3 + sr.d2h_s);
+    // the device's final rows -> this handle's FIFO
+    if (lr1) {
+      const uint64_t n = sub->lr1_rows.size();
+      CUDA_TRY(q->lr1_rows.reserve(n));
+      q->lr1_rows.commit(sub->lr1_rows.read(q->lr1_rows.tail_ptr(), n));
+      r.rows_emitted += n;
+    } else {
+      const uint64_t n = sub->agg_rows.size();
+      CUDA_TRY(q->agg_rows.reserve(n));
+      q->agg_rows.commit(sub->agg_rows.read(q->agg_rows.tail_ptr(), n));
+      r.rows_emitted += n;
+    }
+  }
+  rows_s = now_host() - t0;
+  r.proc_s = proc + rows_s;                        // Proc_i: the slowest device (reading R18)
+  account_batch(q, r);                             // Eq. 4 / 5 (/ 10) on the whole micro-batch
+  if (first) g_err = first_msg;
+  return first;
+}
+
+lms_status group_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx) {
+  lms_status cs = LMS_OK;
+  if (q->g_in_flight) {
+    for (size_t g = 0; g < q->subs.size(); g++) {
+      CUDA_TRY(cudaSetDevice(q->subs[g]->cfg.device));
+      const cudaError_t e = cudaEventQuery(q->g_end[g]);
+      if (e == cudaErrorNotReady) return LMS_OK;   // one micro-batch in flight at a time
+      if (e != cudaSuccess) return fail(LMS_ECUDA, cudaGetErrorString(e));
+    }
+    cs = group_complete(q);
+  }
+  bool admit = false;
+  int32_t reason = kBuffer;
+  double est = std::nan("");
+  const double t0 = now_host();
+  alg1_decide(q, now, admit, reason, est);
+  const double admit_overhead = now_host() - t0;
+  if (admit) {
+    const lms_status s = group_launch(q, now, reason, est, false);
+    if (s && s != LMS_EFORMAT && s != LMS_EOVERFLOW && s != LMS_EINVAL) return s;
+    q->g_cur.admit_overhead_s = admit_overhead;
+    if (admitted) *admitted = 1;
+    if (bidx) *bidx = q->g_cur.index;
+    if (s && !cs) cs = s;
+  }
+  return cs;
+}
+
+}  // namespace
+
 // =====================================================================================
 extern "C" {
 
@@ -496,6 +891,8 @@ lms_status lms_config_init(lms_config* c, int32_t kind) {
   c->flags = 0;
   c->rank = 0;
   c->world = 1;
+  c->num_gpus = 1;
+  c->device_ids = nullptr;
   return LMS_OK;
 }
 
@@ -505,6 +902,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     *out = nullptr;
     lms_status s = validate_config(cfg);
     if (s) return s;
+    if (cfg->num_gpus > 1) return group_create(cfg, out);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(LMS_ECUDA, "no CUDA device");
     if (cfg->device < 0 || cfg->device >= ndev) return fail(LMS_EINVAL, "bad device ordinal");
@@ -679,22 +1077,10 @@ lms_status lms_query_destroy(lms_query* q) {
   }
 }
 
-static lms_status push_common(lms_query* q, uint64_t nbytes, double t) {
-  if (!q) return fail(LMS_EINVAL, "null query");
-  if (nbytes == 0) return fail(LMS_EINVAL, "empty dataset");            // S:76
-  if (!(t >= q->last_ingest)) return fail(LMS_EINVAL, "ingest_time must be non-decreasing");
-  if (is_lr(q->kind) && nbytes % kLrRecBytes) return fail(LMS_EINVAL, "LR dataset is not whole 70 B records");
-  // one micro-batch (host-pushed + borrowed bytes) is capped at kMaxBatchTotal: the LR2 per-CTA
-  // u32 partials stay exact below it (device.h)
-  uint64_t pend = 0;
-  for (const Pending& d : q->pending) pend += d.nbytes;
-  if (nbytes > kMaxBatchTotal || pend + nbytes > kMaxBatchTotal)
-    return fail(LMS_EOVERFLOW, "micro-batch would exceed 2^37 bytes (admit the buffered datasets first)");
-  return LMS_OK;
-}
 
 lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, uint64_t* id) {
   try {
+    if (q && !q->subs.empty()) return group_push(q, bytes, nbytes, t, id, 0);
     lms_status s = push_common(q, nbytes, t);
     if (s) return s;
     if (!bytes) return fail(LMS_EINVAL, "null bytes");
@@ -726,6 +1112,7 @@ lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, 
 
 lms_status lms_push_pinned(lms_query* q, const void* bytes, uint64_t nbytes, double t, uint64_t* id) {
   try {
+    if (q && !q->subs.empty()) return group_push(q, bytes, nbytes, t, id, 1);
     lms_status s = push_common(q, nbytes, t);
     if (s) return s;
     if (!bytes) return fail(LMS_EINVAL, "null bytes");
@@ -761,6 +1148,7 @@ lms_status lms_push_pinned(lms_query* q, const void* bytes, uint64_t nbytes, dou
 
 lms_status lms_push_device(lms_query* q, const void* dptr, uint64_t nbytes, double t, uint64_t* id) {
   try {
+    if (q && !q->subs.empty()) return group_push(q, dptr, nbytes, t, id, 2);
     lms_status s = push_common(q, nbytes, t);
     if (s) return s;
     if (!dptr || (reinterpret_cast<uintptr_t>(dptr) & 15u)) return fail(LMS_EINVAL, "device pointer must be 16 B aligned");
@@ -784,6 +1172,7 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
     if (admitted) *admitted = 0;
+    if (!q->subs.empty()) return group_poll(q, now, admitted, bidx);
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status cs = LMS_OK;
     if (q->parked) cs = complete(q);                  // (pipelined handles polled: drain)
@@ -796,29 +1185,11 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
       lms_status c2 = complete(q);
       cs = cs ? cs : c2;
     }
-    const Mode mode = (Mode)q->cfg.mode;
     bool admit = false;
     int32_t reason = kBuffer;
     double est = std::nan("");
     const double t0 = now_host();
-    if (mode == Mode::Trigger) {
-      if (now >= q->next_trigger) {                 // OS(tN): trigger instants N, 2N, ...
-        q->next_trigger = (std::floor(now / q->cfg.trigger_s) + 1.0) * q->cfg.trigger_s;
-        if (!q->pending.empty()) { admit = true; reason = kAdmitTrigger; }
-      }
-    } else if (mode == Mode::LMStream || mode == Mode::Deadline) {
-      const size_t n = q->pending.size();
-      std::vector<double> ing(n);
-      std::vector<uint64_t> by(n);
-      for (size_t j = 0; j < n; j++) { ing[j] = q->pending[j].ingest; by[j] = q->pending[j].nbytes; }
-      const double thp = q->cum_proc > 0 ? q->cum_bytes / q->cum_proc : 0.0;
-      const double slide = is_tumbling(q->kind) ? 0.0 : (double)q->S;   // SlideTime (Table I)
-      AdmitResult ar = admit_decision(mode, slide, q->cfg.deadline_s, now, ing.data(), by.data(), n, thp,
-                                      q->maxlat_hist.data(), q->maxlat_hist.size());
-      admit = ar.admit;
-      reason = ar.reason;
-      est = ar.est;
-    }
+    alg1_decide(q, now, admit, reason, est);
     const double admit_overhead = now_host() - t0;
     if (admit) {
       lms_status s = launch_batch(q, now, reason, est, false);
@@ -837,6 +1208,13 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
     if (bidx) *bidx = UINT64_MAX;
+    if (!q->subs.empty()) {
+      if (q->g_in_flight) return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
+      if (q->pending.empty()) return LMS_OK;
+      const lms_status s = group_launch(q, now, kAdmitForced, std::nan(""), false);
+      if (bidx && q->g_in_flight) *bidx = q->g_cur.index;
+      return s;
+    }
     if (q->awaiting_close || (q->in_flight && !q->pipeline))
       return fail(LMS_ESTATE, "a batch is in flight (call lms_sync)");
     if (q->p2p_async_pending) return fail(LMS_ESTATE, "fused exchange pending (call lms_p2p_collect)");
@@ -857,6 +1235,7 @@ lms_status lms_force_batch(lms_query* q, double now, uint64_t* bidx) {
 lms_status lms_sync(lms_query* q) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
+    if (!q->subs.empty()) return group_complete(q);
     if (q->awaiting_close) return fail(LMS_ESTATE, "multi-GPU batch: call lms_run_close first");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     return complete_all(q);
@@ -868,6 +1247,14 @@ lms_status lms_sync(lms_query* q) {
 lms_status lms_flush(lms_query* q, double now) {
   try {
     if (!q) return fail(LMS_EINVAL, "null query");
+    if (!q->subs.empty()) {
+      const lms_status s1 = group_complete(q);
+      if (s1 && s1 != LMS_EFORMAT && s1 != LMS_EOVERFLOW && s1 != LMS_EINVAL) return s1;
+      const lms_status s = group_launch(q, now, kAdmitFlush, std::nan(""), true);
+      if (s && s != LMS_EFORMAT && s != LMS_EOVERFLOW && s != LMS_EINVAL) return s;
+      const lms_status s2 = group_complete(q);
+      return s1 ? s1 : (s ? s : s2);
+    }
     if (q->awaiting_close) return fail(LMS_ESTATE, "multi-GPU batch: call lms_run_close first");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status s1 = complete_all(q);
@@ -914,6 +1301,16 @@ lms_status lms_get_batch_record(lms_query* q, uint64_t i, lms_batch_record* out)
 
 lms_status lms_last_kernel_times(lms_query* q, double* batch_s, double* agg_s, double* close_s) {
   if (!q) return fail(LMS_EINVAL, "null query");
+  if (!q->subs.empty()) {                          // the slowest device's
+    double b = 0, a = 0, c = 0;
+    for (lms_query* sub : q->subs) {
+      b = std::max(b, sub->last_batch_s); a = std::max(a, sub->last_agg_s); c = std::max(c, sub->last_close_s);
+    }
+    if (batch_s) *batch_s = b;
+    if (agg_s) *agg_s = a;
+    if (close_s) *close_s = c;
+    return LMS_OK;
+  }
   if (batch_s) *batch_s = q->last_batch_s;
   if (agg_s) *agg_s = q->last_agg_s;
   if (close_s) *close_s = q->last_close_s;
@@ -923,12 +1320,14 @@ lms_status lms_last_kernel_times(lms_query* q, double* batch_s, double* agg_s, d
 lms_status lms_kernel_launches(lms_query* q, uint64_t* n) {
   if (!q || !n) return fail(LMS_EINVAL, "null argument");
   *n = q->launches;
+  for (lms_query* sub : q->subs) *n += sub->launches;
   return LMS_OK;
 }
 
 // ------------------------------------------------------------------ multi-GPU protocol
 lms_status lms_watermark_ptrs(lms_query* q, void** wm, void** tsmin, void** stream) {
   if (!q || !wm || !tsmin || !stream) return fail(LMS_EINVAL, "null argument");
+  if (!q->subs.empty()) return fail(LMS_ESTATE, "a num_gpus > 1 handle runs the multi-GPU protocol itself");
   *wm = &q->qd.state->wm;
   *tsmin = &q->qd.state->ts_min;
   *stream = q->stream;
@@ -1091,7 +1490,11 @@ lms_status lms_p2p_import_local(lms_query* q, lms_query* peer) {
     if (lms_status e = p2p_check(q)) return e;
     if (!peer || peer->qd.world != q->qd.world || peer->qd.K != q->qd.K || peer->kind != q->kind)
       return fail(LMS_EINVAL, "peer handle of another query shape");
-    if (peer->cfg.device != q->cfg.device) return fail(LMS_EINVAL, "in-process peers must share the device");
+    if (peer->cfg.device != q->cfg.device) {       // another device of this process: peer access
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, q->cfg.device, peer->cfg.device);
+      if (!can) return fail(LMS_EINVAL, "in-process peers on devices without peer access");
+    }
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     if (q->peers_h.empty()) q->peers_h.assign(q->qd.world, PeerView{});
     PeerView v{};

@@ -38,7 +38,7 @@ def test_every_declared_symbol_is_exported(L):
 
 
 def test_abi_version_and_struct_sizes(L):
-    assert L.lms_abi_version() == 1
+    assert L.lms_abi_version() == 2
     assert C.sizeof(L.lms_agg_row) == 72
     assert C.sizeof(L.lms_lr1_row) == 32
 
