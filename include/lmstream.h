@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define LMS_ABI_VERSION 2u
+#define LMS_ABI_VERSION 3u
 
 typedef struct lms_query lms_query;      /* opaque, library-owned */
 
@@ -185,6 +185,11 @@ typedef struct {
   uint64_t bad_records;
   uint64_t overflow_records;
   int64_t  watermark;        /* max ts seen (-1: none)                           */
+  double   opt_overhead_s;   /* LMS_FLAG_ONLINE_INFPT: duration of the Eq. 10 refit that
+                                produced this batch's InfPT (run on the handle's worker
+                                thread after the previous batch completed)      */
+  double   opt_block_s;      /* time this batch's launch waited for that refit (Table V
+                                "optimization blocking"); 0 when it had finished   */
 } lms_batch_record;
 
 enum { LMS_ADMIT_FORCED = 0, LMS_ADMIT_BOOTSTRAP = 1, LMS_ADMIT_TARGET = 2,

@@ -17,7 +17,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- constants
-LMS_ABI_VERSION = 2
+LMS_ABI_VERSION = 3
 LMS_OK, LMS_EINVAL, LMS_ENOMEM, LMS_ECUDA, LMS_ENCCL, LMS_EHISTORY, LMS_EPLAN, LMS_EFORMAT, \
     LMS_ESTATE, LMS_EOVERFLOW, LMS_EINTERNAL = 0, -1, -2, -3, -4, -5, -6, -7, -8, -9, -10
 STATUS_NAMES = {0: "LMS_OK", -1: "LMS_EINVAL", -2: "LMS_ENOMEM", -3: "LMS_ECUDA", -4: "LMS_ENCCL",
@@ -70,7 +70,8 @@ class lms_batch_record(C.Structure):
                 ("n_gpu_ops", C.c_uint32), ("plan_mask", C.c_uint32), ("admit_reason", C.c_uint32),
                 ("plan_overhead_s", C.c_double), ("admit_overhead_s", C.c_double),
                 ("windows_closed", C.c_uint64), ("rows_emitted", C.c_uint64), ("late_records", C.c_uint64),
-                ("bad_records", C.c_uint64), ("overflow_records", C.c_uint64), ("watermark", C.c_int64)]
+                ("bad_records", C.c_uint64), ("overflow_records", C.c_uint64), ("watermark", C.c_int64),
+                ("opt_overhead_s", C.c_double), ("opt_block_s", C.c_double)]
 
 
 class lms_p2p_handle(C.Structure):

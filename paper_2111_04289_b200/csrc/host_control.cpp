@@ -1,6 +1,8 @@
 // Host-side control of the LMStream micro-batch loop.  See host_control.h.
 #include "host_control.h"
 
+#include <chrono>
+
 #include <algorithm>
 #include <cmath>
 #include <functional>
@@ -150,6 +152,67 @@ bool infpt_fit(const double* thput, const double* lat, const double* infpt, uint
 double infpt_predict(const double b[3], double thput, double lat) {
   const double v = b[0] + b[1] * (thput / 1e6) + b[2] * lat;
   return std::min(16.0 * 1024 * 1024, std::max(1024.0, v));   // clamp
+}
+
+// ---------------------------------------------------------------- asynchronous Eq. 10 refit
+
+static double mono_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+RefitWorker::~RefitWorker() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+  }
+  cv_.notify_all();
+  if (th_.joinable()) th_.join();
+}
+
+void RefitWorker::submit(Job&& job) {
+  {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return !has_job_; });      // at most one fit outstanding
+    job_ = std::move(job);
+    has_job_ = true;
+    done_ = false;
+    submitted_ = true;
+  }
+  if (!th_.joinable()) th_ = std::thread(&RefitWorker::loop, this);
+  cv_.notify_all();
+}
+
+bool RefitWorker::collect(double& infpt, double& fit_s, double& block_s) {
+  const double t0 = mono_s();
+  std::unique_lock<std::mutex> lk(mu_);
+  cv_.wait(lk, [&] { return done_; });
+  block_s = mono_s() - t0;
+  submitted_ = false;
+  fit_s = fit_s_;
+  if (ok_) infpt = out_;
+  return ok_;
+}
+
+void RefitWorker::loop() {
+  std::unique_lock<std::mutex> lk(mu_);
+  while (true) {
+    cv_.wait(lk, [&] { return stop_ || has_job_; });
+    if (stop_) return;
+    Job j = std::move(job_);
+    lk.unlock();
+    const double t0 = mono_s();
+    double b[3];
+    const bool ok = infpt_fit(j.thput.data(), j.lat.data(), j.infpt.data(), j.thput.size(), b);
+    const double v = ok ? infpt_predict(b, j.target_thput, j.target_lat) : 0.0;
+    const double dt = mono_s() - t0;
+    lk.lock();
+    ok_ = ok;
+    out_ = v;
+    fit_s_ = dt;
+    has_job_ = false;
+    done_ = true;
+    cv_.notify_all();
+  }
 }
 
 double percentile_nearest_rank(std::vector<double> v, double p) {

@@ -7,9 +7,12 @@
 //  * Regression: Eq. 10 online OLS of the inflection point.
 //  * Metrics: Eq. 4 AvgThPut, Eq. 5 MaxLat, nearest-rank percentiles.
 #pragma once
+#include <condition_variable>
 #include <cstdint>
 #include <deque>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace lms {
@@ -59,6 +62,38 @@ Dag query_dag(int32_t kind);                             // SPEC S:153 catalog
 bool infpt_fit(const double* thput, const double* lat, const double* infpt, uint64_t n,
                double b[3]);
 double infpt_predict(const double b[3], double thput, double lat);
+
+// Asynchronous Eq. 10 refit ("LMStream handles the optimization process
+// asynchronously ... the results only need to be returned before the next processing phase").
+// One persistent worker thread per handle: submit() hands over the history snapshot at a
+// batch's completion and returns at once; collect() — called when the next batch is planned,
+// the first consumer of InfPT — waits for that fit and reports how long the fit took and how
+// long the caller was blocked on it (Table V "optimization blocking").
+class RefitWorker {
+ public:
+  struct Job {
+    std::vector<double> thput, lat, infpt;   // Eq. 10 training rows (history)
+    double target_thput = 0, target_lat = 0; // test inputs
+  };
+  RefitWorker() = default;
+  RefitWorker(const RefitWorker&) = delete;
+  RefitWorker& operator=(const RefitWorker&) = delete;
+  ~RefitWorker();
+  void submit(Job&& job);
+  bool pending() const { return submitted_; }
+  // Waits for the last submitted job.  Returns true with the predicted InfPT when the fit
+  // succeeded (false: insufficient / degenerate history, InfPT unchanged).
+  bool collect(double& infpt, double& fit_s, double& block_s);
+
+ private:
+  void loop();
+  std::thread th_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  Job job_;
+  bool has_job_ = false, done_ = false, stop_ = false, submitted_ = false, ok_ = false;
+  double out_ = 0, fit_s_ = 0;
+};
 
 double percentile_nearest_rank(std::vector<double> v, double p);
 

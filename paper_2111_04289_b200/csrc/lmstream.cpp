@@ -138,6 +138,7 @@ struct lms_query {
   double next_trigger = 0;
   double infpt = 150e3;
   std::deque<std::array<double, 3>> reg_hist;
+  RefitWorker refit;               // Eq. 10 refit off the batch path
   Dag dag;
   // in-flight batches: slot `cur_slot` holds the newest batch (in_flight), and with
   // LMS_FLAG_PIPELINE the other slot may hold the previous, still running one (parked), so the
@@ -254,6 +255,10 @@ lms_status launch_close_stage(lms_query* q);
 
 // Alg. 2 labels of a batch (report-only): Part = batch bytes / NumCores.
 void plan_labels(lms_query* q, lms_batch_record& r) {
+  // InfPT_i is first needed here: collect the asynchronous Eq. 10 refit started when the
+  // previous batch completed (its wait is the batch's optimisation blocking, Table V)
+  if (q->refit.pending()) q->refit.collect(q->infpt, r.opt_overhead_s, r.opt_block_s);
+  r.inf_pt_bytes = q->infpt;
   const double t0 = now_host();
   std::vector<uint8_t> dev;
   const double part = (double)r.batch_bytes / (double)q->cfg.num_cores;
@@ -302,20 +307,22 @@ void account_batch(lms_query* q, lms_batch_record& r) {
   if (r.num_datasets > 0) q->maxlat_hist.push_back(r.max_lat_s);
   q->records.push_back(r);
   if ((q->cfg.flags & LMS_FLAG_ONLINE_INFPT) && r.num_datasets > 0) {
+    // Eq. 10: training rows = (AvgThPut, MaxLat) -> InfPT of past batches (the
+    // newest 256); test inputs = the maximum past throughput and the target latency
+    // (SlideTime, Eq. 2, or the mean past MaxLat for tumbling windows, Eq. 3).  The fit runs
+    // on the worker thread; plan_labels of the next batch collects it.
     q->reg_hist.push_back({r.avg_thput_Bps, r.max_lat_s, r.inf_pt_bytes});
     if (q->reg_hist.size() > 256) q->reg_hist.pop_front();
-    std::vector<double> th, la, ip;
+    RefitWorker::Job job;
     double tmax = 0, lsum = 0;
     for (auto& h : q->reg_hist) {
-      th.push_back(h[0]); la.push_back(h[1]); ip.push_back(h[2]);
+      job.thput.push_back(h[0]); job.lat.push_back(h[1]); job.infpt.push_back(h[2]);
       tmax = std::max(tmax, h[0]);
       lsum += h[1];
     }
-    double b[3];
-    if (infpt_fit(th.data(), la.data(), ip.data(), th.size(), b)) {
-      const double tl = is_tumbling(q->kind) ? lsum / (double)q->reg_hist.size() : (double)q->S;
-      q->infpt = infpt_predict(b, tmax, tl);
-    }
+    job.target_thput = tmax;
+    job.target_lat = is_tumbling(q->kind) ? lsum / (double)q->reg_hist.size() : (double)q->S;
+    q->refit.submit(std::move(job));
   }
 }
 
@@ -340,7 +347,6 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
   r.h2d_s = h2d;
   r.est_max_lat_s = est;
   r.admit_reason = (uint32_t)reason;
-  r.inf_pt_bytes = q->infpt;
   plan_labels(q, r);
   // ---- input segments
   std::vector<Segment> segs;
@@ -695,7 +701,6 @@ lms_status group_launch(lms_query* q, double now, int32_t reason, double est, bo
   }
   r.est_max_lat_s = est;
   r.admit_reason = (uint32_t)reason;
-  r.inf_pt_bytes = q->infpt;
   plan_labels(q, r);
   q->pending.clear();
   lms_status bad = LMS_OK;

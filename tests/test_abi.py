@@ -37,10 +37,21 @@ def test_every_declared_symbol_is_exported(L):
     assert set(syms) == set(L.EXPORTED)
 
 
-def test_abi_version_and_struct_sizes(L):
-    assert L.lms_abi_version() == 2
+def test_abi_version_and_struct_sizes(L, tmp_path):
+    assert L.lms_abi_version() == L.LMS_ABI_VERSION == 3
     assert C.sizeof(L.lms_agg_row) == 72
     assert C.sizeof(L.lms_lr1_row) == 32
+    # the ctypes mirrors match the C compiler's layout of include/lmstream.h
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include "lmstream.h"\nint main(void){printf("%zu %zu %zu %zu %zu\\n",'
+                   ' sizeof(lms_config), sizeof(lms_batch_record), sizeof(lms_agg_row), sizeof(lms_lr1_row),'
+                   ' sizeof(lms_dag)); return 0;}\n')
+    exe = tmp_path / "sz"
+    import subprocess
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert got == [C.sizeof(L.lms_config), C.sizeof(L.lms_batch_record), C.sizeof(L.lms_agg_row),
+                   C.sizeof(L.lms_lr1_row), C.sizeof(L.lms_dag)]
 
 
 def test_config_defaults_and_validation(L):

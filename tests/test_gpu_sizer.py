@@ -181,3 +181,9 @@ def test_online_infpt_regression_in_the_loop():
             infpt = RG.predict(b, *RG.targets(hist[-256:], 10.0))   # LR2S: SlideTime 10 s
             updates += 1
     assert updates > 10
+    # the refit ran off the batch path: every batch after a refit carries its
+    # duration, and the wait of the next launch on it (Table V "optimization blocking")
+    fitted = [r for r in recs[1:] if r["opt_overhead_s"] > 0]
+    assert len(fitted) > 10
+    assert all(0 <= r["opt_block_s"] < 1.0 for r in recs)
+    assert recs[0]["opt_overhead_s"] == 0 and recs[0]["opt_block_s"] == 0

@@ -2,7 +2,7 @@
 # One GPU call: tests, smoke, bench, ncu launch list + full captures of the dominant kernels.
 # Usage (under gpurun): bash tools/gpu_round.sh <tag>
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02b}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_power_cap --format=csv > $OUT/nvsmi.txt 2>&1
