@@ -219,12 +219,17 @@ struct CtaCounters {
   uint32_t ts_min, ts_max1;   // ts_max1 = max ts + 1 (0 = none)
 };
 
-__device__ __forceinline__ void flush_counters(CtaCounters c, DevState* st) {
-  __shared__ unsigned long long s_n[32], s_bad[32], s_late[32], s_ovf[32];
-  __shared__ uint32_t s_min[32], s_max[32];
+// scratch: >= 1280 B of 8 B aligned shared memory the CTA no longer uses (the caller's buffers,
+// so that this does not add to a kernel's static shared memory); the CTA synchronises first.
+__device__ __forceinline__ void flush_counters(CtaCounters c, DevState* st, void* scratch) {
+  unsigned long long* s_n = static_cast<unsigned long long*>(scratch);
+  unsigned long long *s_bad = s_n + 32, *s_late = s_n + 64, *s_ovf = s_n + 96;
+  uint32_t* s_min = reinterpret_cast<uint32_t*>(s_n + 128);
+  uint32_t* s_max = s_min + 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   c.n = warp_sum(c.n); c.bad = warp_sum(c.bad); c.late = warp_sum(c.late); c.overflow = warp_sum(c.overflow);
   c.ts_min = warp_min_u32(c.ts_min); c.ts_max1 = warp_max_u32(c.ts_max1);
+  __syncthreads();
   if (lane == 0) { s_n[w] = c.n; s_bad[w] = c.bad; s_late[w] = c.late; s_ovf[w] = c.overflow;
                    s_min[w] = c.ts_min; s_max[w] = c.ts_max1; }
   __syncthreads();
@@ -243,6 +248,11 @@ __device__ __forceinline__ void flush_counters(CtaCounters c, DevState* st) {
       if (mx) atomicMax(&st->wm, (unsigned long long)mx);
     }
   }
+}
+
+__device__ __forceinline__ void flush_counters(CtaCounters c, DevState* st) {
+  __shared__ __align__(8) unsigned long long scratch[160];
+  flush_counters(c, st, scratch);
 }
 
 }  // namespace lms

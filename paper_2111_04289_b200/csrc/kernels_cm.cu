@@ -181,23 +181,15 @@ __device__ __forceinline__ void issue_s(uint32_t dst, const void* src, uint32_t 
                " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
-// Issue the copy of the producer iterator's tile into stage `dst` (full tiles: constant size).
-__device__ __forceinline__ void cm_issue_it(const TileIter& it, uint32_t dst, uint32_t bar) {
-  if (it.full()) {
-    issue_s(dst, it.seg + it.off - kCmHaloL, kCmStage, bar);
-    return;
-  }
-  const TileGeom g = it.geom();
-  const uint32_t bulk = (g.hi - g.lo) & ~15u;
-  if (bulk) issue_s(dst + g.lo, g.seg + g.off - kCmHaloL + g.lo, bulk, bar);
-  else asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(0u) : "memory");
-}
-
 struct CmRec {
   uint32_t ts;
   unsigned long long job;
   uint32_t event, cat, cpu_m;
+  // fast path, CM2: the jobId and cpu digits as SWAR digit values (byte - '0'); the values are
+  // decoded only for survivors, by the drain (cm_job_value / cm_cpu_value)
+  uint32_t jw0, jw1, jw2, cw0, cw1;
 };
+constexpr uint32_t kRawValues = 0xFFFFFFFFu;   // cw1 marker: jw0/jw1 = jobId, cw0 = cpu_m (slow path)
 
 __device__ __forceinline__ bool digits_u32(const uint8_t* b, uint32_t n, uint32_t& v) {
   v = 0;
@@ -448,6 +440,7 @@ __device__ __forceinline__ uint32_t swar4d(uint32_t d) {
 // so the fast path never rejects anything itself.  sb / e: mask bits of the record start and
 // of its '\n' (sb <= 4096).  Every smem address stays inside the stage (see `ec`), so that
 // predicated-off garbage positions cannot fault.
+template <bool kLazy>
 __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
@@ -503,8 +496,9 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   d1 -= 0x30303030u;
   d2 -= 0x30303030u;
   bad |= dbad(d0) | dbad(d1) | (dbad(d2) & 0x8080u);
-  const uint32_t lo2 = __byte_perm(d2 * 0xA01u, 0u, 0x4441u);     // 10 * d2_0 + d2_1
-  r.job = (unsigned long long)(swar4d(d0) * 10000u + swar4d(d1)) * 100ull + lo2;
+  r.jw0 = d0;
+  r.jw1 = d1;
+  r.jw2 = d2;
   // eventType at c4 + 1 = S + o0 + 14 + a4; category at c6 + 1
   r.event = (uint32_t)buf[S + o0 + 14u + a4] - 48u;
   r.cat = (uint32_t)buf[cat_at] - 48u;
@@ -516,8 +510,55 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   ok &= ((p0 >> 8) & 0xFFu) == '.';
   const uint32_t dp0 = (p0 ^ 0x1E00u) - 0x30303030u, dp1 = p1 - 0x30303030u;
   bad |= dbad(dp0) | dbad(dp1);
-  r.cpu_m = swar4d(dp0) * 10000u + swar4d(dp1) - 9000000u * (dp0 & 0xFFu);
+  if (kLazy) {
+    r.cw0 = dp0;
+    r.cw1 = dp1;
+  } else {
+    r.cpu_m = swar4d(dp0) * 10000u + swar4d(dp1) - 9000000u * (dp0 & 0xFFu);
+  }
   return ok && (bad & 0x80808080u) == 0u;
+}
+
+// Values of the digit words cm_fast kept (jobId: 10 digits in jw0..jw2; cpu: D0DDDDDD in cw0, cw1
+// with the integer digit's weight fixed up 10^7 -> 10^6), or the slow path's values (kRawValues).
+__device__ __forceinline__ unsigned long long cm_job_value(uint32_t jw0, uint32_t jw1, uint32_t jw2, uint32_t cw1) {
+  const uint32_t lo2 = __byte_perm(jw2 * 0xA01u, 0u, 0x4441u);     // 10 * d2_0 + d2_1
+  const unsigned long long v = (unsigned long long)(swar4d(jw0) * 10000u + swar4d(jw1)) * 100ull + lo2;
+  return cw1 == kRawValues ? ((unsigned long long)jw1 << 32 | jw0) : v;
+}
+__device__ __forceinline__ uint32_t cm_cpu_value(uint32_t cw0, uint32_t cw1) {
+  const uint32_t v = swar4d(cw0) * 10000u + swar4d(cw1) - 9000000u * (cw0 & 0xFFu);
+  return cw1 == kRawValues ? cw0 : v;
+}
+
+// Tile geometry, packed into one word when the tile's copy is issued (two tiles before it is
+// consumed): payload bytes [0, 13), valid mask bits (stage bytes [16, 16 + hi_bits)) [13, 26),
+// segment start (left halo invalid) bit 26, the next tile continues the segment bit 27.
+constexpr uint32_t kGeoFull = (uint32_t)kCmTile | ((uint32_t)kCmWin << 13) | (1u << 27);
+__device__ __forceinline__ uint32_t geo_payload(uint32_t g) { return g & 0x1FFFu; }
+__device__ __forceinline__ uint32_t geo_hibits(uint32_t g) { return (g >> 13) & 0x1FFFu; }
+__device__ __forceinline__ bool geo_start(uint32_t g) { return (g >> 26) & 1u; }
+__device__ __forceinline__ bool geo_cont(uint32_t g) { return (g >> 27) & 1u; }
+
+// Issue the copy of the producer iterator's tile into stage `dst` (shared-window address) and
+// return its packed geometry.  Full tiles: one constant-size copy.  Segment heads / tails: the
+// 16 B-multiple part by the TMA engine, the < 16 B remainder by lane 0 right here (the stage is
+// free, the bytes are disjoint from the bulk copy's, and the warp synchronises before it reads
+// the stage again).
+__device__ __forceinline__ uint32_t cm_issue(const TileIter& it, uint32_t dst, uint32_t bar, int lane) {
+  if (it.full()) {
+    if (lane == 0) issue_s(dst, it.seg + it.off - kCmHaloL, kCmStage, bar);
+    return kGeoFull;
+  }
+  const TileGeom g = it.geom();
+  const uint32_t bulk = (g.hi - g.lo) & ~15u;
+  if (lane == 0) {
+    if (bulk) issue_s(dst + g.lo, g.seg + g.off - kCmHaloL + g.lo, bulk, bar);
+    else asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(0u) : "memory");
+    for (uint32_t i = g.lo + bulk; i < g.hi; i++)
+      asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + i), "r"((uint32_t)g.seg[g.off - kCmHaloL + i]));
+  }
+  return g.payload | ((g.hi - kCmHaloL) << 13) | ((g.lo != 0 ? 1u : 0u) << 26) | ((g.cont ? 1u : 0u) << 27);
 }
 
 template <int KIND>
@@ -528,10 +569,14 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   __shared__ unsigned long long slot_tag[2];
   // per-warp '\n' / ',' masks of the warp's current window (+ zero words for reads past it)
   __shared__ __align__(16) uint32_t nlm[kWarps][kMaskW32 + 8], cmm[kWarps][kMaskW32 + 8];
-  // CM2: per-warp survivor lists; CM1: per-warp accumulators [warp][slot][cat]
-  __shared__ unsigned long long sv_job[kCM2 ? kWarps : 1][kSurvCap];
-  __shared__ uint32_t sv_m[kCM2 ? kWarps : 1][kSurvCap], sv_p[kCM2 ? kWarps : 1][kSurvCap];
-  __shared__ unsigned long long w_sum[kCM2 ? 1 : kWarps][2][10], w_cnt[kCM2 ? 1 : kWarps][2][10];
+  // (static + dynamic shared memory must stay <= 233472 / 5 - 1024 B per CTA: 5 CTAs per SM)
+  // CM2: per-warp survivor rings (jobId / cpu digit words, pane); CM1: per-warp accumulators
+  constexpr int kSv = kCM2 ? kWarps : 1;
+  __shared__ uint32_t sv_j0[kSv][kSurvCap], sv_j1[kSv][kSurvCap];   // jobId digits 0-7 (+ 8-9)
+  __shared__ uint32_t sv_c0[kSv][kSurvCap], sv_c1[kSv][kSurvCap], sv_p[kSv][kSurvCap];
+  __shared__ unsigned long long w_sum[kCM2 ? 1 : kWarps][kCM2 ? 1 : 2][kCM2 ? 1 : 10];
+  __shared__ unsigned long long w_cnt[kCM2 ? 1 : kWarps][kCM2 ? 1 : 2][kCM2 ? 1 : 10];
+  static_assert(sizeof(nlm) >= 1280, "flush_counters scratch");
 
   const QueryDev& q = a.q;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -544,7 +589,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   uint32_t* const cm32 = cmm[warp];
 
   if (!kCM2)
-    for (int i = tid; i < kWarps * 20; i += blockDim.x) {
+    for (int i = tid; i < (int)(sizeof(w_sum) / 8); i += blockDim.x) {
       (&w_sum[0][0][0])[i] = 0;
       (&w_cnt[0][0][0])[i] = 0;
     }
@@ -556,63 +601,67 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   }
   __syncthreads();
   const uint32_t ntiles = (uint32_t)(t1 - t0);
-  TileIter cur, iss;                           // consumer / producer (2 tiles ahead)
-  cur.init(a.segs, t0);
+  const uint32_t nl_s = smem_addr(nl32), cm_s = smem_addr(cm32);
+  const uint32_t full_s = smem_addr(&full[warp][0]), stage_s = smem_addr(wsmem);
+  TileIter iss;                                // producer: the next tile to issue
   iss.init(a.segs, t0);
-  for (uint32_t s = 0; s < (uint32_t)kCmStages && s < ntiles; s++) {
-    if (lane == 0) cm_issue_it(iss, smem_addr(wsmem + s * kCmStage), smem_addr(&full[warp][s]));
-    iss.next(a.segs);
-  }
+  uint32_t geo0 = 0, geo1 = 0;                 // packed geometry of the tiles in stages 0 / 1
+  if (ntiles > 0) { geo0 = cm_issue(iss, stage_s, full_s, lane); iss.next(a.segs); }
+  if (ntiles > 1) { geo1 = cm_issue(iss, stage_s + kCmStage, full_s + 8u, lane); iss.next(a.segs); }
 
   const unsigned long long wm_prev = q.state->wm_prev;
   const uint32_t k7f = a.k7f, k256 = a.k256, k512 = a.k512;    // runtime constants (see eq_flags)
   const uint32_t wm32 = (uint32_t)min(wm_prev, 0xFFFFFFFFull);  // late iff ts + 1 < wm_prev (ts < 1e9)
   uint32_t n_rec = 0, n_bad = 0, n_late = 0, n_ovf = 0, ts_min = kEmpty32, ts_max1 = 0;
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
-  uint32_t sv_n = 0;                                            // CM2 survivors in my warp's list
-  const uint32_t nl_s = smem_addr(nl32), cm_s = smem_addr(cm32);
-  const uint32_t full_s = smem_addr(&full[warp][0]), stage_s = smem_addr(wsmem);
+  unsigned long long* c_sum = nullptr;                          // CM2: the cached pane's stripe
+  unsigned long long* c_cnt = nullptr;
+  uint32_t sv_h = 0, sv_n = 0;                                  // CM2 survivor ring: head, entries
   uint32_t pc_lo = 0, pc_p = 0;                                 // cached pane [pc_lo, pc_lo + S)
 
-  // CM2: process entries [0, n) of the warp's survivor list with the warp's lanes
+  // CM2: decode and aggregate ring entries [sv_h, sv_h + n) with the warp's lanes
   auto drain = [&](uint32_t n) {
     __syncwarp();
     if ((uint32_t)lane < n) {
-      const uint32_t pp = sv_p[kCM2 ? warp : 0][lane];
-      if (pp != c_pane) { c_pane = pp; c_gslot = claim_slot(q, pp); }
-      const uint32_t idx = c_gslot != kFail32 ? dict_get(q.dict, sv_job[kCM2 ? warp : 0][lane], q.state) : kEmpty32;
+      const uint32_t i = (sv_h + lane) & (kSurvCap - 1);
+      const uint32_t w = kCM2 ? warp : 0;
+      const uint32_t pp = sv_p[w][i], c1 = sv_c1[w][i];
+      const uint32_t j0 = sv_j0[w][i];   // fast path: digits 8, 9 in the high nibbles of bytes 0, 1
+      const bool raw = c1 == kRawValues;
+      const unsigned long long job = cm_job_value(raw ? j0 : (j0 & 0x0F0F0F0Fu), sv_j1[w][i], (j0 >> 4) & 0x0F0Fu, c1);
+      const uint32_t m = cm_cpu_value(sv_c0[w][i], c1);
+      if (pp != c_pane) {
+        c_pane = pp;
+        c_gslot = claim_slot(q, pp);
+        const size_t base = ((size_t)c_gslot * q.stripes + (blockIdx.x & (q.stripes - 1u))) * q.K;
+        c_sum = q.acc_sum + base;
+        c_cnt = q.acc_cnt + base;
+      }
+      const uint32_t idx = c_gslot != kFail32 ? dict_get(q.dict, job, q.state) : kEmpty32;
       if (idx == kEmpty32) n_ovf++;
       else {
-        const size_t gi = ((size_t)c_gslot * q.stripes + (blockIdx.x & (q.stripes - 1u))) * q.K + idx;
-        atomicAdd(&q.acc_sum[gi], (unsigned long long)sv_m[kCM2 ? warp : 0][lane]);
-        atomicAdd(&q.acc_cnt[gi], 1ull);
+        atomicAdd(c_sum + idx, (unsigned long long)m);
+        atomicAdd(c_cnt + idx, 1ull);
       }
     }
+    sv_h = (sv_h + n) & (kSurvCap - 1);
     __syncwarp();
   };
 
   bool fresh = true;              // window bits [0, 256) not inherited from the previous tile
   uint32_t carry_nl = 0;          // the previous tile's last payload byte is a '\n' (when !fresh)
   for (uint32_t it = 0; it < ntiles; it++) {
-    const int s = (int)(it % kCmStages);
-    const uint32_t ph = (it / kCmStages) & 1u;
-    uint8_t* buf = wsmem + s * kCmStage;
-    const TileGeom g = cur.geom();
-    cur.next(a.segs);
-    if (lane == 0) mbar_wait_s(full_s + 8u * s, ph);
-    __syncwarp();
-    {   // remainder bytes the bulk copy could not move (segment tail, < 16 B)
-      const uint32_t bulk_end = g.lo + ((g.hi - g.lo) & ~15u);
-      if (bulk_end < g.hi) {
-        if ((uint32_t)lane < g.hi - bulk_end) buf[bulk_end + lane] = g.seg[g.off - kCmHaloL + bulk_end + lane];
-        __syncwarp();
-      }
-    }
-    const uint32_t hi_bits = g.hi - kCmHaloL;                  // mask bits beyond are invalid
+    const uint32_t s = it & 1u;                                 // kCmStages == 2
+    const uint32_t ph = (it >> 1) & 1u;
+    const uint32_t geo = s ? geo1 : geo0;
+    const uint32_t st_s = stage_s + s * (uint32_t)kCmStage;    // stage base (shared window)
+    const uint8_t* buf = wsmem + s * kCmStage;
+    mbar_wait_s(full_s + 8u * s, ph);                           // every lane: TMA bytes visible
+    const uint32_t hi_bits = geo_hibits(geo);                   // mask bits beyond are invalid
     // ---- Pass 1: exact '\n' / ',' masks, one 32-bit mask word (32 B) per lane per step.
     // Window bits [0, 256) are the previous tile's halo masks when the tile continues the
     // segment (carried below), so a tile classifies 4096 new bytes: 4 words per lane.
-    const uint32_t buf_s = stage_s + s * kCmStage + kCmHaloL;
+    const uint32_t buf_s = st_s + kCmHaloL;
     auto mword = [&](int wi) {
       const uint4 va = lds128(buf_s + 32 * wi), vb = lds128(buf_s + 32 * wi + 16);
       const uint32_t na = gather16x128(eq_flags(va.x, k7f, 0x0A0A0A0Au), eq_flags(va.y, k7f, 0x0A0A0A0Au),
@@ -628,7 +677,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     };
 #pragma unroll
     for (int k = 0; k < 4; k++) mword(8 + lane + 32 * k);
-    fresh = fresh || g.lo != 0;
+    fresh = fresh || geo_start(geo);
     if (fresh && lane < 8) mword(lane);
     __syncwarp();
     if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (warp-uniform): clear stale bits
@@ -655,9 +704,9 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     // Records are owned by the '\n' before them: lane l takes the record after each '\n' of
     // its chunk (if it starts inside the payload); lane 0 also takes the record at payload byte
     // 0 when the tile starts a segment or the byte before it is a '\n'.
-    const bool start0 = lane == 0 && (g.lo != 0 || (fresh ? buf[kCmHaloL - 1] == '\n' : carry_nl != 0));
+    const bool start0 = lane == 0 && (geo_start(geo) || (fresh ? buf[kCmHaloL - 1] == '\n' : carry_nl != 0));
     carry_nl = __shfl_sync(0xffffffffu, nw.w, 31) >> 31;       // last payload byte, for the next tile
-    const uint32_t pay = g.payload;
+    const uint32_t pay = geo_payload(geo);
     uint32_t n0 = nw.x, n1 = nw.y, n2 = nw.z, n3 = nw.w;             // unconsumed newlines (generic lanes)
     const uint32_t cnt_nl = __popc(n0) + __popc(n1) + __popc(n2) + __popc(n3);
     // round 0 serves the usual lane: at most one '\n' in the chunk, no record at byte 0 (records
@@ -673,13 +722,19 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       n_rec += have ? 1u : 0u;
       sb = sel(have, sb, 0u);
       // usual-shape records: branch-free fast path; anything else: the exact general path
-      const bool fast = cm_fast(buf, cm32, sb, e, r) & have;
+      const bool fast = cm_fast<kCM2>(buf, cm32, sb, e, r) & have;
       const bool slow = have & !fast;
       bool ok = fast;
       if (__any_sync(0xffffffffu, slow)) {
         if (slow) {
           const int st = e == 0xFFFFu ? 2 : cm_parse(buf, cm32, sb, e, hi_bits, r);
-          ok = st == 2 ? cm_parse_serial(buf, kCmHaloL + sb, g.hi, r) : st != 0;
+          ok = st == 2 ? cm_parse_serial(buf, kCmHaloL + sb, hi_bits + kCmHaloL, r) : st != 0;
+          if (kCM2) {                  // values, not digit words (cm_job_value / cm_cpu_value)
+            r.jw0 = (uint32_t)r.job;
+            r.jw1 = (uint32_t)(r.job >> 32);
+            r.cw0 = r.cpu_m;
+            r.cw1 = kRawValues;
+          }
         }
       }
       {   // drop malformed (counted) and late (ts < W_prev, counted) records
@@ -696,24 +751,20 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
       const uint32_t p = surv ? pc_p : 0;
       if (kCM2) {
-        // warp-ballot stream compaction into the warp's survivor list
+        // warp-ballot stream compaction into the warp's survivor ring
         const uint32_t bal = __ballot_sync(0xffffffffu, surv);
         if (surv) {
-          const uint32_t pos = sv_n + __popc(bal & ((1u << lane) - 1u));
-          sv_job[warp][pos] = r.job;
-          sv_m[warp][pos] = r.cpu_m;
+          const uint32_t pos = (sv_h + sv_n + __popc(bal & ((1u << lane) - 1u))) & (kSurvCap - 1);
+          sv_j0[warp][pos] = r.cw1 == kRawValues ? r.jw0 : (r.jw0 | ((r.jw2 << 4) & 0xF0F0u));
+          sv_j1[warp][pos] = r.jw1;
+          sv_c0[warp][pos] = r.cw0;
+          sv_c1[warp][pos] = r.cw1;
           sv_p[warp][pos] = p;
         }
         sv_n += __popc(bal);
         if (sv_n >= 32) {
           drain(32);
-          if (sv_n > 32 && (uint32_t)lane < sv_n - 32) {        // move the remainder down
-            sv_job[warp][lane] = sv_job[warp][32 + lane];
-            sv_m[warp][lane] = sv_m[warp][32 + lane];
-            sv_p[warp][lane] = sv_p[warp][32 + lane];
-          }
           sv_n -= 32;
-          __syncwarp();
         }
       } else {
         // CM1: reduce per (pane, category) inside the warp
@@ -796,14 +847,19 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
     }
     __syncwarp();      // stage s and the masks consumed by every lane
-    fresh = !g.cont;
-    if (g.cont && lane < 8) {                   // halo masks = the next tile's window bits [0, 256)
+    fresh = !geo_cont(geo);
+    if (!fresh && lane < 8) {                   // halo masks = the next tile's window bits [0, 256)
       sts32(nl_s + 4 * lane, lds32(nl_s + 4 * (kChunks * 4 + lane)));
       sts32(cm_s + 4 * lane, lds32(cm_s + 4 * (kChunks * 4 + lane)));
     }
+    // lanes 24..31 write mask words 128..135 in the next tile's pass 1 (each lane leaves the
+    // barrier wait on its own): the halo reads above must be done first
+    __syncwarp();
     if (it + kCmStages < ntiles) {
-      if (lane == 0) cm_issue_it(iss, stage_s + s * kCmStage, full_s + 8u * s);
+      const uint32_t g2 = cm_issue(iss, st_s, full_s + 8u * s, lane);
       iss.next(a.segs);
+      geo0 = s ? geo0 : g2;
+      geo1 = s ? g2 : geo1;
     }
   }
 
@@ -825,7 +881,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       }
     }
   }
-  flush_counters(CtaCounters{n_rec, n_bad, n_late, n_ovf, ts_min, ts_max1}, q.state);
+  flush_counters(CtaCounters{n_rec, n_bad, n_late, n_ovf, ts_min, ts_max1}, q.state, &nlm[0][0]);
 }
 
 }  // namespace

@@ -8,14 +8,15 @@ stream), runs one batch (lms_force_batch + lms_sync) and reads its lms_batch_rec
   h2d_s     PCIe copy of the batch (CUDA events on the copy stream)
   device_s  the batch's kernels (CUDA events)
   proc_s    Proc_i (reading R18: device + result D2H)
-Reported per size (median of `reps` batches): those three, the PCIe share h2d / (h2d + proc)
-(the quantity of the paper's Fig. 2), and a two-point model  t(bytes) = a + bytes / bw  of each
+Reported per size (median of `reps` batches): those three, the PCIe share h2d / proc (Proc
+contains the H2D: the batch's kernels wait for the copy on the device; the quantity of the
+paper's Fig. 2), and a two-point model  t(bytes) = a + bytes / bw  of each
 component (a from the smallest batch, bw from the largest).
 
 Derived constants (readings R29 / R30 of DESIGN.md):
   InfPT_0  (Alg. 2's Part at which GPU and CPU costs are equal, Eq. 7-8): on the GPU side the
-           knee of the measured cost curve — the batch size at which the size-proportional time
-           (h2d + device) equals the fixed per-batch overhead a — divided by NumCores (12,
+           knee of the measured cost curve — the batch size at which the size-proportional part
+           of Proc equals its fixed per-batch part a — divided by NumCores (12,
            Part = batch bytes / NumCores).  Below it the batch is overhead-bound ("PCIe
            overhead marginal for small data"), above it time grows with bytes.
   baseTransCost  (Eq. 9: Trans = btc * Part / InfPT, so btc = Trans at Part = InfPT relative to
@@ -78,7 +79,7 @@ def sweep(kind, family, reps):
                 meas["wall_s"].append(wall)
         med = {k: statistics.median(v) for k, v in meas.items()}
         med.update(records=n_rec, bytes=nb,
-                   pcie_share=med["h2d_s"] / (med["h2d_s"] + med["proc_s"]))
+                   pcie_share=med["h2d_s"] / med["proc_s"])
         rows.append(med)
         print(f"{kind} {n_rec:>9} rec {nb / 1e6:10.3f} MB  h2d {med['h2d_s'] * 1e3:8.3f} ms  device "
               f"{med['device_s'] * 1e3:8.3f} ms  proc {med['proc_s'] * 1e3:8.3f} ms  wall "
@@ -89,7 +90,9 @@ def sweep(kind, family, reps):
 
 def derive(rows, num_cores=12):
     """Two-point model per component: the fixed part a = its time at the smallest batch (where
-    the size-proportional part is negligible), the per-byte slope from the largest batch."""
+    the size-proportional part is negligible), the per-byte slope from the largest batch.
+    Proc_i of a pinned push already contains its H2D (the batch's kernels wait for the copy on
+    the device; reading R18), so Proc is the end-to-end cost of a batch."""
     lo, hi = rows[0], rows[-1]
 
     def model(key):
@@ -98,15 +101,13 @@ def derive(rows, num_cores=12):
     a_h, b_h = model("h2d_s")
     a_d, b_d = model("device_s")
     a_p, b_p = model("proc_s")
-    a = a_h + a_p                                        # fixed per-batch overhead (H2D + Proc)
-    per_byte = b_h + b_p
-    knee = a / per_byte                                  # bytes at which a == bytes * per_byte
+    knee = a_p / b_p                                     # bytes at which a == bytes * per_byte
     h2d_knee = a_h + b_h * knee                          # H2D / device time at the knee
     dev_knee = a_d + b_d * knee
     return {
         "model": {"h2d": {"a_s": a_h, "GBps": 1e-9 / b_h}, "device": {"a_s": a_d, "GBps": 1e-9 / b_d},
                   "proc": {"a_s": a_p, "GBps": 1e-9 / b_p}},
-        "fixed_overhead_s": a,
+        "fixed_overhead_s": a_p,
         "knee_batch_bytes": knee,
         "inf_pt_bytes": knee / num_cores,
         "base_trans_cost": h2d_knee / dev_knee,
@@ -118,7 +119,17 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=7)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "calibration.json"))
+    ap.add_argument("--rederive", default=None, help="recompute 'derived' of an existing calibration file")
     args = ap.parse_args()
+    if args.rederive:
+        out = json.load(open(args.rederive))
+        for k in ("LR2S", "CM2S"):
+            for r in out[k]["sweep"]:
+                r["pcie_share"] = r["h2d_s"] / r["proc_s"]
+            out[k]["derived"] = derive(out[k]["sweep"])
+        json.dump(out, open(args.out, "w"), indent=1)
+        print(json.dumps({k: out[k]["derived"] for k in ("LR2S", "CM2S")}, indent=1))
+        return
     import torch
     out = {"gpu": torch.cuda.get_device_name(0), "reps": args.reps,
            "method": "lms_push_pinned + lms_force_batch + lms_sync per batch; medians; see module doc"}

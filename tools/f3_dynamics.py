@@ -7,7 +7,7 @@ traffic, 90 virtual minutes each, one dataset per second.  T
 Spark on an RTX 2080 Ti at 2.5k records/s; a B200 at those rates finishes a batch in
 microseconds, so the rates are SCALED so that the mean offered load is a fixed fraction
 (`--load`, default 0.5 and 0.9) of the B200's end-to-end capacity for that record type (the
-calibrated H2D + Proc bandwidth of tools/calibrate_b200.py), keeping the traffic's shape
+calibrated Proc bandwidth of a pinned push, H2D included, tools/calibrate_b200.py), keeping the traffic's shape
 (U: normal, sigma = mu/4; R: uniform over [0.1, 5] x scale).  Admission is the library's own
 Alg. 1 decision (lms_admit_decision, the function lms_poll calls; CG(dN) = sliding branch with
 SlideTime := N, reading R16) and OS(tN) admits everything buffered every N s; Proc of a batch
@@ -106,8 +106,8 @@ def part_a(calib, loads, minutes):
     out = []
     for fam, rec_b, ck in (("LR1", LR_BYTES, "LR2S"), ("CM1", CM_BYTES, "CM2S")):
         dm = calib[ck]["derived"]["model"]
-        a = dm["h2d"]["a_s"] + dm["proc"]["a_s"]
-        bw = 1.0 / (1.0 / (dm["h2d"]["GBps"] * 1e9) + 1.0 / (dm["proc"]["GBps"] * 1e9))   # e2e B/s
+        a = dm["proc"]["a_s"]                      # Proc of a pinned push contains its H2D
+        bw = dm["proc"]["GBps"] * 1e9                 # end-to-end bytes/s
         cap_rps = bw / rec_b
         for shape in ("U(2.5)", "R(0.1,5)"):
             base = g.Traffic.parse(shape)
@@ -142,7 +142,7 @@ def part_b(minutes, traffic):
     res = {}
     for kind in ("LR1S", "LR1T"):
         for name, over in (("LMStream", dict(mode="lmstream")), ("Baseline OS(t10)", dict(mode="trigger", trigger_s=10.0))):
-            with P.Query(kind, max_batch_bytes=1 << 30, **over) as q:
+            with P.Query(kind, max_batch_bytes=1 << 30, max_result_rows=1 << 24, **over) as q:
                 src = LC.Source(q, "LR", traffic, int(minutes * 60), 1, 211104289)
                 LC.run_stream([src], minutes * 60.0)
                 recs = src.recs
