@@ -450,8 +450,9 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   const uint32_t sh = sb & 31u;
   const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4];
   const uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
-  const uint32_t m0 = __funnelshift_r(v2, v3, sh) & low_bits(min(L - 128u, 32u));
-  const uint32_t m1 = __funnelshift_r(v3, v4, sh) & low_bits(clamp32((int)L - 160));
+  const unsigned long long mid = (((unsigned long long)__funnelshift_r(v3, v4, sh) << 32) | __funnelshift_r(v2, v3, sh)) &
+                                 ((1ull << min(L - 128u, 63u)) - 1ull);          // bits [sb+64, e-64)
+  const uint32_t m0 = (uint32_t)mid, m1 = (uint32_t)(mid >> 32);
   // e clamped into the window for addressing only (e = 0xFFFF: no '\n' in reach; L above
   // already rejects it): with S <= 16 + 4096 and o0, a4, q7 < 35 every load below stays
   // inside the stage, so no address needs its own clamp
@@ -480,13 +481,15 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   ok &= pc == 0x0Au || pc == 0x05u;
   const uint32_t cat_at = kCmHaloL + ec - (pc == 0x0Au ? 32u : 33u);  // c6 + 1
   // ---- fields (digit checks accumulate into bad; bit 7 of a byte = not a digit)
-  // ts: the 8 bytes ending at c0; the (8 - o0) bytes before the digits become '0'
+  // ts: bytes [S, S + 8) hold its o0 digits, then ','.  '0' is subtracted from all 8 bytes as one
+  // 64-bit subtraction (borrows only run toward later bytes, i.e. past the digits; a non-digit
+  // byte among the digits is caught below), then the digit values are shifted to the top of the
+  // word: the bytes after them fall off, zero bytes (leading zeros) come in below.
   uint32_t a0, a1;
-  load8(buf, S + o0 - 8u, a0, a1);
-  const unsigned long long pm = (~0ull >> (min(max(8u * o0, 8u), 64u) - 1u)) >> 1;   // ~0 >> 8*o0
-  const uint32_t pm0 = (uint32_t)pm, pm1 = (uint32_t)(pm >> 32);
-  const uint32_t da0 = ((a0 & ~pm0) | (0x30303030u & pm0)) - 0x30303030u;
-  const uint32_t da1 = ((a1 & ~pm1) | (0x30303030u & pm1)) - 0x30303030u;
+  load8(buf, S, a0, a1);
+  const unsigned long long ta = (((unsigned long long)a1 << 32) | a0) - 0x3030303030303030ull;
+  const unsigned long long tv = ta << (8u * ((8u - o0) & 7u));
+  const uint32_t da0 = (uint32_t)tv, da1 = (uint32_t)(tv >> 32);
   uint32_t bad = dbad(da0) | dbad(da1);
   r.ts = swar4d(da0) * 10000u + swar4d(da1);
   // jobId: 10 digits at c1 + 1 = S + o0 + 2
@@ -572,8 +575,10 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   // (static + dynamic shared memory must stay <= 233472 / 5 - 1024 B per CTA: 5 CTAs per SM)
   // CM2: per-warp survivor rings (jobId / cpu digit words, pane); CM1: per-warp accumulators
   constexpr int kSv = kCM2 ? kWarps : 1;
-  __shared__ uint32_t sv_j0[kSv][kSurvCap], sv_j1[kSv][kSurvCap];   // jobId digits 0-7 (+ 8-9)
-  __shared__ uint32_t sv_c0[kSv][kSurvCap], sv_c1[kSv][kSurvCap], sv_p[kSv][kSurvCap];
+  // {jobId digits 0-3, 4-7 (+ 8, 9 in the high nibbles of bytes 0, 1 of the first word), cpu
+  // words}: one 16 B store / load per survivor
+  __shared__ uint4 sv_e[kSv][kSurvCap];
+  __shared__ uint32_t sv_p[kSv][kSurvCap];
   __shared__ unsigned long long w_sum[kCM2 ? 1 : kWarps][kCM2 ? 1 : 2][kCM2 ? 1 : 10];
   __shared__ unsigned long long w_cnt[kCM2 ? 1 : kWarps][kCM2 ? 1 : 2][kCM2 ? 1 : 10];
   static_assert(sizeof(nlm) >= 1280, "flush_counters scratch");
@@ -625,11 +630,11 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     if ((uint32_t)lane < n) {
       const uint32_t i = (sv_h + lane) & (kSurvCap - 1);
       const uint32_t w = kCM2 ? warp : 0;
-      const uint32_t pp = sv_p[w][i], c1 = sv_c1[w][i];
-      const uint32_t j0 = sv_j0[w][i];   // fast path: digits 8, 9 in the high nibbles of bytes 0, 1
-      const bool raw = c1 == kRawValues;
-      const unsigned long long job = cm_job_value(raw ? j0 : (j0 & 0x0F0F0F0Fu), sv_j1[w][i], (j0 >> 4) & 0x0F0Fu, c1);
-      const uint32_t m = cm_cpu_value(sv_c0[w][i], c1);
+      const uint32_t pp = sv_p[w][i];
+      const uint4 ev = sv_e[w][i];
+      const bool raw = ev.w == kRawValues;
+      const unsigned long long job = cm_job_value(raw ? ev.x : (ev.x & 0x0F0F0F0Fu), ev.y, (ev.x >> 4) & 0x0F0Fu, ev.w);
+      const uint32_t m = cm_cpu_value(ev.z, ev.w);
       if (pp != c_pane) {
         c_pane = pp;
         c_gslot = claim_slot(q, pp);
@@ -649,7 +654,8 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   };
 
   bool fresh = true;              // window bits [0, 256) not inherited from the previous tile
-  uint32_t carry_nl = 0;          // the previous tile's last payload byte is a '\n' (when !fresh)
+  uint32_t carry_nl = 0;          // a record starts at the tile's payload byte 0 (the previous
+                                  // tile's last payload byte is a '\n', or a segment start)
   for (uint32_t it = 0; it < ntiles; it++) {
     const uint32_t s = it & 1u;                                 // kCmStages == 2
     const uint32_t ph = (it >> 1) & 1u;
@@ -678,7 +684,11 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
 #pragma unroll
     for (int k = 0; k < 4; k++) mword(8 + lane + 32 * k);
     fresh = fresh || geo_start(geo);
-    if (fresh && lane < 8) mword(lane);
+    if (fresh) {                                 // (warp-uniform)
+      if (lane < 8) mword(lane);
+      // a record starts at payload byte 0 iff the tile starts its segment or follows a '\n'
+      carry_nl = geo_start(geo) || buf[kCmHaloL - 1] == '\n';
+    }
     __syncwarp();
     if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (warp-uniform): clear stale bits
       for (uint32_t wi = lane; wi < (uint32_t)kMaskW32; wi += 32) {
@@ -704,7 +714,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     // Records are owned by the '\n' before them: lane l takes the record after each '\n' of
     // its chunk (if it starts inside the payload); lane 0 also takes the record at payload byte
     // 0 when the tile starts a segment or the byte before it is a '\n'.
-    const bool start0 = lane == 0 && (geo_start(geo) || (fresh ? buf[kCmHaloL - 1] == '\n' : carry_nl != 0));
+    const bool start0 = lane == 0 && carry_nl != 0;
     carry_nl = __shfl_sync(0xffffffffu, nw.w, 31) >> 31;       // last payload byte, for the next tile
     const uint32_t pay = geo_payload(geo);
     uint32_t n0 = nw.x, n1 = nw.y, n2 = nw.z, n3 = nw.w;             // unconsumed newlines (generic lanes)
@@ -732,6 +742,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
           if (kCM2) {                  // values, not digit words (cm_job_value / cm_cpu_value)
             r.jw0 = (uint32_t)r.job;
             r.jw1 = (uint32_t)(r.job >> 32);
+            r.jw2 = 0;
             r.cw0 = r.cpu_m;
             r.cw1 = kRawValues;
           }
@@ -755,10 +766,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
         const uint32_t bal = __ballot_sync(0xffffffffu, surv);
         if (surv) {
           const uint32_t pos = (sv_h + sv_n + __popc(bal & ((1u << lane) - 1u))) & (kSurvCap - 1);
-          sv_j0[warp][pos] = r.cw1 == kRawValues ? r.jw0 : (r.jw0 | ((r.jw2 << 4) & 0xF0F0u));
-          sv_j1[warp][pos] = r.jw1;
-          sv_c0[warp][pos] = r.cw0;
-          sv_c1[warp][pos] = r.cw1;
+          sv_e[warp][pos] = make_uint4(r.jw0 | ((r.jw2 << 4) & 0xF0F0u), r.jw1, r.cw0, r.cw1);
           sv_p[warp][pos] = p;
         }
         sv_n += __popc(bal);

@@ -15,6 +15,10 @@ comes from the B200 model  Proc(bytes) = a + bytes / bw  fitted on this GPU (cal
 file), the 10 ms poll of P:564 and one batch in flight.  A dataset violates the deadline when
 completion - ingest > d (P:208-210: #violation / #total datasets).
 
+A sensitivity run repeats Part A with a fixed per-batch overhead of `--fixed-a` seconds (a
+Spark-like micro-batch cost; the B200's is ~35 us): it shows the regime in which the paper's
+OS(t3) runaway appears (small batches spend most of their time in overhead).
+
 Part B — timelines (Fig. "Timeline during the initial 20-minute run of LR1S / LR1T",
 P:1002-1028): LMStream (Alg. 1) against the paper's Baseline (Spark's fixed 10 s trigger,
 "always performs ten seconds of buffering", P:1019 = OS(t10)) on R(L,U) traffic, run for real
@@ -101,12 +105,14 @@ def simulate(counts, rec_bytes, proc_model, system, d, t_end):
     return lat, batches
 
 
-def part_a(calib, loads, minutes):
+def part_a(calib, loads, minutes, fixed_s=None):
+    """fixed_s: override the calibrated fixed per-batch overhead (sensitivity: a Spark-like
+    per-micro-batch cost instead of the B200's tens of microseconds)."""
     import lmsgen as g
     out = []
     for fam, rec_b, ck in (("LR1", LR_BYTES, "LR2S"), ("CM1", CM_BYTES, "CM2S")):
         dm = calib[ck]["derived"]["model"]
-        a = dm["proc"]["a_s"]                      # Proc of a pinned push contains its H2D
+        a = dm["proc"]["a_s"] if fixed_s is None else fixed_s   # Proc of a pinned push contains its H2D
         bw = dm["proc"]["GBps"] * 1e9                 # end-to-end bytes/s
         cap_rps = bw / rec_b
         for shape in ("U(2.5)", "R(0.1,5)"):
@@ -121,7 +127,7 @@ def part_a(calib, loads, minutes):
                 secs = int(minutes * 60)
                 counts = [tr.count(t) for t in range(secs)]
                 for d in (5.0, 7.0):
-                    row = {"workload": f"{fam}-{shape}", "load": load, "scale": k, "deadline_s": d,
+                    row = {"workload": f"{fam}-{shape}", "load": load, "scale": k, "deadline_s": d, "fixed_s": a,
                            "mean_rec_per_s": sum(counts) / secs, "capacity_rec_per_s": cap_rps}
                     for name, system in (("OS(t3)", ("OS", 3.0)), (f"CG(d{int(d)})", ("CG", d))):
                         lat, bat = simulate(counts, rec_b, (a, bw), system, d, secs + 30.0)
@@ -163,6 +169,9 @@ def main():
     ap.add_argument("--part", default="AB")
     ap.add_argument("--loads", default="0.5,0.9")
     ap.add_argument("--minutes-a", type=float, default=90.0)
+    ap.add_argument("--fixed-a", type=float, default=1.0,
+                    help="sensitivity run with this fixed per-batch overhead [s] (0: skip)")
+    ap.add_argument("--loads-fixed", default="0.5,0.7")
     ap.add_argument("--minutes-b", type=float, default=20.0)
     ap.add_argument("--traffic-b", default="R(50,500)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "f3_dynamics.json"))
@@ -171,6 +180,9 @@ def main():
     if "A" in args.part:
         calib = json.load(open(args.calib))
         out["violation"] = part_a(calib, [float(x) for x in args.loads.split(",")], args.minutes_a)
+        if args.fixed_a > 0:
+            out["violation_fixed_overhead"] = part_a(calib, [float(x) for x in args.loads_fixed.split(",")],
+                                                     args.minutes_a, fixed_s=args.fixed_a)
         out["calibration"] = {k: calib[k]["derived"] for k in ("LR2S", "CM2S")}
     if "B" in args.part:
         out["timeline"] = part_b(args.minutes_b, args.traffic_b)
