@@ -107,7 +107,24 @@ struct CmArgs {
   SegTable segs;
   unsigned long long total_tiles;
   uint32_t k7f, k256, k512;          // 0x7F7F7F7F, 256, 512: kernel arguments, so they stay in registers
+  uint32_t pane_m, pane_sh;          // pane30: floor(ts / S) = umulhi(ts, pane_m) >> pane_sh
 };
+
+// floor(ts / S) for ts < 2^30 (every CM timestamp: <= 9 digits) with a 32-bit magic number:
+// k = max(32, 30 + ceil(log2 S)), M = ceil(2^k / S) < 2^31 + 1, shift k - 32.  Exact: ts * M / 2^k
+// = ts / S + ts * err / 2^k with 0 <= err < 1, and ts / 2^k < 2^30 / 2^k <= 1 / S, so the error
+// never reaches the next multiple of 1 / S.  S = 1: M = 0, the identity (pane_sh = 32 marks it).
+__device__ __forceinline__ uint32_t pane30(uint32_t ts, uint32_t m, uint32_t sh) {
+  return sh == 32u ? ts : (__umulhi(ts, m) >> sh);
+}
+void pane30_magic(uint32_t S, uint32_t& m, uint32_t& sh) {
+  if (S <= 1) { m = 0; sh = 32; return; }
+  uint32_t lg = 0;
+  while ((1ull << lg) < S) lg++;
+  const uint32_t k = lg + 30 > 32 ? lg + 30 : 32;
+  m = (uint32_t)(((1ull << k) + S - 1) / S);
+  sh = k - 32;
+}
 
 struct TileGeom {
   const uint8_t* seg;
@@ -409,6 +426,27 @@ __device__ __forceinline__ int cm_parse(const uint8_t* buf, const uint32_t* cm32
   return cm_fields(buf, S, c, r) ? 1 : 0;
 }
 
+// Shared-window (32-bit address) forms for the fast path: no 64-bit generic address math.
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+// Bytes [a, a+8) / [a, a+12) of shared memory at any alignment (reads the aligned words).
+__device__ __forceinline__ void lds8u(uint32_t a, uint32_t& d0, uint32_t& d1) {
+  const uint32_t b = a & ~3u, sh = (a & 3u) * 8u;
+  const uint32_t w0 = lds32(b), w1 = lds32(b + 4), w2 = lds32(b + 8);
+  d0 = __funnelshift_r(w0, w1, sh);
+  d1 = __funnelshift_r(w1, w2, sh);
+}
+__device__ __forceinline__ void lds12u(uint32_t a, uint32_t& d0, uint32_t& d1, uint32_t& d2) {
+  const uint32_t b = a & ~3u, sh = (a & 3u) * 8u;
+  const uint32_t w0 = lds32(b), w1 = lds32(b + 4), w2 = lds32(b + 8), w3 = lds32(b + 12);
+  d0 = __funnelshift_r(w0, w1, sh);
+  d1 = __funnelshift_r(w1, w2, sh);
+  d2 = __funnelshift_r(w2, w3, sh);
+}
+
 // Bytes [p, p+8) of smem as two little-endian words (p arbitrary; reads 12 aligned bytes).
 __device__ __forceinline__ void load8(const uint8_t* buf, uint32_t p, uint32_t& d0, uint32_t& d1) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(buf + (p & ~3u));
@@ -441,14 +479,15 @@ __device__ __forceinline__ uint32_t swar4d(uint32_t d) {
 // of its '\n' (sb <= 4096).  Every smem address stays inside the stage (see `ec`), so that
 // predicated-off garbage positions cannot fault.
 template <bool kLazy>
-__device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e, CmRec& r) {
+// buf_s / cm_s: shared-window addresses of the stage and of the warp's comma mask words.
+__device__ __forceinline__ bool cm_fast(uint32_t buf_s, uint32_t cm_s, uint32_t sb, uint32_t e, CmRec& r) {
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
   bool ok = L - 128u <= 63u;
   // ---- exactly 12 commas in [sb, e): head [sb, sb+64) + middle [sb+64, e-64) + tail [e-64, e)
-  const uint32_t* w = cm32 + (sb >> 5);
+  const uint32_t wa = cm_s + 4u * (sb >> 5);
   const uint32_t sh = sb & 31u;
-  const uint32_t v0 = w[0], v1 = w[1], v2 = w[2], v3 = w[3], v4 = w[4];
+  const uint32_t v0 = lds32(wa), v1 = lds32(wa + 4), v2 = lds32(wa + 8), v3 = lds32(wa + 12), v4 = lds32(wa + 16);
   const uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
   const unsigned long long mid = (((unsigned long long)__funnelshift_r(v3, v4, sh) << 32) | __funnelshift_r(v2, v3, sh)) &
                                  ((1ull << min(L - 128u, 63u)) - 1ull);          // bits [sb+64, e-64)
@@ -458,8 +497,8 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   // inside the stage, so no address needs its own clamp
   const uint32_t ec = min(max(e, 64u), (uint32_t)kMaskBits - 1u);
   const uint32_t tp = ec - 64u;
-  const uint32_t* u = cm32 + (tp >> 5);
-  const uint32_t tsh = tp & 31u, u0 = u[0], u1 = u[1], u2 = u[2];
+  const uint32_t ua = cm_s + 4u * (tp >> 5);
+  const uint32_t tsh = tp & 31u, u0 = lds32(ua), u1 = lds32(ua + 4), u2 = lds32(ua + 8);
   const uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
   ok &= __popc(h0) + __popc(h1) + __popc(m0) + __popc(m1) + __popc(t0) + __popc(t1) == 12u;
   // ---- head: c0 = sb + o0 ends ts (1..8 digits); c1 = c0 + 1 (empty field 1); c2 = c0 + 12
@@ -486,7 +525,7 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   // byte among the digits is caught below), then the digit values are shifted to the top of the
   // word: the bytes after them fall off, zero bytes (leading zeros) come in below.
   uint32_t a0, a1;
-  load8(buf, S, a0, a1);
+  lds8u(buf_s + S, a0, a1);
   const unsigned long long ta = (((unsigned long long)a1 << 32) | a0) - 0x3030303030303030ull;
   const unsigned long long tv = ta << (8u * ((8u - o0) & 7u));
   const uint32_t da0 = (uint32_t)tv, da1 = (uint32_t)(tv >> 32);
@@ -494,7 +533,7 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   r.ts = swar4d(da0) * 10000u + swar4d(da1);
   // jobId: 10 digits at c1 + 1 = S + o0 + 2
   uint32_t d0, d1, d2;
-  load12(buf, S + o0 + 2u, d0, d1, d2);
+  lds12u(buf_s + S + o0 + 2u, d0, d1, d2);
   d0 -= 0x30303030u;
   d1 -= 0x30303030u;
   d2 -= 0x30303030u;
@@ -503,13 +542,13 @@ __device__ __forceinline__ bool cm_fast(const uint8_t* buf, const uint32_t* cm32
   r.jw1 = d1;
   r.jw2 = d2;
   // eventType at c4 + 1 = S + o0 + 14 + a4; category at c6 + 1
-  r.event = (uint32_t)buf[S + o0 + 14u + a4] - 48u;
-  r.cat = (uint32_t)buf[cat_at] - 48u;
+  r.event = lds_u8(buf_s + S + o0 + 14u + a4) - 48u;
+  r.cat = lds_u8(buf_s + cat_at) - 48u;
   ok &= r.event <= 9u && r.cat <= 9u;
   // cpu = D.DDDDDD at c8 + 1 = e - 28: the '.' is swapped for '0' for the digit check and
   // SWAR value (D0DD DDDD), and the integer digit's weight is fixed up (10^7 -> 10^6)
   uint32_t p0, p1;
-  load8(buf, kCmHaloL + ec - 28u, p0, p1);
+  lds8u(buf_s + kCmHaloL + ec - 28u, p0, p1);
   ok &= ((p0 >> 8) & 0xFFu) == '.';
   const uint32_t dp0 = (p0 ^ 0x1E00u) - 0x30303030u, dp1 = p1 - 0x30303030u;
   bad |= dbad(dp0) | dbad(dp1);
@@ -622,7 +661,6 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
   unsigned long long* c_sum = nullptr;                          // CM2: the cached pane's stripe
   unsigned long long* c_cnt = nullptr;
   uint32_t sv_h = 0, sv_n = 0;                                  // CM2 survivor ring: head, entries
-  uint32_t pc_lo = 0, pc_p = 0;                                 // cached pane [pc_lo, pc_lo + S)
 
   // CM2: decode and aggregate ring entries [sv_h, sv_h + n) with the warp's lanes
   auto drain = [&](uint32_t n) {
@@ -732,7 +770,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       n_rec += have ? 1u : 0u;
       sb = sel(have, sb, 0u);
       // usual-shape records: branch-free fast path; anything else: the exact general path
-      const bool fast = cm_fast<kCM2>(buf, cm32, sb, e, r) & have;
+      const bool fast = cm_fast<kCM2>(st_s, cm_s, sb, e, r) & have;
       const bool slow = have & !fast;
       bool ok = fast;
       if (__any_sync(0xffffffffu, slow)) {
@@ -756,11 +794,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
         ts_max1 = sel(kept, max(ts_max1, r.ts + 1u), ts_max1);
         surv = kCM2 ? (kept & (r.event == 1u)) : kept;          // WHERE (eventType == 1)
       }
-      if (surv && r.ts - pc_lo >= q.S) {         // pane = floor(ts / S), cached per thread
-        pc_p = pane_of(r.ts, q.S, q.div_magic);
-        pc_lo = pc_p * q.S;
-      }
-      const uint32_t p = surv ? pc_p : 0;
+      const uint32_t p = pane30(r.ts, a.pane_m, a.pane_sh);    // floor(ts / S)
       if (kCM2) {
         // warp-ballot stream compaction into the warp's survivor ring
         const uint32_t bal = __ballot_sync(0xffffffffu, surv);
@@ -940,6 +974,7 @@ cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
   a.k7f = 0x7F7F7F7Fu;
   a.k256 = 256u;
   a.k512 = 512u;
+  pane30_magic(q.S, a.pane_m, a.pane_sh);
   if (a.total_tiles == 0) return cudaSuccess;
   const size_t smem = (size_t)kWarps * kCmStages * kCmStage + kSmemPad;
   const int grid = (int)q.n_agg_ctas;

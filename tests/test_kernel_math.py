@@ -1,0 +1,69 @@
+"""CPU checks of integer identities the CUDA kernels rely on (no GPU, no library calls): each
+test restates a kernel helper's arithmetic in Python and checks it against plain integer
+division / digit parsing over the whole input range the kernel guarantees."""
+import random
+
+
+def pane30_magic(S):
+    # kernels_cm.cu pane30_magic: k = max(32, 30 + ceil(log2 S)), M = ceil(2^k / S), shift k - 32
+    if S <= 1:
+        return 0, 32
+    lg = 0
+    while (1 << lg) < S:
+        lg += 1
+    k = max(32, lg + 30)
+    return ((1 << k) + S - 1) // S, k - 32
+
+
+def pane30(ts, m, sh):
+    return ts if sh == 32 else ((ts * m) >> 32) >> sh
+
+
+def test_pane30_is_floor_division_below_2_pow_30():
+    rng = random.Random(7)
+    slides = list(range(1, 130)) + [300, 600, 3600, 86400, 10 ** 6, 2 ** 20 + 1, 2 ** 29 + 3, 2 ** 30 - 1]
+    for S in slides:
+        m, sh = pane30_magic(S)
+        assert m < 2 ** 32
+        cases = [0, 1, S - 1, S, S + 1, 2 ** 30 - 1, 999_999_999, 99_999_999]
+        cases += [q * S + r for q in (1, 2, (2 ** 30 - 1) // S) for r in (-1, 0, 1) if 0 <= q * S + r < 2 ** 30]
+        cases += [rng.randrange(2 ** 30) for _ in range(300)]
+        for ts in cases:
+            assert pane30(ts, m, sh) == ts // S, (S, ts)
+
+
+def swar4d(d):
+    # kernels_cm.cu swar4d: 4 digit values (first = most significant) -> value
+    p = (d * 0xA01) & 0xFFFFFFFF
+    p = ((p >> 8) & 0xFF) | (((p >> 24) & 0xFF) << 16)       # __byte_perm(p, 0, 0x4341)
+    return ((p * 0x640001) & 0xFFFFFFFF) >> 16
+
+
+def test_swar4d_all_four_digit_strings():
+    for v in range(10000):
+        s = f"{v:04d}"
+        d = sum((ord(c) - 48) << (8 * i) for i, c in enumerate(s))
+        assert swar4d(d) == v
+
+
+def test_ts_shift_decode_all_lengths():
+    # kernels_cm.cu cm_fast ts: bytes [S, S+8) = o0 digits, ',', garbage; 64-bit subtract of
+    # '0' from every byte, shift left by 8 * (8 - o0): the digit values end up in the top o0 bytes
+    rng = random.Random(3)
+    for _ in range(3000):
+        o0 = rng.randint(1, 8)
+        ts = rng.randrange(10 ** o0)
+        txt = f"{ts}".encode()
+        txt = (b"0" * (o0 - len(txt))) + txt if rng.random() < 0.2 else txt
+        o0 = len(txt)
+        tail = bytes([44]) + bytes(rng.randrange(256) for _ in range(7))
+        raw = (txt + tail)[:8]
+        w = int.from_bytes(raw, "little")
+        t = (w - 0x3030303030303030) % 2 ** 64
+        t = (t << (8 * ((8 - o0) & 7))) % 2 ** 64
+        lo, hi = t & 0xFFFFFFFF, t >> 32
+        bad = 0
+        for x in (lo, hi):
+            bad |= (x | ((x + 0x76767676) & 0xFFFFFFFF)) & 0x80808080
+        assert bad == 0
+        assert swar4d(lo) * 10000 + swar4d(hi) == int(txt)
