@@ -10,6 +10,18 @@ namespace lms {
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+// mbarrier parity wait on a shared-window address (every calling lane waits)
+__device__ __forceinline__ void mbar_wait_shared(uint32_t bar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n LAB_WAITS:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra LAB_WAITS;\n}" ::"r"(bar), "r"(phase) : "memory");
+}
 
 // ---- mbarrier + 1-D bulk copy (TMA engine, UBLKCP) -------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
@@ -131,6 +143,22 @@ __device__ __forceinline__ uint32_t dict_get(const Dict& d, unsigned long long k
   }
   atomicExch(&st->key_overflow, 1u);   // every entry taken by other keys: this key is dropped
   return kEmpty32;
+}
+
+// Lookup-or-insert of two keys whose first probes are issued together: the common case (both
+// keys found in their home entries) costs one L2 round trip for the pair instead of two
+// dependent ones; anything else (a miss, a collision, an index being published) falls back to
+// dict_get.  u0 / u1: whether the key is looked up at all (kEmpty32 otherwise).
+__device__ __forceinline__ void dict_get2(const Dict& d, unsigned long long k0, bool u0, unsigned long long k1,
+                                          bool u1, DevState* st, uint32_t& i0, uint32_t& i1) {
+  const unsigned long long* e0 = d.keys + 2 * (fmix64(k0) & d.cap_mask);
+  const unsigned long long* e1 = d.keys + 2 * (fmix64(k1) & d.cap_mask);
+  unsigned long long a0 = kEmpty64, b0 = kEmpty64, a1 = kEmpty64, b1 = kEmpty64;
+  if (u0) asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a0), "=l"(b0) : "l"(e0));
+  if (u1) asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a1), "=l"(b1) : "l"(e1));
+  const bool h0 = a0 == k0 && (uint32_t)b0 != kEmpty32, h1 = a1 == k1 && (uint32_t)b1 != kEmpty32;
+  i0 = !u0 ? kEmpty32 : h0 ? ((uint32_t)b0 >= d.max_keys ? kEmpty32 : (uint32_t)b0) : dict_get(d, k0, st);
+  i1 = !u1 ? kEmpty32 : h1 ? ((uint32_t)b1 >= d.max_keys ? kEmpty32 : (uint32_t)b1) : dict_get(d, k1, st);
 }
 
 // ---- pane table: pane index -> accumulator slot ------------------------------------------

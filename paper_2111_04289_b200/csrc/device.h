@@ -63,6 +63,7 @@ struct DevState {
   unsigned int fifo_count[2];   // LR1 retained-row FIFO sizes
   unsigned int fifo_cur;        // LR1: which FIFO holds the live rows
   unsigned int fifo_overflow;
+  unsigned int lr1_ticket;      // LR1 aggregate launch: CTAs done (the last advances fifo_count)
   int free_top;                 // free accumulator slots on the stack
   unsigned int pane_fail;       // a pane found no free slot (table entry marked kFail32)
   long long close_k_first, close_k_last;   // instances closed by the last close (multi-GPU)
@@ -172,6 +173,7 @@ struct QueryDev {
 
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
 int lr_agg_ctas(const QueryDev& q);
+uint64_t lr_tiles(const QueryDev& q, uint64_t nbytes);   // aggregate tiles of an LR segment
 int cm_agg_ctas(const QueryDev& q);
 size_t lr_agg_smem(const QueryDev& q);
 cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);

@@ -13,8 +13,9 @@
 // 70 bytes per record with SWAR range checks, parses the decoded fields from registers.
 // LR2: native u32 shared-memory atomics into a per-CTA table [2 pane slots][K keys]
 // (K = 200 * num_xways), written once per CTA to a partials array that the close kernel
-// merges per key slice (no global atomics on the hot path).  LR1: dictionary-mapped
-// vehicle counts per pane (global REDs) + projection of a 16 B row into the retained FIFO.
+// merges per key slice (no global atomics on the hot path).  LR1 (k_lr1_agg below): warp-owned
+// 64-record tiles, dictionary-mapped (or dense) vehicle counts per pane (global REDs) and the
+// projection of a 16 B row into the retained FIFO at deterministic positions.
 #include "common.cuh"
 
 #include <mutex>
@@ -127,11 +128,10 @@ __device__ __forceinline__ void lr_issue(const SegTable& segs, SegCursor& c, uns
 
 template <int KIND>
 __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
-  constexpr bool kLR1 = (KIND == kLR1S || KIND == kLR1T);
+  static_assert(KIND == kLR2S, "LR1 runs k_lr1_agg");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kLrStages];
   __shared__ unsigned long long slot_tag[2], loaded_tag[2];
-  __shared__ uint32_t s_fbase, s_fcur;      // LR1: this tile's reserved FIFO range
   const QueryDev& q = a.q;
   uint8_t* stage = smem;
   uint32_t* tsum = reinterpret_cast<uint32_t*>(smem + kLrStages * kLrTileBytes);   // [2][K]
@@ -143,10 +143,8 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   const unsigned long long T = a.total_tiles, G = gridDim.x;
   const unsigned long long t0 = T * blockIdx.x / G, t1 = T * (blockIdx.x + 1) / G;
 
-  if (!kLR1) {
-    for (uint32_t i = tid; i < 4 * K; i += blockDim.x) tsum[i] = 0;
-    if (tid < 2) slot_tag[tid] = loaded_tag[tid] = q.part_tag[blockIdx.x * 2 + tid];
-  }
+  for (uint32_t i = tid; i < 4 * K; i += blockDim.x) tsum[i] = 0;
+  if (tid < 2) slot_tag[tid] = loaded_tag[tid] = q.part_tag[blockIdx.x * 2 + tid];
   if (tid == 0) {
     for (int s = 0; s < kLrStages; s++) mbar_init(&full[s], 1);
     mbar_fence_init();
@@ -157,7 +155,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   iss.init(a.segs);
   if (tid == 0) {
     for (int s = 0; s < kLrStages; s++)
-      if (t0 + s < t1) lr_issue<kLR1>(a.segs, iss, t0 + s, stage + s * kLrTileBytes, &full[s]);
+      if (t0 + s < t1) lr_issue<false>(a.segs, iss, t0 + s, stage + s * kLrTileBytes, &full[s]);
   }
 
   const unsigned long long wm_prev = q.state->wm_prev;
@@ -174,14 +172,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
     const uint32_t bytes = (uint32_t)(rem < (unsigned long long)kLrTileBytes ? rem : kLrTileBytes);
     const uint32_t nrec = bytes / kLrRecBytes;
     uint8_t* buf = stage + s * kLrTileBytes;
-    if (kLR1) {   // one FIFO reservation per tile (was one contended atomic per warp and record)
-      if (tid == 0) {
-        s_fcur = q.state->fifo_cur;
-        s_fbase = atomicAdd(&q.state->fifo_count[s_fcur], nrec);
-      }
-    }
     mbar_wait(&full[s], ph);
-    if (kLR1) __syncthreads();
     if (bytes & 15u) {   // segment tail: copy the last < 16 bytes by hand (uniform branch)
       const uint32_t bulk = bytes & ~15u;
       if ((uint32_t)tid < bytes - bulk) buf[bulk + tid] = a.segs.s[si].ptr[off + bulk + tid];
@@ -197,7 +188,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
       for (int j = 0; j < kPairWords; j++) w[j] = wp[j];
       uint32_t ok = lr_validate_pair(w);
       if (recA + 1 >= nrec) ok &= 1u;   // odd tail: record B does not exist
-      LrRec rr[2] = {lr_decode<0, kLR1>(w), lr_decode<70, kLR1>(w)};
+      LrRec rr[2] = {lr_decode<0, false>(w), lr_decode<70, false>(w)};
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         if (recA + h >= nrec) break;
@@ -205,67 +196,32 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
         const LrRec& r = rr[h];
         // Linear Road domains (reading R1): Dir in {0,1}, Seg <= 99, XWay < num_xways
         const bool valid = ((ok >> h) & 1u) && r.dir <= 1u && r.seg <= 99u && r.xway < q.num_xways;
-        if (kLR1) {
-          // LR1: vehicle count of the record's pane + its projected row in the retained FIFO
-          // at the tile's reserved position (a hole, vidx = kEmpty32, for a dropped record)
-          uint32_t vidx = kEmpty32;
-          if (!valid) cnt.bad++;
-          else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;   // R7
-          else {
-            cnt.ts_min = min(cnt.ts_min, r.ts);
-            cnt.ts_max1 = max(cnt.ts_max1, r.ts + 1u);
-            const uint32_t p = pane_of(r.ts, q.S, q.div_magic);
-            if (p != c_pane) { c_pane = p; c_gslot = claim_slot(q, p); }
-            // lr1_dense (multi-GPU, LMS_FLAG_DENSE_VEHICLES): the vehicle id is the index
-            vidx = c_gslot == kFail32 ? kEmpty32
-                 : q.lr1_dense ? (r.vid < K ? (uint32_t)r.vid : kEmpty32)
-                               : dict_get(q.dict, r.vid, q.state);
-            // dense-vehicle mode cannot represent a VID >= max_keys: the batch is rejected
-            // (LMS_EINVAL at its completion), not silently counted as overflow
-            if (q.lr1_dense && r.vid >= K && c_gslot != kFail32) atomicExch(&q.state->vid_range, 1u);
-            if (vidx == kEmpty32) cnt.overflow++;
-            else atomicAdd(&q.acc_cnt32[(size_t)c_gslot * K + vidx], 1u);
-          }
-          const uint32_t pos = s_fbase + recA + h;
-          if (pos < q.fifo_cap) {
-            Lr1Retained row;
-            row.ts = r.ts; row.vidx = vidx; row.speed = (uint16_t)r.speed; row.xway = (uint16_t)r.xway;
-            row.seg = (uint16_t)r.seg; row.lane = (uint8_t)r.lane; row.dir = (uint8_t)r.dir;
-            __stcs(reinterpret_cast<uint4*>(q.fifo[s_fcur] + pos), *reinterpret_cast<const uint4*>(&row));
-          } else if (vidx != kEmpty32) {
-            atomicExch(&q.state->fifo_overflow, 1u);
-            cnt.overflow++;
-          }
-          continue;
-        }
         if (!valid) { cnt.bad++; continue; }
         if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) { cnt.late++; continue; }   // R7
         cnt.ts_min = min(cnt.ts_min, r.ts);
         cnt.ts_max1 = max(cnt.ts_max1, r.ts + 1u);
         const uint32_t p = pane_of(r.ts, q.S, q.div_magic);
-        if (!kLR1) {
-          const uint32_t key = (r.xway * 2u + r.dir) * 100u + r.seg;
-          if (p != c_pane) {   // find / claim a local pane slot (tag = acc slot << 32 | pane)
-            c_pane = p;
-            local_slot(slot_tag, q, p, c_slot, c_gslot);
-          }
-          if (c_gslot == kFail32) { cnt.overflow++; continue; }
-          if (c_slot < 2) {
-            atomicAdd(&tsum[c_slot * K + key], r.speed);
-            atomicAdd(&tcnt[c_slot * K + key], 1u);
-          } else {
-            const size_t g = (size_t)c_gslot * K + key;
-            atomicAdd(&q.acc_sum[g], (unsigned long long)r.speed);
-            atomicAdd(&q.acc_cnt[g], 1ull);
-          }
+        const uint32_t key = (r.xway * 2u + r.dir) * 100u + r.seg;
+        if (p != c_pane) {   // find / claim a local pane slot (tag = acc slot << 32 | pane)
+          c_pane = p;
+          local_slot(slot_tag, q, p, c_slot, c_gslot);
+        }
+        if (c_gslot == kFail32) { cnt.overflow++; continue; }
+        if (c_slot < 2) {
+          atomicAdd(&tsum[c_slot * K + key], r.speed);
+          atomicAdd(&tcnt[c_slot * K + key], 1u);
+        } else {
+          const size_t g = (size_t)c_gslot * K + key;
+          atomicAdd(&q.acc_sum[g], (unsigned long long)r.speed);
+          atomicAdd(&q.acc_cnt[g], 1ull);
         }
       }
     }
     __syncthreads();   // stage s fully consumed
-    if (tid == 0 && t + kLrStages < t1) lr_issue<kLR1>(a.segs, iss, t + kLrStages, buf, &full[s]);
+    if (tid == 0 && t + kLrStages < t1) lr_issue<false>(a.segs, iss, t + kLrStages, buf, &full[s]);
   }
 
-  if (!kLR1) {
+  {
     __syncthreads();
     // write this CTA's pane partials: overwrite on the batch's first launch (the tag was
     // empty when loaded), accumulate when an earlier launch of the same batch wrote the slot
@@ -293,6 +249,196 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   flush_counters(cnt, q.state);
 }
 
+// ---------------------------------------------------------------------------------------
+// LR1 (LR1S / LR1T) aggregate pass: warp-owned tiles, no CTA barrier in the loop.
+//
+// Every warp walks its own contiguous range of 64-record warp tiles (4480 B, one bulk copy
+// each) through a 2-stage smem ring; lane l decodes records 2l, 2l+1 of the tile (the 35-word
+// pair layout of k_lr_agg: word stride 35 is odd, so the pair loads are bank-conflict free).
+// Per record: validation, pane, vehicle index (dictionary: both records' first probes issued
+// together, dict_get2; dense ids: the id itself), one RED.32 into the pane's vehicle counts,
+// and its 16 B projected row into the retained FIFO.  FIFO positions are deterministic: the
+// FIFO's count at launch start (read by every CTA before any CTA finishes) + tile * 64 + record
+// (tail positions of a segment's last tile are written as holes), and the launch's last CTA
+// advances the count by tiles * 64 — no per-tile reservation atomic and no CTA barrier.
+constexpr int kLr1Warps = 4;
+constexpr int kLr1Threads = kLr1Warps * 32;
+constexpr int kLr1CtasPerSm = 5;
+constexpr int kLr1TileRecs = 64;
+constexpr int kLr1TileBytes = kLr1TileRecs * kLrRecBytes;   // 4480 = 16 * 280
+constexpr int kLr1Stages = 2;
+
+struct Lr1Args {
+  QueryDev q;
+  SegTable segs;
+  unsigned long long total_tiles;
+};
+
+// Producer side of a warp's tile walk: segment / tile within it.
+struct Lr1Iter {
+  int si;
+  unsigned long long t, seg_end;     // global tile index; first tile of the next segment
+  __device__ __forceinline__ void init(const SegTable& s, unsigned long long tile) {
+    si = 0;
+    while (si + 1 < s.n && tile >= s.tile_prefix[si + 1]) si++;
+    t = tile;
+    seg_end = s.tile_prefix[si + 1];
+  }
+  __device__ __forceinline__ void next(const SegTable& s) {
+    t++;
+    while (t >= seg_end && si + 1 < s.n) { si++; seg_end = s.tile_prefix[si + 1]; }
+  }
+};
+
+// Issue tile `it` into stage `dst` (shared-window address); returns its byte count (the < 16 B
+// remainder of a segment's last tile is copied by lane 0 here: the stage is free).
+__device__ __forceinline__ uint32_t lr1_issue(const SegTable& s, const Lr1Iter& it, uint32_t dst, uint32_t bar,
+                                              int lane) {
+  const unsigned long long off = (it.t - s.tile_prefix[it.si]) * (unsigned long long)kLr1TileBytes;
+  const unsigned long long rem = s.s[it.si].nbytes - off;
+  const uint32_t bytes = (uint32_t)(rem < (unsigned long long)kLr1TileBytes ? rem : kLr1TileBytes);
+  const uint32_t bulk = bytes & ~15u;
+  if (lane == 0) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bulk) : "memory");
+    const uint8_t* src = s.s[it.si].ptr + off;
+    if (bulk)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(dst), "l"(src), "r"(bulk), "r"(bar) : "memory");
+    for (uint32_t i = bulk; i < bytes; i++)
+      asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + i), "r"((uint32_t)src[i]));
+  }
+  return bytes;
+}
+
+__global__ void __launch_bounds__(kLr1Threads, kLr1CtasPerSm) k_lr1_agg(const Lr1Args a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[kLr1Warps][kLr1Stages];
+  const QueryDev& q = a.q;
+  DevState* st = q.state;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned long long T = a.total_tiles, GW = (unsigned long long)gridDim.x * kLr1Warps;
+  const unsigned long long gw = (unsigned long long)blockIdx.x * kLr1Warps + warp;
+  const unsigned long long t0 = T * gw / GW, t1 = T * (gw + 1) / GW;
+  const uint32_t K = q.K;
+  // the FIFO count is only advanced by this launch's last CTA, after every CTA read it here
+  const uint32_t fcur = *(volatile uint32_t*)&st->fifo_cur;
+  const unsigned long long fbase = *(volatile unsigned int*)&st->fifo_count[fcur];
+  Lr1Retained* const fifo = q.fifo[fcur];
+  const unsigned long long wm_prev = st->wm_prev;
+  if (lane == 0) {
+    for (int s = 0; s < kLr1Stages; s++) mbar_init(&full[warp][s], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const uint32_t stage_s = smem_addr(smem + warp * (kLr1Stages * kLr1TileBytes));
+  const uint32_t full_s = smem_addr(&full[warp][0]);
+  const uint32_t ntiles = (uint32_t)(t1 - t0);
+  Lr1Iter iss;
+  iss.init(a.segs, t0);
+  uint32_t bytes0 = 0, bytes1 = 0;             // bytes of the tiles in stages 0 / 1
+  unsigned long long tile0 = 0, tile1 = 0;     // their global tile indices
+  if (ntiles > 0) { tile0 = iss.t; bytes0 = lr1_issue(a.segs, iss, stage_s, full_s, lane); iss.next(a.segs); }
+  if (ntiles > 1) { tile1 = iss.t; bytes1 = lr1_issue(a.segs, iss, stage_s + kLr1TileBytes, full_s + 8u, lane); iss.next(a.segs); }
+
+  CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
+  uint32_t c_pane = kEmpty32, c_gslot = kFail32;   // cached slot of the last pane seen
+  for (uint32_t it = 0; it < ntiles; it++) {
+    const uint32_t s = it & 1u;
+    const uint32_t bytes = s ? bytes1 : bytes0;
+    const unsigned long long tile = s ? tile1 : tile0;
+    const uint32_t sb = stage_s + s * (uint32_t)kLr1TileBytes;
+    mbar_wait_shared(full_s + 8u * s, (it >> 1) & 1u);
+    __syncwarp();                                // (lane 0's remainder bytes, tail tiles)
+    const uint32_t nrec = bytes / kLrRecBytes;
+    const uint32_t recA = 2u * lane;
+    LrRec rr[2];
+    uint32_t ok = 0;
+    if (recA < nrec) {
+      uint32_t w[kPairWords];
+#pragma unroll
+      for (int j = 0; j < kPairWords; j++) w[j] = lds_u32(sb + 4u * (lane * kPairWords + j));
+      ok = lr_validate_pair(w);
+      if (recA + 1 >= nrec) ok &= 1u;          // odd tail: record B does not exist
+      rr[0] = lr_decode<0, true>(w);
+      rr[1] = lr_decode<70, true>(w);
+    }
+    bool use[2] = {false, false};
+    uint32_t gslot[2] = {kFail32, kFail32};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if (recA + h >= nrec) continue;
+      cnt.n++;
+      const LrRec& r = rr[h];
+      // Linear Road domains (reading R1): Dir in {0,1}, Seg <= 99, XWay < num_xways
+      const bool valid = ((ok >> h) & 1u) && r.dir <= 1u && r.seg <= 99u && r.xway < q.num_xways;
+      if (!valid) cnt.bad++;
+      else if (wm_prev != 0 && (unsigned long long)r.ts + 1ull < wm_prev) cnt.late++;   // R7
+      else {
+        cnt.ts_min = min(cnt.ts_min, r.ts);
+        cnt.ts_max1 = max(cnt.ts_max1, r.ts + 1u);
+        const uint32_t p = pane_of(r.ts, q.S, q.div_magic);
+        if (p != c_pane) { c_pane = p; c_gslot = claim_slot(q, p); }
+        gslot[h] = c_gslot;
+        use[h] = c_gslot != kFail32;
+        if (!use[h]) cnt.overflow++;
+      }
+    }
+    uint32_t vidx[2];
+    if (q.lr1_dense) {
+      // lr1_dense (multi-GPU, LMS_FLAG_DENSE_VEHICLES): the vehicle id is the index; a VID >=
+      // max_keys rejects the batch (LMS_EINVAL at its completion), never silent overflow
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        vidx[h] = use[h] && rr[h].vid < K ? (uint32_t)rr[h].vid : kEmpty32;
+        if (use[h] && rr[h].vid >= K) atomicExch(&st->vid_range, 1u);
+      }
+    } else {
+      dict_get2(q.dict, rr[0].vid, use[0], rr[1].vid, use[1], st, vidx[0], vidx[1]);
+    }
+    const unsigned long long pos0 = fbase + tile * (unsigned long long)kLr1TileRecs + recA;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if (use[h]) {
+        if (vidx[h] == kEmpty32) cnt.overflow++;
+        else atomicAdd(&q.acc_cnt32[(size_t)gslot[h] * K + vidx[h]], 1u);
+      }
+      // projected row (a hole, vidx = kEmpty32, for a dropped record or a tail position)
+      Lr1Retained row;
+      const bool live = recA + h < nrec;
+      const LrRec& r = rr[h];
+      row.ts = live ? r.ts : 0u;
+      row.vidx = use[h] ? vidx[h] : kEmpty32;
+      row.speed = live ? (uint16_t)r.speed : 0; row.xway = live ? (uint16_t)r.xway : 0;
+      row.seg = live ? (uint16_t)r.seg : 0; row.lane = live ? (uint8_t)r.lane : 0; row.dir = live ? (uint8_t)r.dir : 0;
+      if (pos0 + h < q.fifo_cap) {
+        __stcs(reinterpret_cast<uint4*>(fifo + pos0 + h), *reinterpret_cast<const uint4*>(&row));
+      } else if (use[h] && vidx[h] != kEmpty32) {
+        atomicExch(&st->fifo_overflow, 1u);
+        cnt.overflow++;
+      }
+    }
+    __syncwarp();                                // stage s consumed by every lane
+    if (it + kLr1Stages < ntiles) {
+      const unsigned long long tn = iss.t;
+      const uint32_t b2 = lr1_issue(a.segs, iss, sb, full_s + 8u * s, lane);
+      iss.next(a.segs);
+      bytes0 = s ? bytes0 : b2;
+      bytes1 = s ? b2 : bytes1;
+      tile0 = s ? tile0 : tn;
+      tile1 = s ? tn : tile1;
+    }
+  }
+  flush_counters(cnt, st, smem);                 // (syncs the CTA: the stages are free)
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&st->lr1_ticket, 1u) == gridDim.x - 1) {   // last CTA of the launch
+      st->fifo_count[fcur] = (unsigned int)min(fbase + T * (unsigned long long)kLr1TileRecs, 0xFFFFFFFFull);
+      st->lr1_ticket = 0;
+      __threadfence();
+    }
+  }
+}
+
 }  // namespace
 
 // Load every kernel of this file now (CUDA 12 loads kernels lazily, at first launch, and a
@@ -302,7 +448,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
 void preload_lr_kernels() {
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, k_lr_agg<kLR2S>);
-  cudaFuncGetAttributes(&fa, k_lr_agg<kLR1S>);
+  cudaFuncGetAttributes(&fa, k_lr1_agg);
 }
 
 int lr_agg_ctas(const QueryDev& q) {
@@ -312,13 +458,18 @@ int lr_agg_ctas(const QueryDev& q) {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  (void)q;
-  return nsm * 2;
+  return (q.kind == kLR1S || q.kind == kLR1T) ? nsm * kLr1CtasPerSm : nsm * 2;
+}
+
+uint64_t lr_tiles(const QueryDev& q, uint64_t nbytes) {
+  const uint64_t recs = nbytes / kLrRecBytes, per = (q.kind == kLR1S || q.kind == kLR1T) ? kLr1TileRecs : kLrTileRecs;
+  return (recs + per - 1) / per;
 }
 
 size_t lr_agg_smem(const QueryDev& q) {
   const bool lr1 = (q.kind == kLR1S || q.kind == kLR1T);
-  return (size_t)kLrStages * kLrTileBytes + (lr1 ? 0 : (size_t)4 * q.K * sizeof(uint32_t));
+  return lr1 ? (size_t)kLr1Warps * kLr1Stages * kLr1TileBytes
+             : (size_t)kLrStages * kLrTileBytes + (size_t)4 * q.K * sizeof(uint32_t);
 }
 
 // cudaFuncSetAttribute once per (kernel, device, size): it is not a per-launch call (and the
@@ -354,11 +505,16 @@ cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
       k_lr_agg<kLR2S><<<grid, kLrThreads, smem, st>>>(a);
       break;
     case kLR1S:
-    case kLR1T:
-      e = set_smem_once((const void*)k_lr_agg<kLR1S>, (int)smem);
+    case kLR1T: {
+      e = set_smem_once((const void*)k_lr1_agg, (int)smem);
       if (e != cudaSuccess) return e;
-      k_lr_agg<kLR1S><<<grid, kLrThreads, smem, st>>>(a);
+      Lr1Args b;
+      b.q = q;
+      b.segs = segs;
+      b.total_tiles = a.total_tiles;
+      k_lr1_agg<<<grid, kLr1Threads, smem, st>>>(b);
       break;
+    }
     default:
       return cudaErrorInvalidValue;
   }

@@ -374,8 +374,7 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
     t.tile_prefix[0] = 0;
     for (int i = 0; i < t.n; i++) {
       t.s[i] = segs[s0 + i];
-      const uint64_t tiles = lr ? ((t.s[i].nbytes / kLrRecBytes + kLrTileRecs - 1) / kLrTileRecs)
-                                : ((t.s[i].nbytes + kCmTile - 1) / kCmTile);
+      const uint64_t tiles = lr ? lr_tiles(q->qd, t.s[i].nbytes) : ((t.s[i].nbytes + kCmTile - 1) / kCmTile);
       t.tile_prefix[i + 1] = t.tile_prefix[i] + tiles;
     }
     CUDA_TRY(lr ? launch_lr_agg(q->qd, t, q->stream) : launch_cm_agg(q->qd, t, q->stream));
@@ -1061,6 +1060,12 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     init.evicted_upto = -(1ll << 62);
     init.free_top = (int)q->P;
     QC_TRY(cudaMemcpy(d.state, &init, sizeof(init), cudaMemcpyHostToDevice));
+    // host row FIFO pre-sized now (pinned + touched), so that no batch's result copy pays a
+    // cudaHostAlloc + page touch inside its Proc (it still grows past this if not drained)
+    {
+      const uint64_t pre = std::min<uint64_t>(cfg->max_result_rows, 1ull << 20);
+      QC_TRY(is_lr1(q->kind) ? q->lr1_rows.reserve(pre) : q->agg_rows.reserve(pre));
+    }
     QC_TRY(cudaDeviceSynchronize());
 #undef Q_TRY
 #undef QC_TRY

@@ -15,9 +15,10 @@ comes from the B200 model  Proc(bytes) = a + bytes / bw  fitted on this GPU (cal
 file), the 10 ms poll of P:564 and one batch in flight.  A dataset violates the deadline when
 completion - ingest > d (P:208-210: #violation / #total datasets).
 
-A sensitivity run repeats Part A with a fixed per-batch overhead of `--fixed-a` seconds (a
-Spark-like micro-batch cost; the B200's is ~35 us): it shows the regime in which the paper's
-OS(t3) runaway appears (small batches spend most of their time in overhead).
+Sensitivity runs repeat Part A with a fixed per-batch overhead of a seconds (`--fixed`, a
+Spark-like micro-batch cost; the B200's is ~35 us): they show the regime in which the paper's
+OS(t3) runaway appears — a 3 s batch takes longer than 3 s (a + 3 s x load > 3 s) while the
+deadline sizer's larger batches still keep up.
 
 Part B — timelines (Fig. "Timeline during the initial 20-minute run of LR1S / LR1T",
 P:1002-1028): LMStream (Alg. 1) against the paper's Baseline (Spark's fixed 10 s trigger,
@@ -169,9 +170,8 @@ def main():
     ap.add_argument("--part", default="AB")
     ap.add_argument("--loads", default="0.5,0.9")
     ap.add_argument("--minutes-a", type=float, default=90.0)
-    ap.add_argument("--fixed-a", type=float, default=1.0,
-                    help="sensitivity run with this fixed per-batch overhead [s] (0: skip)")
-    ap.add_argument("--loads-fixed", default="0.5,0.7")
+    ap.add_argument("--fixed", default="1.0:0.5,0.7;2.5:0.3",
+                    help="sensitivity runs 'a:load,..;a:load': fixed per-batch overhead a [s] at those loads")
     ap.add_argument("--minutes-b", type=float, default=20.0)
     ap.add_argument("--traffic-b", default="R(50,500)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "f3_dynamics.json"))
@@ -180,9 +180,11 @@ def main():
     if "A" in args.part:
         calib = json.load(open(args.calib))
         out["violation"] = part_a(calib, [float(x) for x in args.loads.split(",")], args.minutes_a)
-        if args.fixed_a > 0:
-            out["violation_fixed_overhead"] = part_a(calib, [float(x) for x in args.loads_fixed.split(",")],
-                                                     args.minutes_a, fixed_s=args.fixed_a)
+        out["violation_fixed_overhead"] = []
+        for spec in filter(None, args.fixed.split(";")):            # "a:load,load;a:load"
+            fa, lds = spec.split(":")
+            out["violation_fixed_overhead"] += part_a(calib, [float(x) for x in lds.split(",")],
+                                                      args.minutes_a, fixed_s=float(fa))
         out["calibration"] = {k: calib[k]["derived"] for k in ("LR2S", "CM2S")}
     if "B" in args.part:
         out["timeline"] = part_b(args.minutes_b, args.traffic_b)
