@@ -168,6 +168,8 @@ struct QueryDev {
   // window counts are summed into lr1_w and all-reduced before the probe
   uint32_t lr1_dense;
   uint32_t* lr1_w;              // [K]
+  uint32_t* lr1_wc;             // single GPU LR1: window counts of the first closing instances
+                                // [kLr1Wc = 4][K] (k_lr1_wcache), null when not allocated
   PeerView* peers;              // [world] (fused exchange; null until lms_p2p_import)
 };
 
@@ -179,6 +181,7 @@ size_t lr_agg_smem(const QueryDev& q);
 cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
 cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st);
+int close_launches(const QueryDev& q);                   // kernels launch_close enqueues
 cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_lr1_wsum(const QueryDev& q, long long k, cudaStream_t st);
 cudaError_t launch_lr1_probe(const QueryDev& q, long long k, cudaStream_t st);

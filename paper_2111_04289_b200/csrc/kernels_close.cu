@@ -454,10 +454,43 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   if (ticket(st)) finish(q, w);
 }
 
+// LR1 window counts of the first kLr1Wc instances a close emits: wc[i][v] = the count of
+// vehicle index v over instance (nk + i)'s panes, one dense pass over the panes' count arrays
+// (L2-resident: ppw x 4 B x vehicles), so that the probe reads one count per row instead of
+// ppw gathers.  Launched before k_close_lr1 (same window range: the state is not advanced
+// until k_close_lr1's last CTA); a batch that closes nothing returns at once.
+constexpr uint32_t kLr1Wc = 4;           // instances with precomputed window counts
+constexpr uint32_t kLr1WcMaxPpw = 64;    // R/S up to this (more: the probe sums the panes itself)
+__device__ __forceinline__ uint32_t lr1_wc_instances(const QueryDev& q, const WinRange& w) {
+  if (!(w.any && w.k_last >= w.nk) || q.lr1_wc == nullptr || q.world != 1 || q.ppw > kLr1WcMaxPpw) return 0;
+  return (uint32_t)min(w.k_last - w.nk + 1, (long long)kLr1Wc);
+}
+__global__ void __launch_bounds__(kCloseThreads) k_lr1_wcache(const CloseArgs a) {
+  const QueryDev& q = a.q;
+  const WinRange w = win_range(q, a.flush);
+  const uint32_t nI = lr1_wc_instances(q, w);
+  if (nI == 0) return;
+  __shared__ uint32_t sl[kLr1Wc][kLr1WcMaxPpw];
+  for (uint32_t x = threadIdx.x; x < nI * q.ppw; x += blockDim.x)
+    sl[x / q.ppw][x % q.ppw] = find_slot(q, w.nk + x / q.ppw + x % q.ppw);
+  __syncthreads();
+  const uint32_t nv = q.lr1_dense ? q.K : min(q.state->n_keys, q.K);
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i = 0; i < nI; i++)
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += stride) {
+      uint32_t m = 0;
+      for (uint32_t j = 0; j < q.ppw; j++) {
+        const uint32_t g = sl[i][j];
+        if (g != kEmpty32) m += __ldcg(&q.acc_cnt32[(size_t)g * q.K + v]);
+      }
+      q.lr1_wc[(size_t)i * q.K + v] = m;
+    }
+}
+
 // LR1: probe retained rows whose pane is the newest slide of a closing instance.
 constexpr int kLr1Items = 2;             // retained rows per thread and iteration
 constexpr int kLr1SlotCache = 1024;      // panes whose slots a CTA resolves up front
-constexpr int kLr1MaxPpw = 8;            // window panes summed with unrolled loads
+constexpr int kLr1MaxPpw = 8;
 __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) {
   const QueryDev& q = a.q;
   DevState* st = q.state;
@@ -488,24 +521,34 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t ppw = min(q.ppw, (uint32_t)kLr1MaxPpw);   // (R/S <= 8 unrolled; more: loop)
+  const uint32_t nwc = lr1_wc_instances(q, w);              // instances with window counts
   const uint32_t per_cta = blockDim.x * kLr1Items;
   const uint32_t iters = (n + per_cta * gridDim.x - 1) / (per_cta * gridDim.x);
-  for (uint32_t it = 0; it < iters; it++) {
+  // the next iteration's retained rows are loaded one iteration ahead (their DRAM latency
+  // overlaps this iteration's gathers, appends and stores); holes / past-the-end: vidx = none
+  uint4 nxt[kLr1Items];
+  auto load_rows = [&](uint32_t it) {
     const uint32_t base = (it * gridDim.x + blockIdx.x) * per_cta;
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) {
+      const uint32_t idx = base + i * blockDim.x + threadIdx.x;   // coalesced 16 B loads
+      // read once: streaming load (the FIFO is not re-read from L2)
+      nxt[i] = idx < n ? __ldcs(reinterpret_cast<const uint4*>(src + idx)) : make_uint4(0u, kEmpty32, 0u, 0u);
+    }
+  };
+  if (iters) load_rows(0);
+  for (uint32_t it = 0; it < iters; it++) {
     Lr1Retained r[kLr1Items];
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) r[i] = *reinterpret_cast<const Lr1Retained*>(&nxt[i]);
+    if (it + 1 < iters) load_rows(it + 1);
     long long kk[kLr1Items];
     uint32_t m[kLr1Items];
     uint32_t emit = 0, keep = 0;     // bit i: item i
 #pragma unroll
     for (int i = 0; i < kLr1Items; i++) {
-      const uint32_t idx = base + i * blockDim.x + threadIdx.x;   // coalesced 16 B loads
       m[i] = 0; kk[i] = 0;
-      if (idx < n) {
-        {   // read once: streaming load (the FIFO is not re-read from L2)
-          const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + idx));
-          r[i] = *reinterpret_cast<const Lr1Retained*>(&v);
-        }
+      {
         if (r[i].vidx != kEmpty32) {          // (holes: records the aggregate pass dropped)
           const long long p = (long long)pane_of(r[i].ts, q.S, q.div_magic);
           kk[i] = p - (long long)q.ppw + 1;   // instance whose newest slide is pane p
@@ -513,33 +556,34 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
         }
       }
     }
-    // multiplicity: the vehicle's count over the instance's panes; all loads of the items
-    // are independent and issued back to back (latency-bound: L2-resident count tables)
-    uint32_t c[kLr1Items][kLr1MaxPpw];
+    // multiplicity: the vehicle's count over the instance's panes.  Common case: the window
+    // counts k_lr1_wcache precomputed — one L2 load per row, all items' loads back to back.
+    // Otherwise the row sums its instance's pane counts itself (cached slots or table lookups).
+    uint32_t wc_mask = 0;
 #pragma unroll
     for (int i = 0; i < kLr1Items; i++) {
       const long long off = kk[i] - pbase;
-      const bool fast = (emit >> i & 1u) && cached && off >= 0;
-#pragma unroll
-      for (int j = 0; j < kLr1MaxPpw; j++) {
-        const uint32_t g = (fast && (uint32_t)j < ppw) ? s_slot[off + j] : kEmpty32;
-        c[i][j] = g != kEmpty32 ? __ldcg(&q.acc_cnt32[(size_t)g * q.K + r[i].vidx]) : 0u;
+      if ((emit >> i & 1u) && off >= 0 && off < (long long)nwc) {
+        wc_mask |= 1u << i;
+        m[i] = __ldcg(&q.lr1_wc[(size_t)off * q.K + r[i].vidx]);
       }
-      if ((emit >> i & 1u) && !fast)          // rare: panes outside the cached span
-        for (uint32_t j = 0; j < q.ppw; j++) {
-          const uint32_t g = find_slot(q, kk[i] + j);
-          if (g != kEmpty32) m[i] += q.acc_cnt32[(size_t)g * q.K + r[i].vidx];
-        }
-      else if (fast)
-        for (uint32_t j = kLr1MaxPpw; j < q.ppw; j++) {   // R/S > 8
-          const uint32_t g = s_slot[off + j];
-          if (g != kEmpty32) m[i] += q.acc_cnt32[(size_t)g * q.K + r[i].vidx];
-        }
     }
+    const uint32_t slow_mask = emit & ~wc_mask;
+    if (slow_mask) {
+      for (int i = 0; i < kLr1Items; i++) {
+        if (!(slow_mask >> i & 1u)) continue;
+        const long long off = kk[i] - pbase;
+        for (uint32_t j = 0; j < q.ppw; j++) {
+          const uint32_t g = (cached && off >= 0) ? s_slot[off + j] : find_slot(q, kk[i] + j);
+          if (g != kEmpty32) m[i] += __ldcg(&q.acc_cnt32[(size_t)g * q.K + r[i].vidx]);
+        }
+      }
+    }
+    // vehicle ids of the emitted rows (dictionary: one gather each, issued back to back)
+    unsigned long long veh[kLr1Items];
 #pragma unroll
     for (int i = 0; i < kLr1Items; i++)
-#pragma unroll
-      for (int j = 0; j < kLr1MaxPpw; j++) m[i] += c[i][j];
+      veh[i] = (emit >> i & 1u) ? (q.lr1_dense ? (unsigned long long)r[i].vidx : __ldcg(&q.dict.key_by_idx[r[i].vidx])) : 0ull;
     // warp-aggregated appends, item-major so that every store instruction writes consecutive
     // rows: one atomic per warp and iteration on each cursor
     uint32_t em[kLr1Items], km[kLr1Items], ne = 0, nk = 0;
@@ -552,7 +596,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
     // CTA-wide appends: warp totals -> thread 0 -> one atomic per cursor per CTA and iteration
     // (per-warp atomics on the two global cursors were the probe's main serialisation)
     const uint32_t warp = threadIdx.x >> 5;
-    if (lane == 0) s_wtot[warp] = ne | (nk << 16);          // <= 64 rows each per warp
+    if (lane == 0) s_wtot[warp] = ne | (nk << 16);          // <= 32 * kLr1Items rows each per warp
     __syncthreads();
     if (threadIdx.x == 0) {
       uint32_t e_acc = 0, k_acc = 0;
@@ -576,7 +620,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
         if (pos < q.row_cap) {
           lms_lr1_row o;
           o.win_start_s = kk[i] * (long long)q.S;
-          o.vehicle = q.lr1_dense ? r[i].vidx : q.dict.key_by_idx[r[i].vidx];
+          o.vehicle = veh[i];
           o.ts = r[i].ts; o.multiplicity = m[i]; o.speed = r[i].speed; o.xway = r[i].xway;
           o.segment = r[i].seg; o.lane = r[i].lane; o.dir = r[i].dir;
           // streaming stores: 320 MB of rows per 10M probes must not evict the count tables
@@ -736,6 +780,7 @@ void preload_close_kernels() {
   cudaFuncAttributes fa;
   cudaFuncGetAttributes(&fa, k_close_agg);
   cudaFuncGetAttributes(&fa, k_close_lr1);
+  cudaFuncGetAttributes(&fa, k_lr1_wcache);
   cudaFuncGetAttributes(&fa, k_lr1_evict);
   cudaFuncGetAttributes(&fa, k_lr1_wsum);
   cudaFuncGetAttributes(&fa, k_lr1_probe);
@@ -756,9 +801,16 @@ int close_ctas(const QueryDev& q) {
   return q.kind == kLR2S ? 4 * nsm : (q.kind == kLR1S || q.kind == kLR1T) ? 4 * nsm : nsm;
 }
 
+int close_launches(const QueryDev& q) {
+  return ((q.kind == kLR1S || q.kind == kLR1T) && q.lr1_wc != nullptr && q.world == 1) ? 2 : 1;
+}
+
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {
   CloseArgs a{q, flush};
-  if (q.kind == kLR1S || q.kind == kLR1T) k_close_lr1<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+  if (q.kind == kLR1S || q.kind == kLR1T) {
+    if (q.lr1_wc != nullptr && q.world == 1) k_lr1_wcache<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+    k_close_lr1<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+  }
   else k_close_agg<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
   return cudaGetLastError();
 }

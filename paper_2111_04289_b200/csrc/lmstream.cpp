@@ -396,7 +396,7 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
 // Window close (+ LR1 eviction, + multi-GPU owner bucketing), batch report, end event.
 lms_status launch_close_stage(lms_query* q) {
   CUDA_TRY(launch_close(q->qd, q->F().flush ? 1 : 0, q->stream));
-  q->launches++;
+  q->launches += (uint64_t)close_launches(q->qd);
   if (is_lr1(q->kind)) {
     CUDA_TRY(launch_lr1_evict(q->qd, q->stream));
     q->launches++;
@@ -1007,6 +1007,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       Q_TRY(q->dalloc(&d.acc_cnt32, (size_t)q->P * d.K, 0));
       if (d.world > 1 || (cfg->flags & LMS_FLAG_DENSE_VEHICLES)) d.lr1_dense = 1;   // vehicle-indexed counts
       if (d.world > 1) Q_TRY(q->dalloc(&d.lr1_w, d.K, 0));    // + the all-reduced window counts
+      else Q_TRY(q->dalloc(&d.lr1_wc, (size_t)4 * d.K, 0));   // window counts of closing instances
     } else {
       // CM2: up to 16 stripes of the accumulators so that the RED.64s of a few hot jobIds spread
       // over 16 addresses (J = 100: 0.92 -> 0.34 ms per 10M records); 1.5 GB at the defaults
