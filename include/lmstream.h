@@ -127,6 +127,10 @@ typedef struct {
                                        batch i still runs (two batches in flight, separate
                                        report / row buffers); lms_sync and reads complete
                                        them in order.  Stream order keeps window state exact. */
+#define LMS_FLAG_NVLS         0x8u  /* num_gpus > 1, LR2S / CM1*: merge the dense partial tables
+                                       through NVLink-switch multicast (NVLS, multimem.red) when
+                                       every device can join a multicast object; otherwise (or
+                                       without the flag) the owner-push exchange (lms_nvls_active) */
 #define LMS_FLAG_DENSE_VEHICLES 0x4u /* LR1: vehicle ids index the per-pane counts directly
                                        (VID < max_keys) instead of the key dictionary.  A record
                                        with VID >= max_keys is rejected: dropped, counted in
@@ -350,6 +354,14 @@ lms_status  lms_p2p_collect(lms_query* q);
  * lms_p2p_collect a whole multi-GPU micro-batch runs with one host synchronisation and no
  * per-batch NCCL call.  ESTATE: batch in flight, peers not imported.                       */
 lms_status  lms_p2p_device_watermark(lms_query* q, int32_t enable);
+/* *active = 1 iff this single-handle multi-device query (num_gpus > 1, LR2S / CM1S / CM1T)
+ * merges its dense partial tables through NVLS (PAPER.md P:751, P:962 —
+ * the shuffle): the merge accumulators of all devices are the replicas of one NVLink-switch
+ * multicast object, the close's partial rows are reduced into every replica with
+ * multimem.red.add.u64, and each key's owner finalizes it from its local replica and zeroes it
+ * in all replicas with multimem.st — no owner push, no all-to-all.  0: the owner-push exchange
+ * (no LMS_FLAG_NVLS, a device that cannot join a multicast object, CM2S / LR1, one GPU).   */
+lms_status  lms_nvls_active(lms_query* q, int32_t* active);
 
 /* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
  * index the per-pane counts directly (VID < max_keys; a larger VID is rejected: LMS_EINVAL), every

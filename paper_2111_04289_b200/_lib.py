@@ -30,6 +30,7 @@ MODE = {"lmstream": 0, "deadline": 1, "trigger": 2, "manual": 3}
 LMS_FLAG_ONLINE_INFPT = 1
 LMS_FLAG_PIPELINE = 2
 LMS_FLAG_DENSE_VEHICLES = 4
+LMS_FLAG_NVLS = 8
 LMS_OP_SCAN, LMS_OP_FILTER, LMS_OP_PROJECT, LMS_OP_HASHAGG, LMS_OP_HASHJOIN, LMS_OP_SORT, \
     LMS_OP_SHUFFLE, LMS_OP_EXPAND = range(8)
 LMS_DEV_CPU, LMS_DEV_GPU = 0, 1
@@ -124,6 +125,7 @@ _PROTOS = {
     "lms_p2p_exchange_async": (C.c_int32, [_Q]),
     "lms_p2p_collect": (C.c_int32, [_Q]),
     "lms_p2p_device_watermark": (C.c_int32, [_Q, C.c_int32]),
+    "lms_nvls_active": (C.c_int32, [_Q, _P(C.c_int32)]),
     "lms_split": (C.c_int32, [C.c_int32, C.c_void_p, C.c_uint64, C.c_uint32, _P(C.c_uint64)]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "lms_kernel_launches": (C.c_int32, [_Q, _P(C.c_uint64)]),

@@ -85,6 +85,8 @@ struct BatchReport {
   unsigned long long n_records, bad, late, overflow, rows, windows_closed;
   long long watermark;          // -1 if none
   unsigned int n_keys, row_overflow, key_overflow, fifo_overflow, vid_range;
+  unsigned int rehash_req;      // dictionary tombstones above a quarter: the host enqueues the
+                                // grid-wide rebuild (launch_dict_rehash) before the next batch
   long long close_k_first, close_k_last;
   unsigned long long part_rows;
   unsigned int owner_count[kMaxWorld];
@@ -171,6 +173,13 @@ struct QueryDev {
   uint32_t* lr1_wc;             // single GPU LR1: window counts of the first closing instances
                                 // [kLr1Wc = 4][K] (k_lr1_wcache), null when not allocated
   PeerView* peers;              // [world] (fused exchange; null until lms_p2p_import)
+  // NVLS (single-handle multi-device driver, dense LR2 / CM1 tables): multicast addresses of
+  // the merge accumulators — every device's macc_sum / macc_cnt is its replica of one
+  // multicast object, pushes reduce in the NVLink switch with multimem.red into every replica,
+  // owners finalize their keys from their own replica and zero them in all replicas with
+  // multimem.st.  Null: the owner-push path (remote RED.64 into the owner's accumulators).
+  unsigned long long* mc_sum;
+  unsigned long long* mc_cnt;
 };
 
 // Launchers (kernels_*.cu).  All asynchronous on `st`.
@@ -182,6 +191,7 @@ cudaError_t launch_lr_agg(const QueryDev& q, const SegTable& segs, cudaStream_t 
 cudaError_t launch_cm_agg(const QueryDev& q, const SegTable& segs, cudaStream_t st);
 cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st);
 int close_launches(const QueryDev& q);                   // kernels launch_close enqueues
+cudaError_t launch_dict_rehash(const QueryDev& q, cudaStream_t st);   // 2 kernels
 cudaError_t launch_lr1_evict(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_lr1_wsum(const QueryDev& q, long long k, cudaStream_t st);
 cudaError_t launch_lr1_probe(const QueryDev& q, long long k, cudaStream_t st);

@@ -84,6 +84,17 @@ __device__ void reclaim_key(const QueryDev& q, uint32_t idx) {
 
 // Whole CTA: rebuild the dictionary's hash table from the live keys (drops the tombstones;
 // every live key keeps its dense index).
+// Dictionary rebuild policy: above a quarter of the entries tombstoned, the batch report asks
+// the host for the grid-wide rebuild (k_dict_clear + k_dict_reinsert, enqueued before the next
+// batch: ~tens of microseconds for 2^21 entries); only above half does the closing CTA rebuild
+// the table itself (one CTA: milliseconds — a safety net, e.g. for pipelined handles).
+__device__ __forceinline__ bool dict_wants_rehash(const QueryDev& q, const DevState* st) {
+  return st->n_tomb > (uint32_t)((q.dict.cap_mask + 1) / 4);
+}
+__device__ __forceinline__ bool dict_must_rehash(const QueryDev& q, const DevState* st) {
+  return st->n_tomb > (uint32_t)((q.dict.cap_mask + 1) / 2);
+}
+
 __device__ void dict_rehash_cta(const QueryDev& q) {
   const unsigned long long cap = q.dict.cap_mask + 1;
   for (unsigned long long i = threadIdx.x; i < cap; i += blockDim.x) {
@@ -158,8 +169,11 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
   if (w.any && !lr1) evict_rebuild_cta(q, w.k_last);      // LR1: k_lr1_evict frees the slots
   {   // tombstones above a quarter of the table: rebuild it (LR1: in k_lr1_evict)
     __shared__ int s_rehash;
-    if (threadIdx.x == 0)
-      s_rehash = q.kind == kCM2S && q.world == 1 && st->n_tomb > (uint32_t)((q.dict.cap_mask + 1) / 4);
+    if (threadIdx.x == 0) {
+      const bool dk = q.kind == kCM2S && q.world == 1;
+      s_rehash = dk && dict_must_rehash(q, st);
+      q.report->rehash_req = (dk && !s_rehash && dict_wants_rehash(q, st)) ? 1u : 0u;
+    }
     __syncthreads();
     if (s_rehash) dict_rehash_cta(q);
   }
@@ -639,6 +653,26 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
   if (ticket(st)) finish(q, w);
 }
 
+// Grid-wide dictionary rebuild (host-enqueued between batches when a report asked for it):
+// clear every entry, then reinsert every live key (key_by_idx) at its index.
+__global__ void __launch_bounds__(kCloseThreads) k_dict_clear(const QueryDev q) {
+  const unsigned long long n = 2 * (q.dict.cap_mask + 1);
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x)
+    q.dict.keys[i] = kEmpty64;
+}
+__global__ void __launch_bounds__(kCloseThreads) k_dict_reinsert(const QueryDev q) {
+  const uint32_t hwm = min(q.state->n_keys, q.dict.max_keys);
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < hwm; idx += gridDim.x * blockDim.x) {
+    const unsigned long long key = q.dict.key_by_idx[idx];
+    if (key == kEmpty64) continue;
+    unsigned long long h = fmix64(key) & q.dict.cap_mask;
+    while (atomicCAS(q.dict.keys + 2 * h, kEmpty64, key) != kEmpty64) h = (h + 1) & q.dict.cap_mask;
+    reinterpret_cast<unsigned int*>(q.dict.keys + 2 * h + 1)[0] = idx;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) q.state->n_tomb = 0;   // (no other kernel runs on it)
+}
+
 // LR1: zero the vehicle counts of evicted panes, then (last CTA) free their slots.
 __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   DevState* st = q.state;
@@ -674,7 +708,11 @@ __global__ void __launch_bounds__(kCloseThreads) k_lr1_evict(const QueryDev q) {
   if (ticket(st)) {
     evict_rebuild_cta(q, upto);
     __shared__ int s_rehash;
-    if (threadIdx.x == 0) s_rehash = reclaim && st->n_tomb > (uint32_t)((q.dict.cap_mask + 1) / 4);
+    if (threadIdx.x == 0) {
+      s_rehash = reclaim && dict_must_rehash(q, st);
+      // (the close kernel's finish wrote this batch's report before this kernel ran)
+      q.report->rehash_req = (reclaim && !s_rehash && dict_wants_rehash(q, st)) ? 1u : 0u;
+    }
     __syncthreads();
     if (s_rehash) dict_rehash_cta(q);
     if (threadIdx.x == 0) { st->evicted_upto = upto; st->close_ticket = 0; __threadfence(); }
@@ -781,10 +819,22 @@ void preload_close_kernels() {
   cudaFuncGetAttributes(&fa, k_close_agg);
   cudaFuncGetAttributes(&fa, k_close_lr1);
   cudaFuncGetAttributes(&fa, k_lr1_wcache);
+  cudaFuncGetAttributes(&fa, k_dict_clear);
+  cudaFuncGetAttributes(&fa, k_dict_reinsert);
   cudaFuncGetAttributes(&fa, k_lr1_evict);
   cudaFuncGetAttributes(&fa, k_lr1_wsum);
   cudaFuncGetAttributes(&fa, k_lr1_probe);
   cudaFuncGetAttributes(&fa, k_sum_u32);
+}
+
+static int sm_count_close() {
+  static int nsm = -1;
+  if (nsm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
 }
 
 int close_ctas(const QueryDev& q) {
@@ -799,6 +849,12 @@ int close_ctas(const QueryDev& q) {
   // entries (the merge is load-latency bound, not bandwidth bound)
   // LR1: the closing probe is load-latency bound (two 256-thread CTAs per SM at its register count)
   return q.kind == kLR2S ? 4 * nsm : (q.kind == kLR1S || q.kind == kLR1T) ? 4 * nsm : nsm;
+}
+
+cudaError_t launch_dict_rehash(const QueryDev& q, cudaStream_t st) {
+  k_dict_clear<<<4 * sm_count_close(), kCloseThreads, 0, st>>>(q);
+  k_dict_reinsert<<<4 * sm_count_close(), kCloseThreads, 0, st>>>(q);
+  return cudaGetLastError();
 }
 
 int close_launches(const QueryDev& q) {

@@ -119,6 +119,40 @@ __device__ __forceinline__ uint32_t dict_get_sys(const Dict& d, unsigned long lo
   return kEmpty32;
 }
 
+// NVLS multimem operations on a multicast address (PTX ISA multimem.*: the reduction / store is
+// applied by the NVLink switch to the replica of every device in the multicast group).
+__device__ __forceinline__ void mc_red_add(unsigned long long* mc, unsigned long long v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
+__device__ __forceinline__ void mc_store(unsigned long long* mc, unsigned long long v) {
+  asm volatile("multimem.st.relaxed.sys.global.u64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
+__device__ __forceinline__ void fence_alias() { asm volatile("fence.proxy.alias;" ::: "memory"); }
+__device__ __forceinline__ bool dense_kind(const QueryDev& q) {
+  return q.kind == kLR2S || q.kind == kCM1S || q.kind == kCM1T;
+}
+
+// One partial row into the merge accumulators: NVLS (dense tables, every replica) or the owner's
+// accumulators through peer memory (remote RED.64; CM2 jobIds resolved in the owner's dictionary).
+__device__ __forceinline__ void push_row(const QueryDev& q, DevState* st, const lms_agg_row& r, long long w) {
+  if (q.mc_sum != nullptr && dense_kind(q)) {
+    const uint32_t idx = (uint32_t)r.key;
+    if (idx >= q.K) { atomicAdd(&st->overflow, r.count); return; }
+    const size_t g = (size_t)w * q.K + idx;
+    mc_red_add(q.mc_sum + g, r.sum_fixed);
+    mc_red_add(q.mc_cnt + g, r.count);
+    return;
+  }
+  const PeerView P = q.peers[owner_of(q, r)];
+  uint32_t idx;
+  if (q.kind == kCM2S) idx = dict_get_sys(P.dict, r.key, P.state);
+  else idx = (uint32_t)r.key;
+  if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); return; }
+  const size_t g = (size_t)w * q.K + idx;
+  atomicAdd_system(&P.macc_sum[g], r.sum_fixed);   // remote (peer GPU) RMW: system scope
+  atomicAdd_system(&P.macc_cnt[g], r.count);
+}
+
 __global__ void __launch_bounds__(kThreads) k_p2p_push(const QueryDev q, long long k_lo, uint32_t nwin) {
   DevState* st = q.state;
   const unsigned long long n = st->part_rows;
@@ -128,15 +162,9 @@ __global__ void __launch_bounds__(kThreads) k_p2p_push(const QueryDev q, long lo
     const lms_agg_row r = rows[i];
     const long long w = floor_div(r.win_start_s, (long long)q.S) - k_lo;
     if (w < 0 || w >= (long long)nwin) continue;
-    const PeerView P = q.peers[owner_of(q, r)];
-    uint32_t idx;
-    if (q.kind == kCM2S) idx = dict_get_sys(P.dict, r.key, P.state);
-    else idx = (uint32_t)r.key;
-    if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
-    const size_t g = (size_t)w * q.K + idx;
-    atomicAdd_system(&P.macc_sum[g], r.sum_fixed);   // remote (peer GPU) RMW: system scope
-    atomicAdd_system(&P.macc_cnt[g], r.count);
+    push_row(q, st, r, w);
   }
+  fence_alias();
   __threadfence_system();
 }
 
@@ -190,15 +218,9 @@ __global__ void __launch_bounds__(kThreads) k_p2p_push_async(const QueryDev q) {
     const lms_agg_row r = rows[i];
     const long long w = floor_div(r.win_start_s, (long long)q.S) - k_lo;
     if (w < 0 || w >= (long long)nwin) continue;
-    const PeerView P = q.peers[owner_of(q, r)];
-    uint32_t idx;
-    if (q.kind == kCM2S) idx = dict_get_sys(P.dict, r.key, P.state);
-    else idx = (uint32_t)r.key;
-    if (idx == kEmpty32 || idx >= q.K) { atomicAdd(&st->overflow, r.count); continue; }
-    const size_t g = (size_t)w * q.K + idx;
-    atomicAdd_system(&P.macc_sum[g], r.sum_fixed);   // remote (peer GPU) RMW: system scope
-    atomicAdd_system(&P.macc_cnt[g], r.count);
+    push_row(q, st, r, w);
   }
+  fence_alias();
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&st->p2p_ticket, 1u) == gridDim.x - 1;
@@ -274,6 +296,8 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const QueryDev q, long lo
   DevState* st = q.state;
   if (nwin == 0) close_window(q, k_lo, nwin);
   const uint32_t K = q.kind == kCM2S ? min(st->n_keys, q.K) : q.K;
+  const bool nvls = q.mc_sum != nullptr && dense_kind(q);
+  if (nvls) fence_alias();                     // replica reads after the switch reductions
   lms_agg_row* rows = reinterpret_cast<lms_agg_row*>(q.rows);
   const unsigned long long total = (unsigned long long)nwin * K;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
@@ -286,9 +310,18 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const QueryDev q, long lo
       w = (uint32_t)(i / K);
       key = (uint32_t)(i - (unsigned long long)w * K);
       const size_t g = (size_t)w * q.K + key;
-      s = q.macc_sum[g];
-      c = q.macc_cnt[g];
-      if (c) { q.macc_sum[g] = 0; q.macc_cnt[g] = 0; }
+      if (nvls) {
+        // every replica holds every key: the key's owner emits it and zeroes it everywhere
+        if ((uint32_t)(fmix64((unsigned long long)key) % q.world) == q.rank) {
+          s = q.macc_sum[g];
+          c = q.macc_cnt[g];
+          if (c) { mc_store(q.mc_sum + g, 0ull); mc_store(q.mc_cnt + g, 0ull); }
+        }
+      } else {
+        s = q.macc_sum[g];
+        c = q.macc_cnt[g];
+        if (c) { q.macc_sum[g] = 0; q.macc_cnt[g] = 0; }
+      }
     }
     bool want = c > 0;
     double sum, avg;
@@ -327,13 +360,20 @@ __global__ void __launch_bounds__(32) k_finalize_cm1(const QueryDev q, long long
   if (nwin == 0) close_window(q, k_lo, nwin);
   const uint32_t w = blockIdx.x, c = threadIdx.x;
   if (w >= nwin) return;
+  const bool nvls = q.mc_sum != nullptr;
+  if (nvls) {
+    // every replica holds every instance: the instance's owner (k mod world) ranks it
+    const long long m = (k_lo + (long long)w) % (long long)q.world;
+    if ((uint32_t)(m < 0 ? m + q.world : m) != q.rank) return;
+    fence_alias();
+  }
   __shared__ unsigned long long s_sum[10], s_cnt[10];
   if (c < 10) {
     const size_t g = (size_t)w * q.K + c;
     s_sum[c] = q.macc_sum[g];
     s_cnt[c] = q.macc_cnt[g];
-    q.macc_sum[g] = 0;
-    q.macc_cnt[g] = 0;
+    if (nvls) { mc_store(q.mc_sum + g, 0ull); mc_store(q.mc_cnt + g, 0ull); }
+    else { q.macc_sum[g] = 0; q.macc_cnt[g] = 0; }
   }
   __syncwarp();
   const bool want = c < 10 && s_cnt[c] > 0;

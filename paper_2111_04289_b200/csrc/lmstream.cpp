@@ -5,6 +5,7 @@
 // execution is always the GPU path), Eq. 4 / Eq. 5 metrics, Eq. 10 online InfPT.  Device
 // work per micro-batch: one aggregate-pass launch per <= 16 input segments, one close
 // launch (+ LR1 evict), one 88 B report copy; rows are copied after completion.
+#include <cuda.h>            // driver types only: functions come from cudaGetDriverEntryPoint
 #include <cuda_runtime.h>
 
 #include <array>
@@ -176,6 +177,7 @@ struct lms_query {
   // lms_force_batch instead of being dropped
   lms_status deferred_status = LMS_OK;
   std::string deferred_msg;
+  bool rehash_pending = false;     // a batch report asked for the grid-wide dictionary rebuild
   bool poisoned = false;           // a fused-exchange barrier timed out: ranks may disagree on the
                                    // window state, so every later batch call fails (LMS_ESTATE)
   // single-handle multi-device driver (cfg.num_gpus > 1): one sub-handle (rank g of G) per device;
@@ -186,8 +188,21 @@ struct lms_query {
   std::vector<uint32_t*> g_lr1_w;          // LR1: per sub, the device-summed window counts
   lms_batch_record g_cur{};
   bool g_in_flight = false;
+  // NVLS merge tables (group handles of dense kinds): one multicast object, one physical
+  // replica per distinct device, their unicast mappings and the multicast mapping
+  struct Nvls {
+    bool active = false;
+    CUmemGenericAllocationHandle mc = 0;
+    std::vector<CUmemGenericAllocationHandle> phys;
+    std::vector<CUdeviceptr> uc;
+    std::vector<int> dev;
+    CUdeviceptr mcva = 0;
+    size_t size = 0;
+  } nvls;
+  void nvls_release();
 
   ~lms_query() {
+    nvls_release();
     for (size_t g = 0; g < subs.size(); g++) {
       if (g < g_end.size() && g_end[g]) { cudaSetDevice(subs[g]->cfg.device); cudaEventDestroy(g_end[g]); }
       delete subs[g];
@@ -368,6 +383,11 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
 
   const bool lr = is_lr(q->kind);
   CUDA_TRY(cudaEventRecord(q->F().ev_start, q->stream));
+  if (q->rehash_pending) {          // grid-wide dictionary rebuild asked for by an earlier batch
+    CUDA_TRY(launch_dict_rehash(q->qd, q->stream));
+    q->launches += 2;
+    q->rehash_pending = false;
+  }
   for (size_t s0 = 0; s0 < segs.size(); s0 += kMaxSegs) {
     SegTable t{};
     t.n = (int)std::min<size_t>(kMaxSegs, segs.size() - s0);
@@ -456,6 +476,7 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
     r.h2d_s += ms_h2d * 1e-3;
     f.h2d_async = false;
   }
+  if (rep.rehash_req) q->rehash_pending = true;
   r.num_records = rep.n_records;
   r.device_s = q->last_batch_s;
   r.d2h_s = d2h;
@@ -567,6 +588,173 @@ lms_status push_staged(lms_query* q, const void* src, uint64_t nbytes, double t)
   return LMS_OK;
 }
 
+// ---- NVLS (NVLink SHARP) merge tables --------------------------------------------------
+// Driver API functions resolved at run time (the library links the static CUDA runtime only,
+// so that it loads on hosts without a driver; cudaGetDriverEntryPoint needs a device anyway).
+struct DrvApi {
+  bool ok = false;
+  CUresult (*devAttr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+  CUresult (*devGet)(CUdevice*, int) = nullptr;
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*mcGran)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long) = nullptr;
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+  CUresult (*memGran)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addrFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*memUnmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*memRelease)(CUmemGenericAllocationHandle) = nullptr;
+};
+
+const DrvApi& drv() {
+  static DrvApi d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult qr;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &qr) == cudaSuccess &&
+             qr == cudaDriverEntryPointSuccess && *fn != nullptr;
+    };
+    bool ok = true;
+    ok &= get("cuDeviceGetAttribute", (void**)&d.devAttr);
+    ok &= get("cuDeviceGet", (void**)&d.devGet);
+    ok &= get("cuMulticastCreate", (void**)&d.mcCreate);
+    ok &= get("cuMulticastAddDevice", (void**)&d.mcAddDevice);
+    ok &= get("cuMulticastGetGranularity", (void**)&d.mcGran);
+    ok &= get("cuMulticastBindMem", (void**)&d.mcBindMem);
+    ok &= get("cuMulticastUnbind", (void**)&d.mcUnbind);
+    ok &= get("cuMemCreate", (void**)&d.memCreate);
+    ok &= get("cuMemGetAllocationGranularity", (void**)&d.memGran);
+    ok &= get("cuMemAddressReserve", (void**)&d.addrReserve);
+    ok &= get("cuMemAddressFree", (void**)&d.addrFree);
+    ok &= get("cuMemMap", (void**)&d.memMap);
+    ok &= get("cuMemUnmap", (void**)&d.memUnmap);
+    ok &= get("cuMemSetAccess", (void**)&d.memSetAccess);
+    ok &= get("cuMemRelease", (void**)&d.memRelease);
+    cudaGetLastError();
+    d.ok = ok;
+  });
+  return d;
+}
+
+}  // namespace
+
+void lms_query::nvls_release() {
+  if (nvls.mc == 0 && nvls.phys.empty()) return;
+  const DrvApi& d = drv();
+  if (!d.ok) return;
+  for (size_t i = 0; i < nvls.dev.size(); i++) cudaSetDevice(nvls.dev[i]), cudaDeviceSynchronize();
+  if (nvls.mcva) { d.memUnmap(nvls.mcva, nvls.size); d.addrFree(nvls.mcva, nvls.size); }
+  for (size_t i = 0; i < nvls.uc.size(); i++)
+    if (nvls.uc[i]) { d.memUnmap(nvls.uc[i], nvls.size); d.addrFree(nvls.uc[i], nvls.size); }
+  for (size_t i = 0; i < nvls.dev.size() && nvls.mc; i++) {
+    CUdevice dv;
+    if (d.devGet(&dv, nvls.dev[i]) == CUDA_SUCCESS) d.mcUnbind(nvls.mc, dv, 0, nvls.size);
+  }
+  for (CUmemGenericAllocationHandle h : nvls.phys) if (h) d.memRelease(h);
+  if (nvls.mc) d.memRelease(nvls.mc);
+  nvls = Nvls{};
+}
+
+namespace {
+
+// Build the NVLS merge tables of a group handle (dense kinds): returns false (and leaves the
+// owner-push exchange in place) when a device lacks switch multicast or any driver call fails.
+bool nvls_setup(lms_query* q, const std::vector<int>& ids) {
+  const DrvApi& d = drv();
+  if (!d.ok) return false;
+  std::vector<int> devs;
+  for (int id : ids) if (std::find(devs.begin(), devs.end(), id) == devs.end()) devs.push_back(id);
+  for (int id : devs) {
+    CUdevice dv;
+    int mc = 0;
+    if (d.devGet(&dv, id) != CUDA_SUCCESS || d.devAttr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dv) != CUDA_SUCCESS || !mc)
+      return false;
+  }
+  const QueryDev& d0 = q->subs[0]->qd;
+  const size_t half = (size_t)d0.Wmerge * d0.K * sizeof(unsigned long long);
+  lms_query::Nvls& n = q->nvls;
+  auto fail_out = [&]() { q->nvls_release(); cudaGetLastError(); return false; };
+  // one process: no shareable handle is needed, but a driver may insist on one — try in order
+  const CUmemAllocationHandleType types[3] = {CU_MEM_HANDLE_TYPE_NONE, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                              CU_MEM_HANDLE_TYPE_FABRIC};
+  CUmulticastObjectProp mp{};
+  CUmemAllocationProp ap{};
+  size_t gran = 0, size = 0;
+  for (CUmemAllocationHandleType ht : types) {
+    mp = CUmulticastObjectProp{};
+    mp.numDevices = (unsigned int)devs.size();
+    mp.size = 2 * half;
+    mp.handleTypes = ht;
+    ap = CUmemAllocationProp{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = devs[0];
+    ap.requestedHandleTypes = ht;
+    size_t mg = 0, pg = 0;
+    if (d.mcGran(&mg, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || mg == 0 ||
+        d.memGran(&pg, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || pg == 0)
+      continue;
+    gran = std::max(mg, pg);
+    size = (mp.size + gran - 1) / gran * gran;
+    mp.size = size;
+    if (d.mcCreate(&n.mc, &mp) == CUDA_SUCCESS) break;
+    n.mc = 0;
+  }
+  if (n.mc == 0) { cudaGetLastError(); return false; }
+  n.size = size;
+  n.dev = devs;
+  for (int id : devs) {                                   // every device joins before any binds
+    CUdevice dv;
+    if (d.devGet(&dv, id) != CUDA_SUCCESS || d.mcAddDevice(n.mc, dv) != CUDA_SUCCESS) return fail_out();
+  }
+  for (int id : devs) {
+    ap.location.id = id;
+    CUmemGenericAllocationHandle ph = 0;
+    if (d.memCreate(&ph, size, &ap, 0) != CUDA_SUCCESS) return fail_out();
+    n.phys.push_back(ph);
+    if (d.mcBindMem(n.mc, 0, ph, 0, size, 0) != CUDA_SUCCESS) return fail_out();
+    CUdeviceptr va = 0;
+    if (d.addrReserve(&va, size, gran, 0, 0) != CUDA_SUCCESS) return fail_out();
+    n.uc.push_back(va);
+    if (d.memMap(va, size, 0, ph, 0) != CUDA_SUCCESS) return fail_out();
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = id;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if (d.memSetAccess(va, size, &acc, 1) != CUDA_SUCCESS) return fail_out();
+    if (cudaSetDevice(id) != cudaSuccess || cudaMemset((void*)va, 0, size) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess)
+      return fail_out();
+  }
+  if (d.addrReserve(&n.mcva, size, gran, 0, 0) != CUDA_SUCCESS) { n.mcva = 0; return fail_out(); }
+  if (d.memMap(n.mcva, size, 0, n.mc, 0) != CUDA_SUCCESS) return fail_out();
+  std::vector<CUmemAccessDesc> acc(devs.size());
+  for (size_t i = 0; i < devs.size(); i++) {
+    acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc[i].location.id = devs[i];
+    acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  }
+  if (d.memSetAccess(n.mcva, size, acc.data(), acc.size()) != CUDA_SUCCESS) return fail_out();
+  // every sub-handle: its device's replica as the merge accumulators, the multicast address
+  // for the pushes / zeroing (virtual shards on one device share that device's replica)
+  for (size_t g = 0; g < q->subs.size(); g++) {
+    const size_t i = std::find(devs.begin(), devs.end(), ids[g]) - devs.begin();
+    QueryDev& sd = q->subs[g]->qd;
+    sd.macc_sum = reinterpret_cast<unsigned long long*>(n.uc[i]);
+    sd.macc_cnt = reinterpret_cast<unsigned long long*>(n.uc[i] + half);
+    sd.mc_sum = reinterpret_cast<unsigned long long*>(n.mcva);
+    sd.mc_cnt = reinterpret_cast<unsigned long long*>(n.mcva + half);
+  }
+  n.active = true;
+  return true;
+}
+
 lms_status group_create(const lms_config* cfg, lms_query** out) {
   lms_query* q = new (std::nothrow) lms_query();
   if (!q) return fail(LMS_ENOMEM, "host alloc");
@@ -626,6 +814,10 @@ lms_status group_create(const lms_config* cfg, lms_query** out) {
         if (lms_status st = lms_p2p_import_local(a, b)) return bail(st);
     for (lms_query* a : q->subs)
       if (lms_status st = lms_p2p_device_watermark(a, 1)) return bail(st);
+    // dense tables (LR2, CM1) with LMS_FLAG_NVLS: reduce the partials in the NVLink switch when
+    // every device can join a multicast object (else the owner push stays)
+    const bool dense = q->kind == kLR2S || q->kind == kCM1S || q->kind == kCM1T;
+    if (dense && (cfg->flags & LMS_FLAG_NVLS)) nvls_setup(q, ids);
   } else {
     for (lms_query* a : q->subs) {
       uint32_t* w = nullptr;
@@ -1515,6 +1707,12 @@ lms_status lms_p2p_import_local(lms_query* q, lms_query* peer) {
   } catch (...) {
     return fail(LMS_EINTERNAL, "exception in p2p_import_local");
   }
+}
+
+lms_status lms_nvls_active(lms_query* q, int32_t* active) {
+  if (!q || !active) return fail(LMS_EINVAL, "null argument");
+  *active = q->nvls.active ? 1 : 0;
+  return LMS_OK;
 }
 
 lms_status lms_last_close_range(lms_query* q, int64_t* k_first, int64_t* k_last) {

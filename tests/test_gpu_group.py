@@ -79,3 +79,70 @@ def test_group_config_checks():
         with pytest.raises(P.LmsError):
             from paper_2111_04289_b200.dist import RankHandle
             RankHandle(q)                                            # no caller-side protocol
+
+
+def _multicast_object_possible():
+    """Whether this box lets device 0 create a multicast object (CU_DEVICE_ATTRIBUTE_MULTICAST_
+    SUPPORTED and cuMulticastCreate through ctypes; a single-GPU container may report the
+    attribute but refuse the object)."""
+    import ctypes as C
+    try:
+        cu = C.CDLL("libcuda.so.1")
+    except OSError:
+        return False
+    if cu.cuInit(0) != 0:
+        return False
+    dev, v = C.c_int(), C.c_int()
+    if cu.cuDeviceGet(C.byref(dev), 0) != 0 or cu.cuDeviceGetAttribute(C.byref(v), 132, dev) != 0 or not v.value:
+        return False
+
+    class Prop(C.Structure):
+        _fields_ = [("numDevices", C.c_uint), ("size", C.c_size_t), ("handleTypes", C.c_ulonglong),
+                    ("flags", C.c_ulonglong)]
+    for ht in (0, 1, 8):
+        p = Prop(1, 2 << 20, ht, 0)
+        h = C.c_ulonglong()
+        if cu.cuMulticastCreate(C.byref(h), C.byref(p)) == 0:
+            cu.cuMemRelease(h)
+            return True
+    return False
+
+
+def _nvls_active(qname, **cfg):
+    import ctypes as C
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    with P.Query(qname, mode="manual", **cfg) as q:
+        a = C.c_int32()
+        L.check(L.lms_nvls_active(q.h, C.byref(a)), "lms_nvls_active")
+        return a.value
+
+
+@pytest.mark.parametrize("qname,traffic,secs,bs,G", [
+    ("LR2S", "B(1.7)", 45, [3, 7, 1, 10, 4], 2),
+    ("LR2S", "R(0.5,2)", 40, [9, 9, 9], 3),
+    ("CM1S", "B(0.9)", 75, [10, 10, 3, 20], 2),
+    ("CM1T", "U(0.5)", 130, [30, 30, 60], 3),
+])
+def test_group_nvls_dense_merge(qname, traffic, secs, bs, G):
+    """Dense tables (LR2, CM1) merged through NVLS: the close's partial rows are reduced in the
+    NVLink switch into every device's replica of one multicast object (multimem.red), owners
+    finalize from their replica and zero their keys everywhere (multimem.st).  On a device with
+    switch multicast the group handle with LMS_FLAG_NVLS must take that path; without the flag
+    (or where no multicast object can be created) the owner push — both against the oracle."""
+    from paper_2111_04289_b200 import _lib as L
+    fam = qname[:2]
+    params = g.CMParams(num_jobs=200) if fam == "CM" else None
+    data = stream(fam, traffic, secs, params=params)
+    batches, i = [], 0
+    for n in bs:
+        batches.append(data[i:i + n])
+        i += n
+    if i < len(data):
+        batches.append(data[i:])
+    want = oracle_rows(qname, batches)
+    assert _nvls_active(qname, device_ids=[0] * G, flags=L.LMS_FLAG_NVLS) == (1 if _multicast_object_possible() else 0)
+    assert _nvls_active(qname, device_ids=[0] * G) == 0
+    assert _nvls_active("CM2S", device_ids=[0] * G, flags=L.LMS_FLAG_NVLS) == 0   # sparse keys: owner push
+    compare_run(qname, product_run(qname, batches, device_ids=[0] * G, flags=L.LMS_FLAG_NVLS), want)
+    compare_run(qname, product_run(qname, batches, device_ids=[0] * G), want)

@@ -155,6 +155,12 @@ def summarize(name, s, target=None, exclude_flush=True):
            "processing_records_per_s": nrec / sum(dv) if dv and sum(dv) > 0 else None,
            "bad_records": sum(r["bad_records"] for r in s.recs),
            "late_records": sum(r["late_records"] for r in s.recs)}
+    if len(recs) <= 64:                       # short configs: the per-batch series too
+        out["per_batch"] = {"device_ms": [1e3 * x for x in dv], "proc_ms": [1e3 * x for x in pr],
+                            "records": [r["num_records"] for r in recs],
+                            "rows": [r["rows_emitted"] for r in recs]}
+    if pr:
+        out["proc_p99_over_p50"] = pct(pr, 99) / pct(pr, 50)
     if target is not None:
         out["target_s"] = target
         # strict (MaxLat > target): Alg. 1 admits at the first 10 ms poll where EstMaxLat >= target
