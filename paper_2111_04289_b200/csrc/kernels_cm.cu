@@ -484,14 +484,13 @@ __device__ __forceinline__ bool cm_fast(uint32_t buf_s, uint32_t cm_s, uint32_t 
   const uint32_t S = kCmHaloL + sb;
   const uint32_t L = e - sb;
   bool ok = L - 128u <= 63u;
-  // ---- exactly 12 commas in [sb, e): head [sb, sb+64) + middle [sb+64, e-64) + tail [e-64, e)
+  // ---- comma windows: head [sb, sb+64), middle [sb+64, e-64), tail [e-64, e)
   const uint32_t wa = cm_s + 4u * (sb >> 5);
   const uint32_t sh = sb & 31u;
   const uint32_t v0 = lds32(wa), v1 = lds32(wa + 4), v2 = lds32(wa + 8), v3 = lds32(wa + 12), v4 = lds32(wa + 16);
   const uint32_t h0 = __funnelshift_r(v0, v1, sh), h1 = __funnelshift_r(v1, v2, sh);
   const unsigned long long mid = (((unsigned long long)__funnelshift_r(v3, v4, sh) << 32) | __funnelshift_r(v2, v3, sh)) &
                                  ((1ull << min(L - 128u, 63u)) - 1ull);          // bits [sb+64, e-64)
-  const uint32_t m0 = (uint32_t)mid, m1 = (uint32_t)(mid >> 32);
   // e clamped into the window for addressing only (e = 0xFFFF: no '\n' in reach; L above
   // already rejects it): with S <= 16 + 4096 and o0, a4, q7 < 35 every load below stays
   // inside the stage, so no address needs its own clamp
@@ -500,7 +499,6 @@ __device__ __forceinline__ bool cm_fast(uint32_t buf_s, uint32_t cm_s, uint32_t 
   const uint32_t ua = cm_s + 4u * (tp >> 5);
   const uint32_t tsh = tp & 31u, u0 = lds32(ua), u1 = lds32(ua + 4), u2 = lds32(ua + 8);
   const uint32_t t0 = __funnelshift_r(u0, u1, tsh), t1 = __funnelshift_r(u1, u2, tsh);
-  ok &= __popc(h0) + __popc(h1) + __popc(m0) + __popc(m1) + __popc(t0) + __popc(t1) == 12u;
   // ---- head: c0 = sb + o0 ends ts (1..8 digits); c1 = c0 + 1 (empty field 1); c2 = c0 + 12
   // (10-digit jobId); then taskIndex, machineId free-form: c4 = the 2nd comma after c2, and
   // eventType is 1 character: the next comma (c5) is at c4 + 2.
@@ -512,6 +510,13 @@ __device__ __forceinline__ bool cm_fast(uint32_t buf_s, uint32_t cm_s, uint32_t 
   const uint32_t x = rr & (rr - 1u);                              // c3 cleared
   const uint32_t a4 = lsb32(x | 0x80000000u);                     // c4 = c2 + 1 + a4
   ok &= x != 0u && a4 <= 29u && ((x >> a4) & 7u) == 5u;
+  // ---- exactly 12 commas: the head checks pin c0..c5 as the only commas in [sb, c5] and the
+  // tail checks below pin c6..c11 as the only ones in window bits [30, 64) = [e-34, e), so the
+  // record has 13 fields iff no comma lies after c5 in the head window, none in the middle
+  // [sb+64, e-64), and none in tail bits [0, 30) (c5 <= sb + 52 < the tail's start: L >= 128)
+  const unsigned long long head = ((unsigned long long)h1 << 32) | h0;
+  const unsigned long long after_c5 = head >> ((o0 + 16u + a4) & 63u);
+  ok &= ((after_c5 | mid) == 0ull) & ((t0 & 0x3FFFFFFFu) == 0u);
   // ---- tail, window [e-64, e): commas exactly at e-29, e-20, e-11, e-2 within [e-30, e)
   // (cpu, ram, disk 8 chars, constraint 1 char); c7 (priority end) at e-31 or e-32 and
   // c6 = c7 - 2 (1-char category): window bits 30..34 = 0b01010 or 0b00101.
