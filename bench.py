@@ -572,6 +572,12 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
+        # NCCL's communicator setup (ranks, NVLink / NVLS transports) goes to stderr, so a
+        # scaling run's log shows how many ranks each communicator had; stdout keeps the one
+        # JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:

@@ -6,26 +6,29 @@
 // variable)"; operators Scan (CSV) / Filtering / Projection / Aggregation (Table III).
 // Record grammar: DESIGN.md reading R1 (13-column task_events line, <= 255 B + '\n').
 //
-// Design (B200).  A tile is a 16 KB window = 16128 B payload + 256 B right halo (the tail of
-// the last record that STARTS in the payload: a record belongs to the tile holding its first
-// byte) + a 16 B left halo (the byte before the tile).  Persistent CTAs (128 threads, 5 per
-// SM) walk a contiguous tile range through a 2-stage smem ring filled by TMA-engine bulk
-// copies (cp.async.bulk).
-//  * Pass 1 (all threads, round-robin 16 B pieces: conflict-free LDS.128): exact SWAR byte
-//    equality against '\n' and ',' (3 ops per class per word + a shared AND), gathered to one
-//    mask bit per byte with IDP.4A; masks go to smem.
-//  * Pass 2: thread t owns window chunk t (128 B): record starts = byte after a '\n'.
-//  * Pass 3, per record: the '\n' is the first newline bit of a 192-bit window; the 12 commas
-//    are counted with POPC; commas 0..5 are the 6 lowest bits of the 64-bit window at the
-//    record start, commas 6..11 the 6 highest bits of the 64-bit window ending at the '\n'
-//    (FLO), which covers every record of 130..255 B with the usual field widths; anything
-//    else (or any short line) takes an exact byte-serial path.  ts / eventType / category
-//    are parsed from smem bytes, the 10-digit jobId and the cpu field with SWAR arithmetic.
-//  * CM2: eventType == 1 survivors are compacted with warp ballots into a per-warp smem
-//    list and processed 32 at a time by full warps (dictionary jobId -> index, two RED.64
-//    into the pane accumulators) — no CTA barrier on the dependent-latency path.
-//    CM1: per-warp ballot/REDUX reduction per (pane, category) into per-warp smem
-//    accumulators, one RED.64 pair per CTA and key at the end.
+// Design (B200).  Persistent CTAs of 4 warps, 5 CTAs per SM.  Every WARP walks its own
+// contiguous range of warp tiles through a private 2-stage smem ring filled by TMA-engine bulk
+// copies (cp.async.bulk, L2 evict-first), so no CTA barrier sits in the loop.  A warp tile is a
+// 4352 B window = 4096 B payload + 256 B right halo (the tail of the last record that STARTS in
+// the payload: a record belongs to the tile holding its first byte) + a 16 B left halo (the
+// byte before the tile).  The producer (lane 0) issues a tile two tiles ahead and packs its
+// geometry into one register word; every lane waits on the stage's mbarrier.
+//  * Pass 1 (lane l: 32 B words l, l+32, ...; conflict-free LDS.128): exact SWAR byte equality
+//    against '\n' and ',' (3 ops per 4-byte word and class), gathered to one mask bit per byte
+//    with IDP.4A chains; the masks go to per-warp smem.  The right halo's masks are the next
+//    tile's first 256 B: carried over, so a tile classifies exactly 4096 new bytes.
+//  * Pass 2: lane l owns payload chunk l (128 B); records are owned by the '\n' before them;
+//    a record's '\n' is the first one of chunk l+1 or l+2 (shuffles, branch-free first-bit).
+//  * Pass 3, per record (one per lane per round, branch-free fast path cm_fast for the usual
+//    shape): the 12 commas are pinned by bit tests in a 64-bit head window at the record start
+//    and a 64-bit tail window ending at the '\n', plus zero tests of the windows between them;
+//    ts / jobId / cpu digits are validated and valued with SWAR arithmetic on 32-bit
+//    shared-window loads.  Any other shape (or a malformed line) takes the exact general paths
+//    (cm_parse, cm_parse_serial), so every byte sequence gets the oracle's answer.
+//  * CM2: eventType == 1 survivors are ballot-compacted into a per-warp smem ring as SWAR digit
+//    words and decoded / aggregated 32 at a time by full warps (dictionary jobId -> index, two
+//    RED.64 into the striped pane accumulators).  CM1: per-warp ballot/REDUX reduction per
+//    (pane, category) into per-warp smem accumulators, one RED.64 pair per CTA and key.
 #include "common.cuh"
 
 #include <mutex>
