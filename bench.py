@@ -173,7 +173,7 @@ class Runner:
         if world > 1:
             from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange
             self.h, self.ex = RankHandle(self.q), TorchDistExchange()
-            if p2p:
+            if p2p and p2p != "dense":
                 self.ex.setup_p2p([self.h], device_watermark=p2p == "device")
 
     def batch(self, t, sync):
@@ -549,11 +549,12 @@ def main():
                     help="micro-batches of the e2e Proc p50/p99 loop (0 = skip)")
     ap.add_argument("--seed", type=int, default=211104289)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "p2p", "p2p-async", "device"],
-                    help="N > 1: partial-aggregate exchange (NCCL all-to-all + owner merge; the fused "
-                         "peer-memory push into the owners' accumulators with host-driven passes; or "
-                         "the same fully enqueued with a device-side barrier; or also the watermark "
-                         "exchange on the device: no per-batch collective)")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "alltoall", "dense", "p2p", "p2p-async", "device"],
+                    help="N > 1: partial-aggregate exchange (auto: dense for LR2 / CM1, alltoall for CM2; "
+                         "NCCL all-to-all + owner merge; one SUM all-reduce of the dense [instances][K] "
+                         "partials (LR2 / CM1); the fused peer-memory push into the owners' accumulators "
+                         "with host-driven passes; or the same fully enqueued with a device-side barrier; "
+                         "or also the watermark exchange on the device: no per-batch collective)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -586,7 +587,12 @@ def main():
     pct = P.percentile                  # nearest rank, computed by the library
 
     scaling = args.scaling if world > 1 else "weak"
-    p2p = {"alltoall": False, "p2p": True, "p2p-async": "async", "device": "device"}[args.exchange]
+    def exchange_mode(w):
+        choice = args.exchange
+        if choice == "auto":
+            choice = "dense" if w["kind"] in ("LR2S", "CM1S", "CM1T") else "alltoall"
+        return {"alltoall": False, "dense": "dense", "p2p": True, "p2p-async": "async", "device": "device"}[choice]
+    p2p = exchange_mode(wl)
     seed = args.seed
     res = device_run(wl, args.steps, args.warmup, seed, rank, world, torch, dist, p2p, scaling)
     el = res["elapsed_s"]
@@ -606,7 +612,8 @@ def main():
     sec = None
     if args.secondary and args.secondary != args.workload:
         w2 = WORKLOADS[args.secondary]
-        r2 = device_run(w2, max(5, args.steps // 2), args.warmup, seed, rank, world, torch, dist, p2p, scaling)
+        r2 = device_run(w2, max(5, args.steps // 2), args.warmup, seed, rank, world, torch, dist, exchange_mode(w2),
+                        scaling)
         if world > 1:
             r2["elapsed_s"] = max_over_ranks(r2["elapsed_s"], torch, dist)
         a2 = statistics.mean(r2["agg_s"])
@@ -620,7 +627,7 @@ def main():
                "close_kernel_ms_mean": 1e3 * statistics.mean(r2["close_s"]),
                "clocks": r2["clocks"], "gpu_launches": r2["launches"]}
         if args.latency_batches > 0:
-            d2, _ = latency_run(w2, args.latency_batches, seed, rank, world, torch, dist, p2p, scaling)
+            d2, _ = latency_run(w2, args.latency_batches, seed, rank, world, torch, dist, exchange_mode(w2), scaling)
             sec["batch_latency_ms"] = {"batches": len(d2), "device_p50": 1e3 * pct(d2, 50),
                                        "device_p99": 1e3 * pct(d2, 99)}
     e2e = None

@@ -362,6 +362,22 @@ lms_status  lms_p2p_device_watermark(lms_query* q, int32_t enable);
  * in all replicas with multimem.st — no owner push, no all-to-all.  0: the owner-push exchange
  * (no LMS_FLAG_NVLS, a device that cannot join a multicast object, CM2S / LR1, one GPU).   */
 lms_status  lms_nvls_active(lms_query* q, int32_t* active);
+/* Dense exchange (the small key sets — LR2 2000 keys, CM1 10 categories — are
+ * reduced as dense arrays, PAPER.md P:751 / P:962 "shuffle"): after lms_run_close + lms_sync
+ * of a batch that closed instances, for each merge window [k_lo, k_lo + nwin) (nwin <= the
+ * merge window, lms_merge_window; instances from lms_last_close_range):
+ *   lms_dense_partials  adds THIS rank's partial rows of those instances (all keys) into its
+ *                       merge accumulators and returns them: *sum_dptr / *cnt_dptr = u64
+ *                       [nwin][K] device arrays (row-major, K = the query's key space) of
+ *                       *n_elems = nwin * K elements, owned by the library;
+ *   (the caller SUM-all-reduces both arrays over the ranks, on the library's stream)
+ *   lms_dense_finalize  rank 0 finalizes every key (AVG, HAVING avg < 40, CM1 rank) into its
+ *                       row FIFO (rows_emitted of the batch record) and clears its arrays; the
+ *                       other ranks clear theirs and emit nothing.
+ * ESTATE: not a multi-GPU LR2S / CM1S / CM1T handle, or batch not complete; EINVAL: nwin.   */
+lms_status  lms_dense_partials(lms_query* q, int64_t k_lo, uint32_t nwin, void** sum_dptr, void** cnt_dptr,
+                               uint64_t* n_elems);
+lms_status  lms_dense_finalize(lms_query* q, int64_t k_lo, uint32_t nwin);
 
 /* Multi-GPU LR1 (LR1S / LR1T with world > 1; Table IV, reading R8).  Vehicles
  * index the per-pane counts directly (VID < max_keys; a larger VID is rejected: LMS_EINVAL), every

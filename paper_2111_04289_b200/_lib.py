@@ -126,6 +126,8 @@ _PROTOS = {
     "lms_p2p_collect": (C.c_int32, [_Q]),
     "lms_p2p_device_watermark": (C.c_int32, [_Q, C.c_int32]),
     "lms_nvls_active": (C.c_int32, [_Q, _P(C.c_int32)]),
+    "lms_dense_partials": (C.c_int32, [_Q, C.c_int64, C.c_uint32, _P(C.c_void_p), _P(C.c_void_p), _P(C.c_uint64)]),
+    "lms_dense_finalize": (C.c_int32, [_Q, C.c_int64, C.c_uint32]),
     "lms_split": (C.c_int32, [C.c_int32, C.c_void_p, C.c_uint64, C.c_uint32, _P(C.c_uint64)]),
     "lms_last_kernel_times": (C.c_int32, [_Q, _P(C.c_double), _P(C.c_double), _P(C.c_double)]),
     "lms_kernel_launches": (C.c_int32, [_Q, _P(C.c_uint64)]),

@@ -199,6 +199,8 @@ cudaError_t launch_sum_u32(uint32_t* dst, const uint32_t* const* srcs, uint32_t 
 cudaError_t launch_bucket(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st);
+cudaError_t launch_merge_rows(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
+                              uint32_t nwin, cudaStream_t st);   // k_merge only (no finalize)
 cudaError_t launch_p2p_push(const QueryDev& q, long long k_lo, uint32_t nwin, cudaStream_t st);
 cudaError_t launch_p2p_exchange_async(const QueryDev& q, cudaStream_t st);
 cudaError_t launch_wm_exchange(const QueryDev& q, cudaStream_t st);

@@ -709,6 +709,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const uint32_t st_s = stage_s + s * (uint32_t)kCmStage;    // stage base (shared window)
     const uint8_t* buf = wsmem + s * kCmStage;
     mbar_wait_s(full_s + 8u * s, ph);                           // every lane: TMA bytes visible
+    __syncwarp();                                               // lane 0's remainder bytes (tail tiles)
     const uint32_t hi_bits = geo_hibits(geo);                   // mask bits beyond are invalid
     // ---- Pass 1: exact '\n' / ',' masks, one 32-bit mask word (32 B) per lane per step.
     // Window bits [0, 256) are the previous tile's halo masks when the tile continues the

@@ -456,6 +456,12 @@ cudaError_t launch_p2p_exchange_async(const QueryDev& q, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_merge_rows(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
+                              uint32_t nwin, cudaStream_t st) {
+  k_merge<<<sm_count(), kThreads, 0, st>>>(q, static_cast<const lms_agg_row*>(rows), n, k_lo, nwin);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_merge(const QueryDev& q, const void* rows, unsigned long long n, long long k_lo,
                          uint32_t nwin, cudaStream_t st) {
   if (n) k_merge<<<sm_count(), kThreads, 0, st>>>(q, static_cast<const lms_agg_row*>(rows), n, k_lo, nwin);

@@ -1862,6 +1862,52 @@ lms_status merge_pass(lms_query* q, const void* rows, uint64_t n, long long k_lo
   }
 }
 
+// Dense exchange for the small key sets (LR2: 2000 keys, CM1: 10 categories; SURVEY §8(e):
+// ReduceScatter / AllReduce of dense arrays instead of an all-to-all of partial rows).
+lms_status lms_dense_partials(lms_query* q, int64_t k_lo, uint32_t nwin, void** sum_dptr, void** cnt_dptr,
+                              uint64_t* n_elems) {
+  try {
+    if (!q || !sum_dptr || !cnt_dptr || !n_elems) return fail(LMS_EINVAL, "null argument");
+    if (q->qd.world < 2 || !(q->kind == kLR2S || q->kind == kCM1S || q->kind == kCM1T))
+      return fail(LMS_ESTATE, "dense exchange: multi-GPU LR2S / CM1S / CM1T handles only");
+    if (q->in_flight || q->awaiting_close) return fail(LMS_ESTATE, "batch not complete (call lms_sync)");
+    if (nwin == 0 || nwin > q->qd.Wmerge) return fail(LMS_EINVAL, "nwin must be in [1, merge window]");
+    CUDA_TRY(cudaSetDevice(q->cfg.device));
+    if (k_lo == q->last_report.close_k_first && !q->records.empty()) q->records.back().rows_emitted = 0;
+    // this rank's partial rows of the instances (every owner's) -> its merge accumulators
+    const uint64_t n = q->last_report.part_rows;
+    if (n) {
+      CUDA_TRY(launch_merge_rows(q->qd, q->qd.send_rows, n, k_lo, nwin, q->stream));
+      q->launches++;
+    }
+    *sum_dptr = q->qd.macc_sum;
+    *cnt_dptr = q->qd.macc_cnt;
+    *n_elems = (uint64_t)nwin * q->qd.K;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in dense_partials");
+  }
+}
+
+lms_status lms_dense_finalize(lms_query* q, int64_t k_lo, uint32_t nwin) {
+  try {
+    if (!q) return fail(LMS_EINVAL, "null query");
+    if (q->qd.world < 2 || !(q->kind == kLR2S || q->kind == kCM1S || q->kind == kCM1T))
+      return fail(LMS_ESTATE, "dense exchange: multi-GPU LR2S / CM1S / CM1T handles only");
+    if (nwin == 0 || nwin > q->qd.Wmerge) return fail(LMS_EINVAL, "nwin must be in [1, merge window]");
+    if (q->qd.rank == 0) return merge_pass(q, nullptr, 0, k_lo, nwin);   // finalize (AVG, HAVING, rank)
+    CUDA_TRY(cudaSetDevice(q->cfg.device));                              // the others: zero their copy
+    const size_t bytes = (size_t)nwin * q->qd.K * sizeof(unsigned long long);
+    CUDA_TRY(cudaMemsetAsync(q->qd.macc_sum, 0, bytes, q->stream));
+    CUDA_TRY(cudaMemsetAsync(q->qd.macc_cnt, 0, bytes, q->stream));
+    CUDA_TRY(cudaStreamSynchronize(q->stream));
+    if (!q->records.empty()) q->records.back().rows_emitted = 0;
+    return LMS_OK;
+  } catch (...) {
+    return fail(LMS_EINTERNAL, "exception in dense_finalize");
+  }
+}
+
 lms_status lms_merge(lms_query* q, const void* rows, uint64_t n) {
   if (!q || (n && !rows)) return fail(LMS_EINVAL, "null argument");
   if (q->qd.world < 2 || is_lr1(q->kind)) return fail(LMS_ESTATE, "not a multi-GPU aggregate handle");

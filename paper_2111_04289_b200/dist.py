@@ -161,6 +161,17 @@ class RankHandle:
     def sync(self) -> int:
         return self.q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT, L.LMS_EOVERFLOW))
 
+    # ---- dense exchange (LR2S / CM1*: small key sets reduced as dense arrays)
+    def dense_partials(self, k_lo: int, nwin: int):
+        """int64 device views of this rank's merge accumulators [nwin][K] (sums, counts) after
+        its own partial rows of instances [k_lo, k_lo + nwin) were added (all-reduce: SUM)."""
+        s, c, n = C.c_void_p(), C.c_void_p(), C.c_uint64()
+        check(L.lms_dense_partials(self.q.h, k_lo, nwin, C.byref(s), C.byref(c), C.byref(n)), "lms_dense_partials")
+        return device_view(s.value, n.value * 8, "i8"), device_view(c.value, n.value * 8, "i8")
+
+    def dense_finalize(self, k_lo: int, nwin: int):
+        return check(L.lms_dense_finalize(self.q.h, k_lo, nwin), "lms_dense_finalize", (L.LMS_OK, L.LMS_EOVERFLOW))
+
     def merge(self, rows_u8):
         n = rows_u8.numel() // ROW_BYTES
         ptr = rows_u8.data_ptr() if n else None
@@ -241,6 +252,13 @@ class TorchDistExchange:
         with self._on(h):
             self._all_reduce(t, self.dist.ReduceOp.SUM)
 
+    def allreduce_dense(self, handles, arrays):
+        """In-place SUM all-reduce of arrays[0] = (sums, counts) on the handle's stream."""
+        (h,), ((sums, cnts),) = handles, arrays
+        with self._on(h):
+            self._all_reduce(sums, self.dist.ReduceOp.SUM)
+            self._all_reduce(cnts, self.dist.ReduceOp.SUM)
+
     def all_to_all(self, handles, sends):
         """sends[0] = (uint8 rows tensor grouped by owner, per-owner counts) -> received rows."""
         import torch
@@ -268,6 +286,8 @@ class _Null:
 
 def run_batch(handles, exchange, now: float, flush: bool = False, p2p=False) -> list[int]:
     """One micro-batch on every local handle (steps 1-6 above; LR1: close_lr1's steps).
+    p2p="dense" (LR2S / CM1*): the partial sums are reduced as dense [instances][K] arrays with
+    one SUM all-reduce per merge window (SURVEY §8(e): small key sets) and rank 0 finalizes;
     p2p=True: fused exchange (exchange.setup_p2p done once) instead of all-to-all + lms_merge,
     host-driven passes; p2p="async": the same exchange fully enqueued behind the close with a
     device-side barrier (one host synchronisation per batch); p2p="device": in addition the
@@ -288,6 +308,9 @@ def run_batch(handles, exchange, now: float, flush: bool = False, p2p=False) -> 
         return _exchange_async(handles, exchange)
     sts = [h.sync() for h in handles]
     if handles[0].windows_closed() == 0:   # same on every rank: nothing to exchange (most batches)
+        return sts
+    if p2p == "dense":
+        exchange_dense(handles, exchange)
         return sts
     if p2p:
         exchange_p2p(handles, exchange)
@@ -314,6 +337,20 @@ def exchange_p2p(handles, exchange, k_from=None):
         for h in handles:
             h.p2p_finalize(k, nwin)
         exchange.barrier(handles)
+
+
+def exchange_dense(handles, exchange):
+    """Dense exchange of the last close's instances, one merge window at a time."""
+    k0, k1 = handles[0].last_close_range()
+    wmerge = handles[0].merge_window()
+    k = k0
+    while k <= k1:
+        nwin = min(wmerge, k1 - k + 1)
+        arrays = [h.dense_partials(k, nwin) for h in handles]
+        exchange.allreduce_dense(handles, arrays)
+        for h in handles:
+            h.dense_finalize(k, nwin)
+        k += nwin
 
 
 def _exchange_async(handles, exchange):

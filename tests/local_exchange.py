@@ -43,6 +43,15 @@ class LocalExchange:
             t.copy_(tot)
         torch.cuda.synchronize()
 
+    def allreduce_dense(self, handles, arrays):
+        import torch
+        torch.cuda.synchronize()
+        for i in range(2):
+            tot = torch.stack([a[i] for a in arrays]).sum(0, dtype=arrays[0][i].dtype)
+            for a in arrays:
+                a[i].copy_(tot)
+        torch.cuda.synchronize()
+
     def all_to_all(self, handles, sends):
         import torch
         world = len(handles)

@@ -98,6 +98,70 @@ def test_gloo_world2_exchange():
         assert sorted(map(bytes, got)) == sorted(map(bytes, want))   # exactly the rows it owns
 
 
+class FakeDenseHandle:
+    """CPU stand-in for a dense (LR2 / CM1) RankHandle: per merge window, this rank's partial
+    [nwin][K] sums / counts; rank 0 "finalizes" (records what the all-reduce gave it)."""
+
+    def __init__(self, rank, k0, k1, wmerge, K, seed):
+        self.rank, self.k0, self.k1, self.wmerge, self.K = rank, k0, k1, wmerge, K
+        self.stream_ptr = 0
+        self.rng = np.random.default_rng(seed)
+        self.sent, self.final = {}, {}
+
+    def last_close_range(self):
+        return self.k0, self.k1
+
+    def merge_window(self):
+        return self.wmerge
+
+    def dense_partials(self, k_lo, nwin):
+        s = torch.from_numpy(self.rng.integers(0, 1000, nwin * self.K).astype(np.int64))
+        c = torch.from_numpy(self.rng.integers(0, 5, nwin * self.K).astype(np.int64))
+        self.sent[k_lo] = (s.clone(), c.clone())
+        self._cur = (s, c)
+        return s, c
+
+    def dense_finalize(self, k_lo, nwin):
+        s, c = self._cur
+        self.final[k_lo] = (s.clone(), c.clone(), nwin)
+        return 0
+
+
+def _dense_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2111_04289_b200.dist import TorchDistExchange, exchange_dense
+        h = FakeDenseHandle(rank, k0=-5, k1=7, wmerge=5, K=2000, seed=rank)
+        exchange_dense([h], TorchDistExchange())
+        q.put((rank, {k: (v[0].numpy().tobytes(), v[1].numpy().tobytes()) for k, v in h.sent.items()},
+               {k: (v[0].numpy().tobytes(), v[1].numpy().tobytes(), v[2]) for k, v in h.final.items()}))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_dense_exchange():
+    """exchange_dense: every merge window of the close range (13 instances, windows of 5:
+    k = -5, 0, 5) is SUM-all-reduced over the ranks before the finalize."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_dense_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(world)], key=lambda x: x[0])
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, sent, final in res:
+        assert sorted(final) == [-5, 0, 5] and [final[k][2] for k in (-5, 0, 5)] == [5, 5, 3]
+        for k in (-5, 0, 5):
+            want_s = sum(np.frombuffer(r[1][k][0], np.int64) for r in res)
+            want_c = sum(np.frombuffer(r[1][k][1], np.int64) for r in res)
+            assert np.array_equal(np.frombuffer(final[k][0], np.int64), want_s)
+            assert np.array_equal(np.frombuffer(final[k][1], np.int64), want_c)
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_split_points_record_boundaries(world):
     from paper_2111_04289_b200.dist import split_points

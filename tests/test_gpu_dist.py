@@ -18,7 +18,7 @@ def sharded_run(qname, batches, world, p2p=False, **cfg):
     fam = qname[:2]
     hs = [RankHandle(P.Query(qname, mode="manual", rank=r, world=world, **cfg)) for r in range(world)]
     ex = LocalExchange()
-    if p2p:
+    if p2p and p2p != "dense":
         ex.setup_p2p(hs, device_watermark=p2p == "device")
     outs, t = [], 0.0
     for b in batches + [None]:
@@ -61,6 +61,15 @@ def test_virtual_shards_match_oracle(qname, traffic, world, p2p):
         assert sum(r["late_records"] for r in recs) == o.late
         assert all(r["windows_closed"] == o.windows_closed for r in recs)
         assert all(r["watermark"] == (-1 if o.watermark is None else o.watermark) for r in recs)
+
+
+@pytest.mark.parametrize("qname,traffic,world", [("LR2S", "B(1.7)", 2), ("LR2S", "U(0.8)", 4),
+                                                  ("CM1S", "B(0.9)", 3), ("CM1T", "B(0.7)", 2)])
+def test_virtual_shards_dense_exchange(qname, traffic, world):
+    """Dense exchange (small key sets): per merge window each rank's partial
+    sums / counts as [instances][K] arrays, one SUM all-reduce, rank 0 finalizes — against
+    the oracle (long flushes take several merge windows)."""
+    test_virtual_shards_match_oracle(qname, traffic, world, "dense")
 
 
 @pytest.mark.parametrize("qname,traffic,world", [("LR1S", "B(0.4)", 2), ("LR1S", "U(0.3)", 3), ("LR1T", "B(0.3)", 2)])

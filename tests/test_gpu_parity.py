@@ -121,8 +121,11 @@ def test_device_and_host_segments_mixed():
 def test_many_segments_more_than_one_launch():
     """> 128 borrowed device segments in one batch: several aggregate launches per batch, and
     segment cursors crossing many tiny segments inside one launch."""
-    for fam, qname in (("LR", "LR2S"), ("CM", "CM2S")):
-        data = stream(fam, "B(0.02)", 300)
+    for fam, qname in (("LR", "LR2S"), ("CM", "CM2S"), ("LR", "LR1S")):
+        # (LR1: every launch reads the retained-row FIFO's count when it starts and its last CTA
+        # advances it; a segment's tail tile writes hole rows)
+        params = g.LRParams(num_vehicles=150) if qname == "LR1S" else None
+        data = stream(fam, "B(0.02)", 300, params=params)
         batches = [data[:170], data[170:190], data[190:]]
         devmask = [[True] * len(b) for b in batches]
         compare_run(qname, product_run(qname, batches, device_batches=devmask), oracle_rows(qname, batches))
@@ -134,6 +137,8 @@ def test_empty_flush_and_tiny_batches():
     compare_run("CM2S", product_run("CM2S", one), oracle_rows("CM2S", one))
     one = [[g.lr_record(g.SEED, 3, 0)]]
     compare_run("LR2S", product_run("LR2S", one), oracle_rows("LR2S", one))
+    compare_run("LR1S", product_run("LR1S", one), oracle_rows("LR1S", one))
+    compare_run("LR1S", product_run("LR1S", []), oracle_rows("LR1S", []))
 
 
 def test_xways_domain_and_high_key_space():

@@ -24,7 +24,8 @@ def _port():
 
 
 @pytest.mark.parametrize("workload,exchange", [("cm2", "alltoall"), ("lr2", "alltoall"), ("cm2", "p2p"),
-                                               ("lr2", "p2p-async"), ("cm2", "device")])
+                                               ("lr2", "p2p-async"), ("cm2", "device"), ("lr2", "dense"),
+                                               ("cm2", "auto")])
 def test_torchrun_two_ranks(workload, exchange):
     env = dict(os.environ, LMS_DIST_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",

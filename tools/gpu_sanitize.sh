@@ -9,6 +9,9 @@ for tool in memcheck synccheck racecheck; do
     > $OUT/$tool.txt 2>&1
   timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python -m pytest -q -x \
     "tests/test_gpu_dist.py::test_virtual_shards_match_oracle[CM2S-B(1.3)-2-p2p]" \
-    "tests/test_gpu_dist.py::test_virtual_shards_match_oracle[LR2S-B(1.7)-2-alltoall]" >> $OUT/$tool.txt 2>&1
+    "tests/test_gpu_dist.py::test_virtual_shards_match_oracle[LR2S-B(1.7)-2-alltoall]" \
+    "tests/test_gpu_group.py::test_group_parity_streams[LR1S-B(0.4)-40-bs5-2]" \
+    "tests/test_gpu_group.py::test_group_parity_streams[CM1S-B(0.9)-75-bs3-2]" >> $OUT/$tool.txt 2>&1
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python -m pytest -q -x tests/test_gpu_churn.py >> $OUT/$tool.txt 2>&1
   tail -3 $OUT/$tool.txt
 done
