@@ -301,8 +301,11 @@ __device__ __forceinline__ uint32_t lr1_issue(const SegTable& s, const Lr1Iter& 
   if (lane == 0) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bulk) : "memory");
     const uint8_t* src = s.s[it.si].ptr + off;
+    // read-once input: L2 evict-first, so the 700 MB stream does not push the vehicle
+    // dictionary and the live panes' counts out of L2
     if (bulk)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      asm volatile("{\n .reg .b64 pol;\n createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+                   " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
                    ::"r"(dst), "l"(src), "r"(bulk), "r"(bar) : "memory");
     for (uint32_t i = bulk; i < bytes; i++)
       asm volatile("st.shared.u8 [%0], %1;" ::"r"(dst + i), "r"((uint32_t)src[i]));

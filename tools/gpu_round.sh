@@ -3,7 +3,7 @@
 # stream-latency configs and the f3 timelines.
 # Usage (under gpurun): bash tools/gpu_round.sh <tag>
 set -u
-TAG=${1:-r02h}
+TAG=${1:-r02i}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_power_cap --format=csv > $OUT/nvsmi.txt 2>&1
@@ -22,4 +22,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_cl
   for f in 0 4; do echo "== lr1 flags=$f (10M records per batch; batch 5 closes the first instance)"; timeout 300 python tools/prof_batch.py --workload lr1 --batches 7 --records 10000000 --flags $f; done; } > $OUT/kernel_timings_by_kind.txt 2>&1
 timeout 1200 python tools/latency_configs.py --out $OUT/latency_configs.json > $OUT/latency_configs.log 2>&1; tail -6 $OUT/latency_configs.log
 timeout 1500 python tools/f3_dynamics.py --part B --out $OUT/f3_timelines.json > $OUT/f3b.log 2>&1; tail -6 $OUT/f3b.log
+timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; cat $OUT/bench_ref.json
 ls -la $OUT
