@@ -152,6 +152,8 @@ struct QueryDev {
                                 // over `stripes` addresses); the close sums the stripes. Else 1.
   uint32_t* acc_cnt32;          // LR1 [P][K]
   uint32_t* part32;             // LR2 [C][2][2][K]
+  uint32_t lr2_direct;          // LR2: CTAs add their smem tables straight into the pane
+                                // accumulators (RED.64) instead of writing part32 for the close
   unsigned long long* part64;   // CM1 [C][2][2][K]
   unsigned long long* part_tag; // [C][2] (slot << 32 | pane), kEmpty64 = unused
   uint32_t n_agg_ctas;          // C

@@ -328,13 +328,13 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
   // the LAST CTA to arrive (ticket), never by a fixed CTA: finish() rewrites next_k /
   // next_k_valid / ts_min, and a CTA that had not read them yet could otherwise see a torn
   // snapshot (next_k_valid = 1 with a stale next_k) and close instances that do not exist.
-  if (q.kind != kLR2S && !(w.any && w.k_last >= w.nk)) {
+  if ((q.kind != kLR2S || q.lr2_direct) && !(w.any && w.k_last >= w.nk)) {
     if (ticket(st)) finish(q, w);
     return;
   }
 
   // 1. merge LR2 partials of this batch into the pane accumulators (my key slice)
-  if (q.kind == kLR2S) merge_partials(q, k0, k1);
+  if (q.kind == kLR2S && !q.lr2_direct) merge_partials(q, k0, k1);
   __syncthreads();
 
   // 2. emit closing instances

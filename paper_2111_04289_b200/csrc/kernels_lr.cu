@@ -221,7 +221,23 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
     if (tid == 0 && t + kLrStages < t1) lr_issue<false>(a.segs, iss, t + kLrStages, buf, &full[s]);
   }
 
-  {
+  if (q.lr2_direct) {
+    // add this CTA's tables into the pane accumulators (one RED.64 pair per key seen): the
+    // close then has nothing to merge, and a batch that closes no instance skips it entirely
+    __syncthreads();
+    for (int sl = 0; sl < 2; sl++) {
+      const unsigned long long tg = slot_tag[sl];
+      if (tg == kEmpty64 || (uint32_t)(tg >> 32) == kFail32) continue;
+      const size_t gbase = (size_t)(uint32_t)(tg >> 32) * K;
+      for (uint32_t k = tid; k < K; k += blockDim.x) {
+        const uint32_t cv = tcnt[sl * K + k];
+        if (cv) {
+          atomicAdd(&q.acc_sum[gbase + k], (unsigned long long)tsum[sl * K + k]);
+          atomicAdd(&q.acc_cnt[gbase + k], (unsigned long long)cv);
+        }
+      }
+    }
+  } else {
     __syncthreads();
     // write this CTA's pane partials: overwrite on the batch's first launch (the tag was
     // empty when loaded), accumulate when an earlier launch of the same batch wrote the slot

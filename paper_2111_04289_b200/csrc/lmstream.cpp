@@ -11,6 +11,7 @@
 #include <array>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <algorithm>
@@ -1212,6 +1213,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       Q_TRY(q->dalloc(&d.acc_cnt, (size_t)q->P * d.stripes * d.K, 0));
     }
     if (q->kind == kLR2S) {
+      d.lr2_direct = std::getenv("LMS_LR2_PARTIALS") == nullptr ? 1u : 0u;   // (A/B switch)
       Q_TRY(q->dalloc(&d.part32, (size_t)d.n_agg_ctas * 4 * d.K, 0));
       Q_TRY(q->dalloc(&d.part_tag, (size_t)d.n_agg_ctas * 2, 0xFF));
     } else {
