@@ -570,6 +570,35 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
         }
       }
     }
+    // warp-aggregated appends, item-major so that every store instruction writes consecutive
+    // rows: one atomic per warp and iteration on each cursor
+    uint32_t em[kLr1Items], km[kLr1Items], ne = 0, nk = 0;
+#pragma unroll
+    for (int i = 0; i < kLr1Items; i++) {
+      em[i] = __ballot_sync(0xffffffffu, emit >> i & 1u);
+      km[i] = __ballot_sync(0xffffffffu, keep >> i & 1u);
+      ne += __popc(em[i]); nk += __popc(km[i]);
+    }
+    // CTA-wide appends: warp totals -> thread 0 -> one atomic per cursor per CTA and iteration
+    // (per-warp atomics on the two global cursors were the probe's main serialisation)
+    const uint32_t warp = threadIdx.x >> 5;
+    if (lane == 0) s_wtot[warp] = ne | (nk << 16);          // <= 32 * kLr1Items rows each per warp
+    __syncthreads();
+    // thread 0 reserves the CTA's rows; the reservations' latency overlaps the gathers below
+    // (their results are only needed by the stores)
+    unsigned long long res_rows = 0;
+    uint32_t res_fifo = 0;
+    if (threadIdx.x == 0) {
+      uint32_t e_acc = 0, k_acc = 0;
+      for (uint32_t wi = 0; wi < blockDim.x / 32u; wi++) {
+        const uint32_t t = s_wtot[wi];
+        s_woff[wi] = e_acc | (k_acc << 16);
+        e_acc += t & 0xFFFFu;
+        k_acc += t >> 16;
+      }
+      res_rows = e_acc ? atomicAdd(&st->rows, (unsigned long long)e_acc) : 0ull;
+      res_fifo = k_acc ? atomicAdd(&st->fifo_count[cur ^ 1u], k_acc) : 0u;
+    }
     // multiplicity: the vehicle's count over the instance's panes.  Common case: the window
     // counts k_lr1_wcache precomputed — one L2 load per row, all items' loads back to back.
     // Otherwise the row sums its instance's pane counts itself (cached slots or table lookups).
@@ -598,31 +627,7 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_lr1(const CloseArgs a) 
 #pragma unroll
     for (int i = 0; i < kLr1Items; i++)
       veh[i] = (emit >> i & 1u) ? (q.lr1_dense ? (unsigned long long)r[i].vidx : __ldcg(&q.dict.key_by_idx[r[i].vidx])) : 0ull;
-    // warp-aggregated appends, item-major so that every store instruction writes consecutive
-    // rows: one atomic per warp and iteration on each cursor
-    uint32_t em[kLr1Items], km[kLr1Items], ne = 0, nk = 0;
-#pragma unroll
-    for (int i = 0; i < kLr1Items; i++) {
-      em[i] = __ballot_sync(0xffffffffu, emit >> i & 1u);
-      km[i] = __ballot_sync(0xffffffffu, keep >> i & 1u);
-      ne += __popc(em[i]); nk += __popc(km[i]);
-    }
-    // CTA-wide appends: warp totals -> thread 0 -> one atomic per cursor per CTA and iteration
-    // (per-warp atomics on the two global cursors were the probe's main serialisation)
-    const uint32_t warp = threadIdx.x >> 5;
-    if (lane == 0) s_wtot[warp] = ne | (nk << 16);          // <= 32 * kLr1Items rows each per warp
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t e_acc = 0, k_acc = 0;
-      for (uint32_t wi = 0; wi < blockDim.x / 32u; wi++) {
-        const uint32_t t = s_wtot[wi];
-        s_woff[wi] = e_acc | (k_acc << 16);
-        e_acc += t & 0xFFFFu;
-        k_acc += t >> 16;
-      }
-      s_rbase = e_acc ? atomicAdd(&st->rows, (unsigned long long)e_acc) : 0ull;
-      s_fbase = k_acc ? atomicAdd(&st->fifo_count[cur ^ 1u], k_acc) : 0u;
-    }
+    if (threadIdx.x == 0) { s_rbase = res_rows; s_fbase = res_fifo; }
     __syncthreads();
     const uint32_t wo = s_woff[warp];
     unsigned long long rbase = s_rbase + (wo & 0xFFFFu);
