@@ -187,3 +187,41 @@ def test_online_infpt_regression_in_the_loop():
     assert len(fitted) > 10
     assert all(0 <= r["opt_block_s"] < 1.0 for r in recs)
     assert recs[0]["opt_overhead_s"] == 0 and recs[0]["opt_block_s"] == 0
+
+
+@pytest.mark.parametrize("qname,fam,traffic", [("LR2S", "LR", "R(0.02,20)"), ("CM2S", "CM", "R(0.01,2)"),
+                                              ("LR1S", "LR", "R(0.02,20)"), ("CM1S", "CM", "R(0.01,2)")])
+def test_batch_plan_labels_match_oracle_planner(qname, fam, traffic):
+    """Alg. 2 labels of every micro-batch (report-only): the record's plan_mask /
+    n_cpu_ops / n_gpu_ops equal the oracle planner's MapDevice on the query's DAG with
+    Part = batch bytes / NumCores and the batch's InfPT — batch sizes spanning the 150 KB
+    inflection point (both device labels occur), also with the online Eq. 10 InfPT."""
+    import paper_2111_04289_b200 as P
+    from oracle import planner as PL
+    from paper_2111_04289_b200 import _lib as L
+    params = g.LRParams(num_vehicles=200) if qname == "LR1S" else None
+    secs = [d for _, d in g.stream_datasets(fam, traffic, 40, seed=3, params=params)]
+    sizes = [1, 1, 2, 5, 9, 13, 9]
+    seen = set()
+    for flags in (0, L.LMS_FLAG_ONLINE_INFPT):
+        with P.Query(qname, mode="manual", flags=flags) as q:
+            t, i = 0.0, 0
+            for n in sizes:
+                for d in secs[i:i + n]:
+                    q.push(d, t)
+                    t += 1.0
+                i += n
+                q.force(t)
+                q.sync(ok=(L.LMS_OK, L.LMS_EFORMAT))
+            recs = q.records()
+        dag = PL.dag_for(qname)
+        for r in recs:
+            if r["batch_bytes"] == 0:
+                continue
+            want = PL.map_device(dag, r["batch_bytes"] / 12.0, r["inf_pt_bytes"], PL.BASE_TRANS_COST)
+            mask = sum(1 << o for o, dv in enumerate(want) if dv == PL.GPU)
+            assert r["plan_mask"] == mask, (r["batch_bytes"], r["inf_pt_bytes"], r["plan_mask"], want)
+            assert r["n_gpu_ops"] == sum(1 for dv in want if dv == PL.GPU)
+            assert r["n_cpu_ops"] == sum(1 for dv in want if dv == PL.CPU)
+            seen.add(mask)
+    assert len(seen) >= 2        # the sizes straddle the inflection point: both labellings occur
