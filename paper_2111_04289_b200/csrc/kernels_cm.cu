@@ -481,6 +481,24 @@ __device__ __forceinline__ uint32_t swar4d(uint32_t d) {
 // so the fast path never rejects anything itself.  sb / e: mask bits of the record start and
 // of its '\n' (sb <= 4096).  Every smem address stays inside the stage (see `ec`), so that
 // predicated-off garbage positions cannot fault.
+// The exact general path for a record the fast path did not accept (other field shapes,
+// malformed lines), out of line: it is rare, and kept out of the hot loop's instruction
+// footprint.  Values come back in registers (no address of the caller's record escapes).
+struct CmSlow {
+  uint32_t ok, ts, event, cat, cpu_m, job_lo, job_hi;
+};
+__device__ __noinline__ CmSlow cm_slow(const uint8_t* buf, const uint32_t* cm32, uint32_t sb, uint32_t e,
+                                       uint32_t hi_bits) {
+  CmRec r{};
+  const int st = e == 0xFFFFu ? 2 : cm_parse(buf, cm32, sb, e, hi_bits, r);
+  const bool ok = st == 2 ? cm_parse_serial(buf, kCmHaloL + sb, hi_bits + kCmHaloL, r) : st != 0;
+  CmSlow o;
+  o.ok = ok ? 1u : 0u;
+  o.ts = r.ts; o.event = r.event; o.cat = r.cat; o.cpu_m = r.cpu_m;
+  o.job_lo = (uint32_t)r.job; o.job_hi = (uint32_t)(r.job >> 32);
+  return o;
+}
+
 template <bool kLazy>
 // buf_s / cm_s: shared-window addresses of the stage and of the warp's comma mask words.
 __device__ __forceinline__ bool cm_fast(uint32_t buf_s, uint32_t cm_s, uint32_t sb, uint32_t e, CmRec& r) {
@@ -784,13 +802,14 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       bool ok = fast;
       if (__any_sync(0xffffffffu, slow)) {
         if (slow) {
-          const int st = e == 0xFFFFu ? 2 : cm_parse(buf, cm32, sb, e, hi_bits, r);
-          ok = st == 2 ? cm_parse_serial(buf, kCmHaloL + sb, hi_bits + kCmHaloL, r) : st != 0;
+          const CmSlow o = cm_slow(buf, cm32, sb, e, hi_bits);
+          ok = o.ok != 0;
+          r.ts = o.ts; r.event = o.event; r.cat = o.cat; r.cpu_m = o.cpu_m;
           if (kCM2) {                  // values, not digit words (cm_job_value / cm_cpu_value)
-            r.jw0 = (uint32_t)r.job;
-            r.jw1 = (uint32_t)(r.job >> 32);
+            r.jw0 = o.job_lo;
+            r.jw1 = o.job_hi;
             r.jw2 = 0;
-            r.cw0 = r.cpu_m;
+            r.cw0 = o.cpu_m;
             r.cw1 = kRawValues;
           }
         }
