@@ -386,3 +386,100 @@ def close_lr1(handles, exchange) -> list[int]:
     for h in handles:
         h.run_close()
     return [h.sync() for h in handles]
+
+
+# ----------------------------------------------------------------------------- admission
+
+class DistAdmission:
+    """Alg. 1 / CG(dN) for micro-batches partitioned across ranks.
+
+    Every dataset arrives once and is split at record boundaries (lms_split): each rank
+    registers its own partition with push(ingest_s, local_bytes), in the same order on every
+    rank.  poll(now) sums the partitions' bytes over the ranks (one SUM all-reduce), rank 0
+    judges the GLOBAL datasets with the library's Alg. 1 (lms_admit_decision: Eq. 6 EstMaxLat
+    against SlideTime / the deadline / the mean past MaxLat) and broadcasts its decision, so
+    every rank admits the same datasets at the same poll and then forces its partition
+    (lms_force_batch).  complete(proc_local): a partitioned batch completes when its slowest
+    partition does, so Proc is the MAX over ranks; rank 0's Eq. 4 (AvgThPut: global bytes over
+    the running Proc sum) and Eq. 5 (MaxLat = max Buff + Proc) history drives the next poll.
+    mode: L.LMS_MODE_LMSTREAM or L.LMS_MODE_DEADLINE (CG(dN): SlideTime := N, d0 tumbling)."""
+
+    def __init__(self, mode: int, slide_s: float = 0.0, deadline_s: float = 0.0, group=None):
+        import torch.distributed as dist
+        if mode not in (L.LMS_MODE_LMSTREAM, L.LMS_MODE_DEADLINE):
+            raise ValueError("DistAdmission runs Alg. 1 (LMS_MODE_LMSTREAM / LMS_MODE_DEADLINE)")
+        self.dist, self.group = dist, group
+        self.rank = dist.get_rank(group)
+        self.dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+        self.mode, self.slide_s, self.deadline_s = mode, float(slide_s), float(deadline_s)
+        self.buffered = []          # [(ingest_s, global bytes, local bytes)] judged, not admitted
+        self.new = []               # [(ingest_s, local bytes)] since the last poll
+        self.bytes_hist, self.proc_sum, self.maxlat_hist = 0, 0.0, []
+        self.in_flight = None       # (admit time, [(ingest_s, global bytes, local bytes)])
+        self.last_proc = float("nan")   # Proc of the last completed batch (max over ranks)
+
+    @property
+    def avg_thput(self) -> float:
+        """Eq. 4 over the completed batches (0 before the first: bootstrap)."""
+        return self.bytes_hist / self.proc_sum if self.proc_sum > 0 else 0.0
+
+    def push(self, ingest_s: float, local_bytes: int):
+        self.new.append((float(ingest_s), int(local_bytes)))
+
+    def poll(self, now: float):
+        """-> (admitted, n_datasets, est_max_lat, reason); the same on every rank."""
+        import torch
+        if self.in_flight is not None:
+            return False, 0, float("nan"), -2
+        new, self.new = self.new, []
+        if new:                                   # global bytes of the new partitions
+            t = torch.tensor([b for _, b in new], dtype=torch.int64, device=self.dev)
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+            glob = [int(x) for x in t.cpu().tolist()]
+            # Alg. 1: tmp = buffered U new, new sorted by creation time (stable: arrival order)
+            order = sorted(range(len(new)), key=lambda i: new[i][0])
+            self.buffered += [(new[i][0], glob[i], new[i][1]) for i in order]
+        dec = torch.zeros(3, dtype=torch.float64, device=self.dev)
+        if self.rank == 0:
+            admit, est, reason = self._decide(now)
+            dec[0], dec[1], dec[2] = float(admit), est, float(reason)
+        self.dist.broadcast(dec, src=0, group=self.group)
+        d = dec.cpu().tolist()
+        admitted, est, reason = bool(d[0]), d[1], int(d[2])
+        if not admitted:
+            return False, 0, est, reason
+        batch, self.buffered = self.buffered, []
+        self.in_flight = (float(now), batch)
+        return True, len(batch), est, reason
+
+    def _decide(self, now: float):
+        n = len(self.buffered)
+        ing = (C.c_double * max(1, n))(*[x for x, _, _ in self.buffered])
+        byt = (C.c_uint64 * max(1, n))(*[b for _, b, _ in self.buffered])
+        hist = (C.c_double * max(1, len(self.maxlat_hist)))(*self.maxlat_hist)
+        admit, est, reason = C.c_int32(), C.c_double(), C.c_int32()
+        check(L.lms_admit_decision(self.mode, self.slide_s, self.deadline_s, float(now), ing, byt, n,
+                                   self.avg_thput, hist, len(self.maxlat_hist), C.byref(admit),
+                                   C.byref(est), C.byref(reason)), "lms_admit_decision")
+        return admit.value, est.value, reason.value
+
+    @property
+    def in_flight_local_bytes(self) -> int:
+        """This rank's bytes of the admitted, not yet completed batch (its partition)."""
+        return sum(b for _, _, b in self.in_flight[1]) if self.in_flight else 0
+
+    def complete(self, proc_local: float) -> float:
+        """The in-flight batch finished on this rank after proc_local seconds: Proc = max over
+        ranks; returns the batch's MaxLat (Eq. 5)."""
+        import torch
+        now, batch = self.in_flight
+        self.in_flight = None
+        t = torch.tensor([float(proc_local)], dtype=torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        proc = float(t.cpu().item())
+        self.last_proc = proc
+        self.bytes_hist += sum(b for _, b, _ in batch)
+        self.proc_sum += proc
+        ml = max(now - x for x, _, _ in batch) + proc
+        self.maxlat_hist.append(ml)
+        return ml

@@ -318,3 +318,116 @@ def test_gloo_world2_p2p_setup_and_passes():
         assert imported == [0, 1]
         assert calls == [("push", 10, 2), ("fin", 10, 2), ("push", 12, 1), ("fin", 12, 1),
                          ("push", 12, 1), ("fin", 12, 1)]   # + the remainder after an async pass
+
+
+# ----------------------------------------------------------------------------- Alg. 1 / CG(dN) across ranks
+
+def _adm_arrivals(seed, n, world):
+    """Datasets every 0.25 s (B-shaped traffic with jitter), 0.2-3 MB each, split unevenly
+    over the ranks (each rank's partition size = its share of the record-boundary split)."""
+    import random
+    rng = random.Random(seed)
+    out = []
+    for i in range(n):
+        tot = rng.randrange(200_000, 3_000_000)
+        cuts = sorted(rng.randrange(0, tot + 1) for _ in range(world - 1))
+        parts = [b - a for a, b in zip([0] + cuts, cuts + [tot])]
+        out.append((round(0.25 * i + rng.uniform(0, 0.2), 6), tot, parts))
+    return out
+
+
+def _adm_proc(rank, local_bytes):
+    """Deterministic per-rank Proc model: fixed overhead + bytes / rank speed (rank 1 slower)."""
+    return 0.03 + local_bytes / (4e6 if rank == 0 else 3e6)
+
+
+def _adm_worker(rank, world, port, q, mode, slide, dl, arr, t_end):
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import math
+
+        from paper_2111_04289_b200.dist import DistAdmission
+        adm = DistAdmission(mode, slide_s=slide, deadline_s=dl)
+        out, nxt, tick, last = [], 0, 0, int(math.floor(t_end / 0.01 + 1e-9))
+        while tick <= last:
+            now = tick * 0.01
+            while nxt < len(arr) and arr[nxt][0] <= now + 1e-12:
+                adm.push(arr[nxt][0], arr[nxt][2][rank])
+                nxt += 1
+            ok, n, est, reason = adm.poll(now)
+            if not ok:
+                tick += 1
+                continue
+            proc_local = _adm_proc(rank, adm.in_flight_local_bytes)
+            ml = adm.complete(proc_local)
+            out.append((now, n, est, reason, ml, adm.avg_thput))
+            proc = max(_adm_proc(r, sum(a[2][r] for a in arr[sum(o[1] for o in out[:-1]):sum(o[1] for o in out)]))
+                       for r in range(world))
+            tick = max(tick + 1, int(math.ceil((now + proc) / 0.01 - 1e-9)))
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode_name,slide,dl", [("deadline", 0.0, 1.0), ("deadline", 0.0, 0.0),
+                                                ("lmstream", 5.0, 0.0)])
+def test_gloo_world2_alg1_partitioned(mode_name, slide, dl):
+    """CG(d1), CG(d0) and LMStream's sliding branch for micro-batches partitioned over two ranks
+    (P:417): rank 0 decides on the global datasets (bytes summed over the ranks) and
+    broadcasts; Proc = max over ranks.  Both ranks must take exactly the decisions of the
+    oracle's Admission driver fed the global datasets and the max-over-ranks Proc."""
+    import math
+
+    from oracle import sizer as Z
+    from paper_2111_04289_b200 import _lib as L
+    world, t_end = 2, 20.0
+    arr = _adm_arrivals(11, 70, world)
+    mode = L.LMS_MODE_DEADLINE if mode_name == "deadline" else L.LMS_MODE_LMSTREAM
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_adm_worker, args=(r, world, port, q, mode, slide, dl, arr, t_end))
+          for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    def nan_free(rows):
+        return [tuple(None if isinstance(x, float) and math.isnan(x) else x for x in r) for r in rows]
+    assert nan_free(res[0]) == nan_free(res[1]), "ranks took different decisions"
+    # oracle mirror: global datasets, Proc = max over ranks of the same per-rank model
+    adm = Z.Admission(mode_name, slide_s=slide, deadline_s=dl)
+    want, nxt, tick, last, done = [], 0, 0, int(math.floor(t_end / 0.01 + 1e-9)), 0
+    while tick <= last:
+        now = tick * 0.01
+        while nxt < len(arr) and arr[nxt][0] <= now + 1e-12:
+            adm.push(Z.Dataset(nxt, arr[nxt][0], arr[nxt][1]))
+            nxt += 1
+        d = adm.poll(now)
+        if not d.admitted:
+            tick += 1
+            continue
+        ids = [x.id for x in d.batch]
+        assert ids == list(range(done, done + len(ids)))
+        done += len(ids)
+        proc = max(_adm_proc(r, sum(arr[i][2][r] for i in ids)) for r in range(world))
+        ml = adm.complete(proc)
+        want.append((now, len(ids), d.est_max_lat, d.reason, ml, adm.avg_thput))
+        tick = max(tick + 1, int(math.ceil((now + proc) / 0.01 - 1e-9)))
+    got = res[0]
+    assert len(got) == len(want) and len(want) >= 5
+    reasons = {"bootstrap": 1, "slide": 2, "tumbling": 2, "tumbling-bootstrap": 3, "cap": 4}
+    for g_, w in zip(got, want):
+        assert g_[0] == w[0] and g_[1] == w[1]
+        assert g_[3] == reasons[w[3]], (g_, w)
+        if w[2] is None:
+            assert math.isnan(g_[2])
+        else:
+            assert g_[2] == pytest.approx(w[2], rel=1e-12)
+        assert g_[4] == pytest.approx(w[4], rel=1e-12)
+        assert g_[5] == pytest.approx(w[5], rel=1e-12)
+    if mode_name == "deadline" and dl > 0:
+        assert sum(w[3] == "slide" for w in want) >= 5
