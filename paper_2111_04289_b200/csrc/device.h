@@ -154,6 +154,8 @@ struct QueryDev {
   uint32_t* part32;             // LR2 [C][2][2][K]
   uint32_t lr2_direct;          // LR2: CTAs add their smem tables straight into the pane
                                 // accumulators (RED.64) instead of writing part32 for the close
+  uint32_t lr2_flush_tiles;     // LR2: a CTA adds its u32 tables into the accumulators every this
+                                // many tiles (8192: a u32 sum cannot wrap)
   unsigned long long* part64;   // CM1 [C][2][2][K]
   unsigned long long* part_tag; // [C][2] (slot << 32 | pane), kEmpty64 = unused
   uint32_t n_agg_ctas;          // C

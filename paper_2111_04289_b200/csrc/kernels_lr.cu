@@ -12,8 +12,10 @@
 // every word load is aligned and bank-conflict free: word stride 35 is odd), validates all
 // 70 bytes per record with SWAR range checks, parses the decoded fields from registers.
 // LR2: native u32 shared-memory atomics into a per-CTA table [2 pane slots][K keys]
-// (K = 200 * num_xways), written once per CTA to a partials array that the close kernel
-// merges per key slice (no global atomics on the hot path).  LR1 (k_lr1_agg below): warp-owned
+// (K = 200 * num_xways); at the end (and every q.lr2_flush_tiles tiles, so that a u32 sum cannot
+// wrap) the CTA adds its tables into the u64 pane accumulators, one RED.64 pair per key seen
+// (no global atomics per record).  LMS_LR2_PARTIALS=1 (A/B only) keeps round 1's per-CTA
+// partials merged by the close.  LR1 (k_lr1_agg below): warp-owned
 // 64-record tiles, dictionary-mapped (or dense) vehicle counts per pane (global REDs) and the
 // projection of a 16 B row into the retained FIFO at deterministic positions.
 #include "common.cuh"
@@ -126,6 +128,24 @@ __device__ __forceinline__ void lr_issue(const SegTable& segs, SegCursor& c, uns
   }
 }
 
+// Add the CTA's [2 panes][K] u32 tables into the u64 pane accumulators (one RED.64 pair per
+// key seen) and, if `zero`, clear them for further records.
+__device__ __forceinline__ void lr2_add_tables(const QueryDev& q, const unsigned long long* slot_tag, uint32_t* tsum,
+                                               uint32_t* tcnt, uint32_t K, int tid, bool zero) {
+  for (int sl = 0; sl < 2; sl++) {
+    const unsigned long long tg = slot_tag[sl];
+    if (tg == kEmpty64 || (uint32_t)(tg >> 32) == kFail32) continue;
+    const size_t gbase = (size_t)(uint32_t)(tg >> 32) * K;
+    for (uint32_t k = tid; k < K; k += blockDim.x) {
+      const uint32_t cv = tcnt[sl * K + k];
+      if (cv) {
+        atomicAdd(&q.acc_sum[gbase + k], (unsigned long long)tsum[sl * K + k]);
+        atomicAdd(&q.acc_cnt[gbase + k], (unsigned long long)cv);
+        if (zero) { tsum[sl * K + k] = 0; tcnt[sl * K + k] = 0; }
+      }
+    }
+  }
+}
 template <int KIND>
 __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   static_assert(KIND == kLR2S, "LR1 runs k_lr1_agg");
@@ -161,6 +181,7 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
   const unsigned long long wm_prev = q.state->wm_prev;
   CtaCounters cnt{0, 0, 0, 0, kEmpty32, 0};
   uint32_t c_pane = kEmpty32, c_slot = 0, c_gslot = kFail32;   // cached slots of the last pane seen
+  uint32_t tiles_since_flush = 0;
 
   for (unsigned long long t = t0; t < t1; t++) {
     const int s = (int)((t - t0) % kLrStages);
@@ -219,24 +240,20 @@ __global__ void __launch_bounds__(kLrThreads, 2) k_lr_agg(const LrArgs a) {
     }
     __syncthreads();   // stage s fully consumed
     if (tid == 0 && t + kLrStages < t1) lr_issue<false>(a.segs, iss, t + kLrStages, buf, &full[s]);
+    // bound the u32 tables (CTA-uniform): q.lr2_flush_tiles (<= 8192) tiles of 512 records at
+    // speed <= 999 stay below 2^32
+    if (++tiles_since_flush == q.lr2_flush_tiles && t + 1 < t1) {
+      lr2_add_tables(q, slot_tag, tsum, tcnt, K, tid, true);
+      tiles_since_flush = 0;
+      __syncthreads();
+    }
   }
 
   if (q.lr2_direct) {
     // add this CTA's tables into the pane accumulators (one RED.64 pair per key seen): the
     // close then has nothing to merge, and a batch that closes no instance skips it entirely
     __syncthreads();
-    for (int sl = 0; sl < 2; sl++) {
-      const unsigned long long tg = slot_tag[sl];
-      if (tg == kEmpty64 || (uint32_t)(tg >> 32) == kFail32) continue;
-      const size_t gbase = (size_t)(uint32_t)(tg >> 32) * K;
-      for (uint32_t k = tid; k < K; k += blockDim.x) {
-        const uint32_t cv = tcnt[sl * K + k];
-        if (cv) {
-          atomicAdd(&q.acc_sum[gbase + k], (unsigned long long)tsum[sl * K + k]);
-          atomicAdd(&q.acc_cnt[gbase + k], (unsigned long long)cv);
-        }
-      }
-    }
+    lr2_add_tables(q, slot_tag, tsum, tcnt, K, tid, false);
   } else {
     __syncthreads();
     // write this CTA's pane partials: overwrite on the batch's first launch (the tag was

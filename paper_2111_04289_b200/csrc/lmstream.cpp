@@ -1214,6 +1214,9 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     }
     if (q->kind == kLR2S) {
       d.lr2_direct = std::getenv("LMS_LR2_PARTIALS") == nullptr ? 1u : 0u;   // (A/B switch)
+      d.lr2_flush_tiles = 8192u;   // 8192 tiles * 512 records * speed <= 999 < 2^32
+      if (const char* f = std::getenv("LMS_LR2_FLUSH_TILES"))   // test hook: exercise the flush
+        d.lr2_flush_tiles = std::max(1u, std::min(8192u, (uint32_t)std::strtoul(f, nullptr, 10)));
       Q_TRY(q->dalloc(&d.part32, (size_t)d.n_agg_ctas * 4 * d.K, 0));
       Q_TRY(q->dalloc(&d.part_tag, (size_t)d.n_agg_ctas * 2, 0xFF));
     } else {

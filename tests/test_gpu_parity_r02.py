@@ -150,3 +150,20 @@ def test_push_pinned_equals_push():
     compare_run("CM2S", got, oracle_rows("CM2S", batches))
     for (gr, _, _), (wr, _, _) in zip(got, want):
         assert sorted(map(bytes, gr)) == sorted(map(bytes, wr))
+
+
+_LR2_FLUSH = {}
+
+
+@pytest.mark.parametrize("flush_tiles", [1, 3])
+def test_lr2_periodic_table_flush(monkeypatch, flush_tiles):
+    """LR2 aggregate CTAs add their u32 [pane][key] tables into the u64 accumulators every
+    lr2_flush_tiles tiles (8192 by default, so that a u32 sum cannot wrap at any batch size);
+    LMS_LR2_FLUSH_TILES forces the period down to 1 / 3 tiles, so every CTA flushes several
+    times inside one launch.  Results must equal the oracle's."""
+    monkeypatch.setenv("LMS_LR2_FLUSH_TILES", str(flush_tiles))
+    data = [d for _, d in g.stream_datasets("LR", "B(30)", 36, seed=23)]    # 3e4 records/s
+    batches = [data[i:i + 12] for i in range(0, len(data), 12)]             # ~700 tiles / 296 CTAs
+    if "ora" not in _LR2_FLUSH:
+        _LR2_FLUSH["ora"] = oracle_rows("LR2S", batches)
+    compare_run("LR2S", product_run("LR2S", batches), _LR2_FLUSH["ora"])
