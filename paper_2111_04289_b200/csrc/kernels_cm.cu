@@ -725,6 +725,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     const uint32_t ph = (it >> 1) & 1u;
     const uint32_t geo = s ? geo1 : geo0;
     const uint32_t st_s = stage_s + s * (uint32_t)kCmStage;    // stage base (shared window)
+    const uint8_t* buf = wsmem + s * kCmStage;
     mbar_wait_s(full_s + 8u * s, ph);                           // every lane: TMA bytes visible
     __syncwarp();                                               // lane 0's remainder bytes (tail tiles)
     const uint32_t hi_bits = geo_hibits(geo);                   // mask bits beyond are invalid
@@ -751,7 +752,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     if (fresh) {                                 // (warp-uniform)
       if (lane < 8) mword(lane);
       // a record starts at payload byte 0 iff the tile starts its segment or follows a '\n'
-      carry_nl = geo_start(geo) || lds_u8(st_s + kCmHaloL - 1) == '\n';
+      carry_nl = geo_start(geo) || buf[kCmHaloL - 1] == '\n';
     }
     __syncwarp();
     if (hi_bits < (uint32_t)kMaskBits) {        // segment tail (warp-uniform): clear stale bits
@@ -801,7 +802,7 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
       bool ok = fast;
       if (__any_sync(0xffffffffu, slow)) {
         if (slow) {
-          const CmSlow o = cm_slow(wsmem + s * kCmStage, cm32, sb, e, hi_bits);
+          const CmSlow o = cm_slow(buf, cm32, sb, e, hi_bits);
           ok = o.ok != 0;
           r.ts = o.ts; r.event = o.event; r.cat = o.cat; r.cpu_m = o.cpu_m;
           if (kCM2) {                  // values, not digit words (cm_job_value / cm_cpu_value)
@@ -917,14 +918,13 @@ __global__ void __launch_bounds__(kCmThreads, kCtasPerSm) k_cm_agg(const CmArgs 
     }
     __syncwarp();      // stage s and the masks consumed by every lane
     fresh = !geo_cont(geo);
-    // halo masks = the next tile's window bits [0, 256), copied by lanes 24..31: the same lanes
-    // write mask words 128..135 in the next tile's pass 1, so program order keeps the copy's
-    // reads ahead of those writes (no second warp barrier)
-    if (!fresh && lane >= 24) {
-      const uint32_t j = (uint32_t)lane - 24u;
-      sts32(nl_s + 4 * j, lds32(nl_s + 4 * (kChunks * 4 + j)));
-      sts32(cm_s + 4 * j, lds32(cm_s + 4 * (kChunks * 4 + j)));
+    if (!fresh && lane < 8) {                   // halo masks = the next tile's window bits [0, 256)
+      sts32(nl_s + 4 * lane, lds32(nl_s + 4 * (kChunks * 4 + lane)));
+      sts32(cm_s + 4 * lane, lds32(cm_s + 4 * (kChunks * 4 + lane)));
     }
+    // lanes 24..31 write mask words 128..135 in the next tile's pass 1 (each lane leaves the
+    // barrier wait on its own): the halo reads above must be done first
+    __syncwarp();
     if (it + kCmStages < ntiles) {
       const uint32_t g2 = cm_issue(iss, st_s, full_s + 8u * s, lane);
       iss.next(a.segs);
