@@ -195,12 +195,31 @@ class Runner:
                 return n
 
 
-def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p, scaling):
-    """Throughput: K timed micro-batches, inputs resident in HBM (generated before timing)."""
-    inputs = [(*gen_second_dev(wl, t, seed, rank, world, scaling, torch), t) for t in range(warmup + steps)]
+FILL_DIVISOR = 50   # window-fill batches carry 1/50 of a step's records
+
+
+def fill_window(run, wl, seed, rank, world, scaling, torch, t_end, sync):
+    """Untimed window fill: the R seconds before t_end as small micro-batches (every key of the
+    workload still appears in every pane), so that the measured batches run in steady state —
+    every pane of the window live, closes summing R/S panes — not while the window fills."""
+    R = int(round(run.q.cfg.range_s))
+    small = dict(wl, records=max(1, wl["records"] // FILL_DIVISOR))
+    for t in range(t_end - R, t_end):
+        buf, n = gen_second_dev(small, t, seed, rank, world, scaling, torch)
+        run.q.push_device(buf.data_ptr(), n, float(t))
+        run.batch(t, sync=True)
+        del buf
+    return R
+
+
+def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p, scaling, t0=100):
+    """Throughput: K timed micro-batches, inputs resident in HBM (generated before timing), after
+    an untimed window fill (seconds t0 - R .. t0 - 1) and W warm-up batches."""
+    inputs = [(*gen_second_dev(wl, t, seed, rank, world, scaling, torch), t) for t in range(t0, t0 + warmup + steps)]
     torch.cuda.synchronize()
     run = Runner(wl, rank, world, torch, p2p, pipeline=True, cap=1 << 20)
     q = run.q
+    nfill = fill_window(run, wl, seed, rank, world, scaling, torch, t0, sync=True)
     out = {"agg_s": [], "close_s": [], "batch_s": [], "rows": 0}
     for i in range(warmup):
         buf, n, t = inputs[i]
@@ -236,7 +255,7 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p, scaling):
     out["launches"] = q.kernel_launches() - launches0
     out["clocks"] = clk.summary()
     out["bytes_per_step"] = statistics.mean(n for _, n, _ in inputs[warmup:])
-    recs = [q.record(i) for i in range(warmup, warmup + steps)]
+    recs = [q.record(nfill + i) for i in range(warmup, warmup + steps)]
     out["records"] = sum(r["num_records"] for r in recs)
     out["bad"] = sum(r["bad_records"] for r in recs)
     q.close()
@@ -251,6 +270,7 @@ def latency_run(wl, n_batches, seed, rank, world, torch, dist, p2p, scaling, t0=
     batch's device time).  N > 1: per batch the max over ranks."""
     run = Runner(wl, rank, world, torch, p2p, pipeline=False, cap=1 << 20)
     q = run.q
+    fill_window(run, wl, seed, rank, world, scaling, torch, t0, sync=True)
     dev_s, agg_s = [], []
     for i in range(n_batches + 3):
         buf, n = gen_second_dev(wl, t0 + i, seed, rank, world, scaling, torch)
@@ -660,7 +680,10 @@ def main():
                        "batch_bytes_per_gpu": res["bytes_per_step"],
                        "parallelism": (f"dp{world} (row partition per rank, {scaling} scaling; exchange: {args.exchange})"
                                        if world > 1 else "single GPU"),
-                       "l2": "inputs (>= 0.7 GB/step) exceed the 126 MB L2; no flush needed"},
+                       "l2": "inputs (>= 0.7 GB/step) exceed the 126 MB L2; no flush needed",
+                       "window": "steady state: an untimed fill of the R seconds before the first warm-up batch "
+                                 f"(1/{FILL_DIVISOR} of a step's records per second) leaves every pane of the "
+                                 "window live, so closing batches sum R/S panes"},
             "roofline": roofline(res["bytes_per_step"], agg_avg, pk,
                                  "k_cm_agg<CM2S> (framing+decode+filter+aggregate)" if wl["family"] == "CM"
                                  else "k_lr_agg<LR2S>", ncu_traffic(args.workload)),

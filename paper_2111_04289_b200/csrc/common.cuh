@@ -85,6 +85,15 @@ __device__ __forceinline__ long long floor_div(long long a, long long b) {
   return q;
 }
 
+// floor(a / S) through the pane magic (pane_of: exact for 0 <= a < 2^32, and for negative a by
+// floor(a / S) = -1 - floor((-a - 1) / S)); anything else: the 64-bit division.  Window ranges
+// are floor_div_S of watermark / ts differences: no 64-bit division on the close's latency path.
+__device__ __forceinline__ long long floor_div_S(long long a, uint32_t S, unsigned long long magic) {
+  if (a >= 0 && a < (1ll << 32)) return (long long)pane_of((uint32_t)a, S, magic);
+  if (a < 0 && a > -(1ll << 32)) return -(long long)pane_of((uint32_t)(-a - 1), S, magic) - 1;
+  return floor_div(a, (long long)S);
+}
+
 __device__ __forceinline__ unsigned long long fmix64(unsigned long long k) {
   k ^= k >> 33;
   k *= 0xff51afd7ed558ccdull;

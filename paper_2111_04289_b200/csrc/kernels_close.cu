@@ -24,6 +24,7 @@ namespace lms {
 namespace {
 
 constexpr int kCloseThreads = 256;
+constexpr int kCloseThreadsCm2 = 1024;  // k_close_agg for CM2S: 32 warps over (pane, stripe) pairs
 constexpr int kMaxPartEntries = 1024;   // 2 * aggregate CTAs
 constexpr int kMaxG = 4;                // distinct pane slots merged in smem per batch
 constexpr int kMaxSlice = 64;           // keys per close CTA (LR2: 200 * xways / 148 <= 22)
@@ -47,8 +48,8 @@ __device__ __forceinline__ WinRange win_range(const QueryDev& q, int flush) {
   w.any = true;
   const long long W = (long long)wm - 1;
   if (st->next_k_valid) w.nk = st->next_k;
-  else w.nk = floor_div((long long)st->ts_min - (long long)q.R, (long long)q.S) + 1;
-  w.k_last = flush ? floor_div(W, (long long)q.S) : floor_div(W - (long long)q.R, (long long)q.S);
+  else w.nk = floor_div_S((long long)st->ts_min - (long long)q.R, q.S, q.div_magic) + 1;
+  w.k_last = floor_div_S(flush ? W : W - (long long)q.R, q.S, q.div_magic);
   return w;
 }
 
@@ -312,16 +313,98 @@ __device__ void merge_partials(const QueryDev& q, uint32_t k0, uint32_t k1) {
   }
 }
 
-__global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) {
+// Shared-memory u64 accumulation as two native u32 atomics (a 64-bit shared atomicAdd is a CAS
+// loop): the carry out of the low word is added to the high word by the add that produced it.
+__device__ __forceinline__ void smem_add64(uint32_t* lo, uint32_t* hi, unsigned long long v) {
+  if (v == 0) return;
+  const uint32_t vl = (uint32_t)v, old = atomicAdd(lo, vl);
+  atomicAdd(hi, (uint32_t)(v >> 32) + (old + vl < old ? 1u : 0u));
+}
+
+// CM2 emission of instance k for keys [k0, k1): a key's accumulators are spread over
+// q.stripes copies per pane (the aggregate's striped RED.64s), so one thread per key would walk
+// ppw * stripes loads one round trip at a time (~400 per key at R/S = 12, 16 stripes: a closing
+// batch's close took ~60 us).  The CM2 close runs 1024-thread CTAs: the CTA takes its keys 64
+// at a time, lane l of warp w holds keys base + l and base + 32 + l and walks the (pane,
+// stripe) pairs w, w + W, ... of the instance (coalesced over keys, 4 independent loads per
+// pair, unrolled), the warps' partial sums meet in shared memory (u32-pair atomics), and
+// threads 0..63 emit one key each.
+__device__ __forceinline__ void close_striped(const QueryDev& q, const WinRange& w, long long k, uint32_t k0, uint32_t k1,
+                                              const uint32_t* wslots, bool reclaim, lms_agg_row* rows) {
+  constexpr uint32_t KB = 64;
+  __shared__ uint32_t r_lo[4][KB], r_hi[4][KB];              // sum, count, first-pane count, next-pane count
+  DevState* st = q.state;
+  const uint32_t W = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool last = reclaim && k == w.k_last;
+  const uint32_t ssh = __ffs(q.stripes) - 1, smask = q.stripes - 1;   // stripes: a power of two
+  const uint32_t npairs = q.ppw << ssh;
+  const uint32_t gx = wslots[q.ppw];                           // the pane after the instance
+  for (uint32_t kb = k0; kb < k1; kb += KB) {
+    for (uint32_t i = threadIdx.x; i < 4 * KB; i += blockDim.x) { (&r_lo[0][0])[i] = 0; (&r_hi[0][0])[i] = 0; }
+    __syncthreads();
+    const uint32_t key0 = kb + lane, key1 = kb + 32 + lane;
+    const bool v0 = key0 < k1, v1 = key1 < k1;
+    unsigned long long s0 = 0, c0 = 0, f0 = 0, x0 = 0, s1 = 0, c1 = 0, f1 = 0, x1 = 0;
+#pragma unroll 4
+    for (uint32_t pr = warp; pr < npairs; pr += W) {
+      const uint32_t j = pr >> ssh, g = wslots[j];
+      const bool u = g != kEmpty32;
+      const size_t gi = ((size_t)g * q.stripes + (pr & smask)) * q.K;
+      const unsigned long long a0 = (u && v0) ? q.acc_sum[gi + key0] : 0ull, n0 = (u && v0) ? q.acc_cnt[gi + key0] : 0ull;
+      const unsigned long long a1 = (u && v1) ? q.acc_sum[gi + key1] : 0ull, n1 = (u && v1) ? q.acc_cnt[gi + key1] : 0ull;
+      s0 += a0; c0 += n0; s1 += a1; c1 += n1;
+      if (j == 0) { f0 += n0; f1 += n1; }
+    }
+    if (last && gx != kEmpty32)
+      for (uint32_t sp = warp; sp < q.stripes; sp += W) {
+        const size_t gi = ((size_t)gx * q.stripes + sp) * q.K;
+        if (v0) x0 += q.acc_cnt[gi + key0];
+        if (v1) x1 += q.acc_cnt[gi + key1];
+      }
+    smem_add64(&r_lo[0][lane], &r_hi[0][lane], s0);
+    smem_add64(&r_lo[1][lane], &r_hi[1][lane], c0);
+    smem_add64(&r_lo[2][lane], &r_hi[2][lane], f0);
+    smem_add64(&r_lo[3][lane], &r_hi[3][lane], x0);
+    smem_add64(&r_lo[0][32 + lane], &r_hi[0][32 + lane], s1);
+    smem_add64(&r_lo[1][32 + lane], &r_hi[1][32 + lane], c1);
+    smem_add64(&r_lo[2][32 + lane], &r_hi[2][32 + lane], f1);
+    smem_add64(&r_lo[3][32 + lane], &r_hi[3][32 + lane], x1);
+    __syncthreads();
+    if (threadIdx.x < KB) {
+      const uint32_t i = threadIdx.x, key = kb + i;
+      const unsigned long long s = ((unsigned long long)r_hi[0][i] << 32) | r_lo[0][i];
+      const unsigned long long c = ((unsigned long long)r_hi[1][i] << 32) | r_lo[1][i];
+      const unsigned long long cf = ((unsigned long long)r_hi[2][i] << 32) | r_lo[2][i];
+      const unsigned long long cx = ((unsigned long long)r_hi[3][i] << 32) | r_lo[3][i];
+      // the last closing instance decides key eviction: after this close the live panes are
+      // k_last + 1 .. k_last + ppw (the watermark is below (k_last + 1) S + R)
+      const bool dead = last && key < k1 && (c - cf) + cx == 0;
+      const bool want = key < k1 && c > 0;
+      const double sum = (double)s / 1e6;                     // SUM(cpu) from the exact fixed-point sum (R20)
+      const double avg = want ? sum / (double)c : 0.0;
+      const unsigned long long pos = row_slot(st, want);
+      if (want) {
+        if (pos < q.row_cap) {
+          lms_agg_row r;
+          r.win_start_s = k * (long long)q.S;
+          r.win_end_s = r.win_start_s + (long long)q.R;
+          r.count = c; r.sum_fixed = s; r.sum = sum; r.avg = avg; r.rank = 0;
+          r.key = q.dict.key_by_idx[key]; r.key_xway = r.key_dir = r.key_seg = 0;
+          rows[pos] = r;
+        } else {
+          atomicExch(&st->row_overflow, 1u);
+        }
+      }
+      if (dead) reclaim_key(q, key);                          // (after its row: the row reads key_by_idx)
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kCloseThreadsCm2) k_close_agg(const CloseArgs a) {
   const QueryDev& q = a.q;
   DevState* st = q.state;
   const WinRange w = win_range(q, a.flush);
-  const uint32_t K = (q.kind == kCM2S) ? min(st->n_keys, q.K) : q.K;
-  const uint32_t k0 = (uint32_t)((unsigned long long)K * blockIdx.x / gridDim.x);
-  const uint32_t k1 = (uint32_t)((unsigned long long)K * (blockIdx.x + 1) / gridDim.x);
-  const uint32_t P = q.P;
-  __shared__ uint32_t wslots[257];   // R/S <= 256, + the pane after the instance
-  const bool reclaim = q.kind == kCM2S && q.world == 1;
 
   // Most batches close no window (slide S > batch span): nothing to merge (CM: the aggregate
   // pass wrote the pane accumulators directly), emit or evict.  The state is still advanced by
@@ -332,6 +415,13 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
     if (ticket(st)) finish(q, w);
     return;
   }
+
+  const uint32_t K = (q.kind == kCM2S) ? min(st->n_keys, q.K) : q.K;
+  const uint32_t k0 = (uint32_t)((unsigned long long)K * blockIdx.x / gridDim.x);
+  const uint32_t k1 = (uint32_t)((unsigned long long)K * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t P = q.P;
+  __shared__ uint32_t wslots[257];   // R/S <= 256, + the pane after the instance
+  const bool reclaim = q.kind == kCM2S && q.world == 1;
 
   // 1. merge LR2 partials of this batch into the pane accumulators (my key slice)
   if (q.kind == kLR2S && !q.lr2_direct) merge_partials(q, k0, k1);
@@ -382,7 +472,11 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
         }
         continue;
       }
-      // LR2 / CM2: one thread per key of my slice
+      if (q.stripes > 1) {   // CM2: the 16 stripes of a key split over the CTA's warps
+        close_striped(q, w, k, k0, k1, wslots, reclaim, rows);
+        continue;
+      }
+      // LR2 (one stripe): one thread per key of my slice
       for (uint32_t kb = k0; kb < k1; kb += blockDim.x) {
         const uint32_t key = kb + threadIdx.x;
         unsigned long long s = 0, c = 0, c_first = 0;
@@ -456,10 +550,14 @@ __global__ void __launch_bounds__(kCloseThreads) k_close_agg(const CloseArgs a) 
     }
     __syncthreads();
     const uint32_t nev = s_nev;
+    // (key, stripe) pairs over the whole CTA: warp w zeroes stripes w, w + W, ... of the slice
+    // (one stripe: every thread over the keys, as before)
+    const uint32_t W = q.stripes > 1 ? blockDim.x / 32 : 1, wid = q.stripes > 1 ? threadIdx.x >> 5 : 0;
+    const uint32_t t0 = q.stripes > 1 ? (threadIdx.x & 31) : threadIdx.x, tn = q.stripes > 1 ? 32 : blockDim.x;
     for (uint32_t i = 0; i < nev; i++) {
       const size_t g = s_ev[i];
-      for (uint32_t sp = 0; sp < q.stripes; sp++)
-        for (uint32_t k = kk0 + threadIdx.x; k < kk1; k += blockDim.x) {
+      for (uint32_t sp = wid; sp < q.stripes; sp += W)
+        for (uint32_t k = kk0 + t0; k < kk1; k += tn) {
           q.acc_sum[(g * q.stripes + sp) * q.K + k] = 0;
           q.acc_cnt[(g * q.stripes + sp) * q.K + k] = 0;
         }
@@ -872,7 +970,7 @@ cudaError_t launch_close(const QueryDev& q, int flush, cudaStream_t st) {
     if (q.lr1_wc != nullptr && q.world == 1) k_lr1_wcache<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
     k_close_lr1<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
   }
-  else k_close_agg<<<close_ctas(q), kCloseThreads, 0, st>>>(a);
+  else k_close_agg<<<close_ctas(q), q.kind == kCM2S ? kCloseThreadsCm2 : kCloseThreads, 0, st>>>(a);
   return cudaGetLastError();
 }
 

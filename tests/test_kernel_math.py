@@ -67,3 +67,28 @@ def test_ts_shift_decode_all_lengths():
             bad |= (x | ((x + 0x76767676) & 0xFFFFFFFF)) & 0x80808080
         assert bad == 0
         assert swar4d(lo) * 10000 + swar4d(hi) == int(txt)
+
+
+def floor_div_S(a, S):
+    # common.cuh floor_div_S: pane_of's magic ceil(2^64 / S) (lmstream.cpp: ~0 / S + 1),
+    # umul64hi for 0 <= a < 2^32, -1 - floor((-a - 1) / S) for -2^32 < a < 0
+    magic = ((2 ** 64 - 1) // S) + 1 if S > 1 else 0
+
+    def pane_of(ts):
+        return ts if S == 1 else (ts * magic) >> 64
+
+    if 0 <= a < 2 ** 32:
+        return pane_of(a)
+    if -(2 ** 32) < a < 0:
+        return -pane_of(-a - 1) - 1
+    return a // S
+
+
+def test_floor_div_S_is_floor_division():
+    rng = random.Random(11)
+    for S in list(range(1, 70)) + [300, 3600, 86400, 2 ** 20, 2 ** 31 - 1, 2 ** 31]:
+        cases = [0, 1, -1, S - 1, S, -S, -S - 1, 2 ** 32 - 1, -(2 ** 32) + 1, 2 ** 32, -(2 ** 32) - 5]
+        cases += [q * S + r for q in (-3, -1, 1, 7, (2 ** 32 - 1) // S) for r in (-1, 0, 1)]
+        cases += [rng.randrange(-(2 ** 32) + 1, 2 ** 32) for _ in range(300)]
+        for a in cases:
+            assert floor_div_S(a, S) == a // S, (S, a)
