@@ -26,6 +26,7 @@ The oracle (oracle/) runs only in the cpu_baseline leg and the --impl reference 
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -169,7 +170,8 @@ class Runner:
         self.q = make_query(wl, rank, world, pipeline, cap, torch)
         self.world = world
         self.p2p = p2p
-        self.rowbuf = np.zeros(1 << 16, P.AGG_DTYPE)      # caller-owned result buffer (pages touched)
+        self.rowbuf = np.zeros(1 << 16, P.AGG_DTYPE)      # caller-owned result buffer
+        self.rowbuf.view(np.uint8)[:] = 1                 # (pages touched: np.zeros maps them lazily)
         if world > 1:
             from paper_2111_04289_b200.dist import RankHandle, TorchDistExchange
             self.h, self.ex = RankHandle(self.q), TorchDistExchange()
@@ -230,6 +232,8 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p, scaling, 
     launches0 = q.kernel_launches()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dev = torch.cuda.current_device()
+    gc.collect()
+    gc.disable()                                     # no collector pause inside the timed steps
     with ClockSampler(dev) as clk:
         if world > 1:
             dist.barrier()
@@ -251,6 +255,7 @@ def device_run(wl, steps, warmup, seed, rank, world, torch, dist, p2p, scaling, 
         if world > 1:
             dist.barrier()
         clk.mark(False)
+    gc.enable()
     out["elapsed_s"] = e0.elapsed_time(e1) / 1e3
     out["launches"] = q.kernel_launches() - launches0
     out["clocks"] = clk.summary()

@@ -124,8 +124,9 @@ typedef struct {
 
 #define LMS_FLAG_ONLINE_INFPT 0x1u  /* Eq. 10 online regression of InfPT */
 #define LMS_FLAG_PIPELINE     0x2u  /* single GPU: lms_force_batch may launch batch i+1 while
-                                       batch i still runs (two batches in flight, separate
-                                       report / row buffers); lms_sync and reads complete
+                                       batches i, i-1 still run (up to three batches in flight,
+                                       separate report / row buffers; the oldest is completed
+                                       when a fourth is launched); lms_sync and reads complete
                                        them in order.  Stream order keeps window state exact. */
 #define LMS_FLAG_NVLS         0x8u  /* num_gpus > 1, LR2S / CM1*: merge the dense partial tables
                                        through NVLink-switch multicast (NVLS, multimem.red) when

@@ -43,12 +43,16 @@ struct WinRange {
 __device__ __forceinline__ WinRange win_range(const QueryDev& q, int flush) {
   const DevState* st = q.state;
   WinRange w{0, -1, false};
+  // the four state words in one round trip (no load behind a branch on another)
   const unsigned long long wm = st->wm;
+  const uint32_t nk_valid = st->next_k_valid;
+  const unsigned long long ts_min = st->ts_min;
+  const long long next_k = st->next_k;
   if (wm == 0) return w;
   w.any = true;
   const long long W = (long long)wm - 1;
-  if (st->next_k_valid) w.nk = st->next_k;
-  else w.nk = floor_div_S((long long)st->ts_min - (long long)q.R, q.S, q.div_magic) + 1;
+  if (nk_valid) w.nk = next_k;
+  else w.nk = floor_div_S((long long)ts_min - (long long)q.R, q.S, q.div_magic) + 1;
   w.k_last = floor_div_S(flush ? W : W - (long long)q.R, q.S, q.div_magic);
   return w;
 }

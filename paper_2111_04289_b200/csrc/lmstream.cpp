@@ -143,8 +143,9 @@ struct lms_query {
   RefitWorker refit;               // Eq. 10 refit off the batch path
   Dag dag;
   // in-flight batches: slot `cur_slot` holds the newest batch (in_flight), and with
-  // LMS_FLAG_PIPELINE the other slot may hold the previous, still running one (parked), so the
-  // host prepares and launches batch i+1 while the GPU runs batch i
+  // LMS_FLAG_PIPELINE up to kPipeDepth - 1 older slots hold earlier, still running batches
+  // (parked, oldest = cur_slot - n_parked), so the host prepares and launches batch i+1 while
+  // the GPU runs batches i, i-1: a host stall shorter than two batches does not idle the GPU
   struct Flight {
     lms_batch_record cur{};
     int in_buf = 0;
@@ -155,10 +156,11 @@ struct lms_query {
     BatchReport* d_report = nullptr;
     void* d_rows = nullptr;            // result rows of this batch
   };
-  Flight fl[2];
+  static constexpr int kPipeDepth = 3;
+  Flight fl[kPipeDepth];
   int cur_slot = 0;
   bool pipeline = false;
-  bool parked = false;
+  int n_parked = 0;
   bool in_flight = false;
   bool awaiting_close = false;     // multi-GPU: aggregate pass launched, close not yet
   bool p2p_async_pending = false;  // fused exchange enqueued behind the close (lms_p2p_collect)
@@ -500,11 +502,17 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
   return st;
 }
 
-// Complete the oldest in-flight batch (the parked one first).
+// Slot of the oldest parked batch.
+int oldest_parked(const lms_query* q) {
+  return (q->cur_slot - q->n_parked + lms_query::kPipeDepth) % lms_query::kPipeDepth;
+}
+
+// Complete the oldest in-flight batch (the parked ones first, oldest first).
 lms_status complete(lms_query* q) {
-  if (q->parked) {
-    q->parked = false;
-    return complete_flight(q, q->fl[q->cur_slot ^ 1]);
+  if (q->n_parked > 0) {
+    const int sl = oldest_parked(q);
+    q->n_parked--;
+    return complete_flight(q, q->fl[sl]);
   }
   if (!q->in_flight) return LMS_OK;
   q->in_flight = false;
@@ -522,9 +530,29 @@ lms_status take_deferred(lms_query* q, lms_status s) {
 
 // Complete every in-flight batch (oldest first); the first error wins.
 lms_status complete_all(lms_query* q) {
-  lms_status a = complete(q);
-  lms_status b = complete(q);
-  return take_deferred(q, a ? a : b);
+  lms_status a = LMS_OK;
+  while (q->n_parked > 0 || q->in_flight) {
+    const lms_status b = complete(q);
+    a = a ? a : b;
+  }
+  return take_deferred(q, a);
+}
+
+// Pipelined handles: complete the parked batches (oldest first) until none still reads
+// staging buffer `buf` (a host push is about to refill it); a format / overflow status is
+// deferred to the next call.
+bool parked_uses(const lms_query* q, int buf) {
+  for (int i = 1; i <= q->n_parked; i++)
+    if (q->fl[(q->cur_slot - i + lms_query::kPipeDepth) % lms_query::kPipeDepth].in_buf == buf) return true;
+  return false;
+}
+lms_status release_staging(lms_query* q, int buf) {
+  while (q->n_parked > 0 && parked_uses(q, buf)) {
+    const lms_status c = complete(q);
+    if (c && c != LMS_EFORMAT && c != LMS_EOVERFLOW) return c;
+    if (c && !q->deferred_status) { q->deferred_status = c; q->deferred_msg = g_err; }
+  }
+  return LMS_OK;
 }
 
 // Pipelined launch (LMS_FLAG_PIPELINE): park the running batch in its slot and switch to the
@@ -532,10 +560,10 @@ lms_status complete_all(lms_query* q) {
 lms_status park_current(lms_query* q) {
   if (!q->in_flight) return LMS_OK;
   lms_status s = LMS_OK;
-  if (q->parked) s = complete(q);
-  q->parked = true;
+  if (q->n_parked == lms_query::kPipeDepth - 1) s = complete(q);   // the oldest slot is reused
+  q->n_parked++;
   q->in_flight = false;
-  q->cur_slot ^= 1;
+  q->cur_slot = (q->cur_slot + 1) % lms_query::kPipeDepth;
   return s;
 }
 
@@ -1141,7 +1169,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     QC_TRY(cudaStreamCreateWithFlags(&q->copy_stream, cudaStreamNonBlocking));
     // pipelining (two batches in flight) only for single-GPU handles
     q->pipeline = (cfg->flags & LMS_FLAG_PIPELINE) && cfg->world == 1;
-    const int nslots = q->pipeline ? 2 : 1;
+    const int nslots = q->pipeline ? lms_query::kPipeDepth : 1;
     for (int sl = 0; sl < nslots; sl++) {
       lms_query::Flight& f = q->fl[sl];
       for (cudaEvent_t* e : {&f.ev_admit, &f.ev_start, &f.ev_agg, &f.ev_close, &f.ev_end}) QC_TRY(cudaEventCreate(e));
@@ -1295,11 +1323,10 @@ lms_status lms_push(lms_query* q, const void* bytes, uint64_t nbytes, double t, 
     if (!is_lr(q->kind) && static_cast<const uint8_t*>(bytes)[nbytes - 1] != '\n')
       return fail(LMS_EINVAL, "CM dataset does not end with a newline");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
-    // pipelined: the staging buffer may still feed the parked (previous) batch
-    if (q->parked && q->fl[q->cur_slot ^ 1].in_buf == q->in_cur) {
-      lms_status c = complete(q);
-      if (c && c != LMS_EFORMAT && c != LMS_EOVERFLOW) return c;
-      if (c && !q->deferred_status) { q->deferred_status = c; q->deferred_msg = g_err; }
+    // pipelined: the staging buffer may still feed a parked (earlier) batch
+    if (q->n_parked > 0) {
+      const lms_status c = release_staging(q, q->in_cur);
+      if (c) return c;
     }
     const int b = q->in_cur;
     if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
@@ -1332,10 +1359,9 @@ lms_status lms_push_pinned(lms_query* q, const void* bytes, uint64_t nbytes, dou
     if (!is_lr(q->kind) && static_cast<const uint8_t*>(bytes)[nbytes - 1] != '\n')
       return fail(LMS_EINVAL, "CM dataset does not end with a newline");
     CUDA_TRY(cudaSetDevice(q->cfg.device));
-    if (q->parked && q->fl[q->cur_slot ^ 1].in_buf == q->in_cur) {   // (see lms_push)
-      lms_status c = complete(q);
-      if (c && c != LMS_EFORMAT && c != LMS_EOVERFLOW) return c;
-      if (c && !q->deferred_status) { q->deferred_status = c; q->deferred_msg = g_err; }
+    if (q->n_parked > 0) {                                            // (see lms_push)
+      const lms_status c = release_staging(q, q->in_cur);
+      if (c) return c;
     }
     const int b = q->in_cur;
     if (q->in_used[b] + nbytes > q->in_cap) return fail(LMS_EOVERFLOW, "batch buffer full (max_batch_bytes)");
@@ -1383,7 +1409,10 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
     if (!q->subs.empty()) return group_poll(q, now, admitted, bidx);
     CUDA_TRY(cudaSetDevice(q->cfg.device));
     lms_status cs = LMS_OK;
-    if (q->parked) cs = complete(q);                  // (pipelined handles polled: drain)
+    while (q->n_parked > 0) {                         // (pipelined handles polled: drain)
+      const lms_status c = complete(q);
+      cs = cs ? cs : c;
+    }
     if (q->poisoned) return fail(LMS_ESTATE, "handle poisoned by a failed fused exchange");
     cs = take_deferred(q, cs);
     if (q->in_flight) {

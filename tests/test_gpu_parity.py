@@ -268,7 +268,7 @@ def _pipelined_run(qname, batches, device_mask):
 @pytest.mark.parametrize("qname,traffic", [("CM2S", "B(1.3)"), ("LR2S", "U(0.6)"), ("CM1S", "B(0.9)"),
                                            ("LR1S", "B(0.4)")])
 def test_pipelined_batches_equal_serial(qname, traffic):
-    """LMS_FLAG_PIPELINE (two batches in flight, per-slot report / row buffers, staging-buffer
+    """LMS_FLAG_PIPELINE (up to three batches in flight, per-slot report / row buffers, staging-buffer
     guard for host pushes) gives the same rows and batch records as the serial path, which the
     other tests hold to the oracle."""
     import numpy as np

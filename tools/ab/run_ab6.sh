@@ -1,0 +1,20 @@
+OUT=gpurun_out/ab6; mkdir -p $OUT
+LIB=paper_2111_04289_b200/liblmstream.so
+for v in D L1 L2 D L1 L2; do cp tools/ab/liblmstream_$v.so $LIB
+  for f in 0 4; do echo "== $v flags=$f"; timeout 300 python tools/prof_batch.py --workload lr1 --batches 7 --records 10000000 --flags $f | tail -5; done
+done > $OUT/lr1_ab.txt 2>&1
+python - $OUT/lr1_ab.txt <<'PY'
+import re, sys, collections
+cur, d = None, collections.defaultdict(list)
+for ln in open(sys.argv[1]):
+    if ln.startswith("=="): cur = ln.split()[1:]; continue
+    m = re.search(r"rows (\d+), batch [0-9.]+ ms agg ([0-9.]+) ms close ([0-9.]+) ms", ln)
+    if m and cur: d[tuple(cur)].append((float(m.group(2)), float(m.group(3)), int(m.group(1))))
+for k, v in sorted(d.items()):
+    a = sorted(x[0] for x in v if x[2] == 0)
+    print(k, "agg median %.4f min %.4f n=%d" % (a[len(a)//2], a[0], len(a)))
+PY
+cp tools/ab/liblmstream_L2.so $LIB
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r02.py tests/test_gpu_churn.py tests/test_gpu_dist.py tests/test_gpu_group.py -q -x -k "LR1 or lr1" > $OUT/pytest_L2.txt 2>&1; tail -2 $OUT/pytest_L2.txt
+cp tools/ab/liblmstream_L1.so $LIB
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_r02.py tests/test_gpu_churn.py -q -x -k "LR1 or lr1" > $OUT/pytest_L1.txt 2>&1; tail -2 $OUT/pytest_L1.txt
