@@ -151,7 +151,12 @@ struct lms_query {
     int in_buf = 0;
     bool h2d_async = false;            // its staging buffer was filled by lms_push_pinned
     bool flush = false;
-    cudaEvent_t ev_admit = nullptr, ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr, ev_end = nullptr;
+    cudaEvent_t ev_admit = nullptr, ev_start = nullptr, ev_agg = nullptr, ev_close = nullptr;
+    // the batch's device-time start: ev_start only when a wait on an asynchronous H2D sits
+    // between admission and the kernels, otherwise the admission event itself (one event record
+    // fewer per batch); ev_close also marks the batch's end (nothing is enqueued after it)
+    cudaEvent_t start() const { return start_is_admit ? ev_admit : ev_start; }
+    bool start_is_admit = false;
     BatchReport* h_report = nullptr;   // mapped pinned
     BatchReport* d_report = nullptr;
     void* d_rows = nullptr;            // result rows of this batch
@@ -218,7 +223,7 @@ struct lms_query {
       if (e) cudaEventDestroy(e);
     for (Flight& f : fl) {
       if (f.h_report) cudaFreeHost(f.h_report);
-      for (cudaEvent_t e : {f.ev_admit, f.ev_start, f.ev_agg, f.ev_close, f.ev_end})
+      for (cudaEvent_t e : {f.ev_admit, f.ev_start, f.ev_agg, f.ev_close})
         if (e) cudaEventDestroy(e);
     }
     if (h_count) cudaFreeHost(h_count);
@@ -377,15 +382,16 @@ lms_status launch_batch(lms_query* q, double now, int32_t reason, double est, bo
   q->F().h2d_async = q->h2d_pending[buf];
   // Proc (reading R18) runs from admission: an asynchronous H2D still in flight is part of it
   CUDA_TRY(cudaEventRecord(q->F().ev_admit, q->stream));
+  q->F().start_is_admit = !q->h2d_pending[buf];
   if (q->h2d_pending[buf]) {        // asynchronous pushes: the kernels wait for their H2D
     CUDA_TRY(cudaStreamWaitEvent(q->stream, q->ev_h2d_end[buf], 0));
     q->h2d_pending[buf] = false;
+    CUDA_TRY(cudaEventRecord(q->F().ev_start, q->stream));
   }
   q->in_cur ^= 1;
   q->in_used[q->in_cur] = 0;
 
   const bool lr = is_lr(q->kind);
-  CUDA_TRY(cudaEventRecord(q->F().ev_start, q->stream));
   if (q->rehash_pending) {          // grid-wide dictionary rebuild asked for by an earlier batch
     CUDA_TRY(launch_dict_rehash(q->qd, q->stream));
     q->launches += 2;
@@ -428,9 +434,9 @@ lms_status launch_close_stage(lms_query* q) {
     CUDA_TRY(launch_bucket(q->qd, q->stream));
     q->launches += 2;
   }
+  // the batch report lives in mapped pinned memory: the close kernel writes it to the host, and
+  // ev_close is the batch's end event too
   CUDA_TRY(cudaEventRecord(q->F().ev_close, q->stream));
-  // the batch report lives in mapped pinned memory: the close kernel writes it to the host
-  CUDA_TRY(cudaEventRecord(q->F().ev_end, q->stream));
   q->awaiting_close = false;
   q->in_flight = true;
   return LMS_OK;
@@ -438,14 +444,14 @@ lms_status launch_close_stage(lms_query* q) {
 
 // Complete the batch of slot f (its end event, report, rows -> host FIFO, Eq. 4/5/10).
 lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
-  CUDA_TRY(cudaEventSynchronize(f.ev_end));
+  CUDA_TRY(cudaEventSynchronize(f.ev_close));
   lms_batch_record& r = f.cur;
   const BatchReport rep = *f.h_report;
   float ms_total = 0, ms_agg = 0, ms_close = 0, ms_end = 0;
-  CUDA_TRY(cudaEventElapsedTime(&ms_total, f.ev_start, f.ev_close));
-  CUDA_TRY(cudaEventElapsedTime(&ms_agg, f.ev_start, f.ev_agg));
+  CUDA_TRY(cudaEventElapsedTime(&ms_total, f.start(), f.ev_close));
+  CUDA_TRY(cudaEventElapsedTime(&ms_agg, f.start(), f.ev_agg));
   CUDA_TRY(cudaEventElapsedTime(&ms_close, f.ev_agg, f.ev_close));
-  CUDA_TRY(cudaEventElapsedTime(&ms_end, f.ev_admit, f.ev_end));
+  CUDA_TRY(cudaEventElapsedTime(&ms_end, f.ev_admit, f.ev_close));
   q->last_batch_s = ms_total * 1e-3;
   q->last_agg_s = ms_agg * 1e-3;
   q->last_close_s = ms_close * 1e-3;
@@ -458,7 +464,7 @@ lms_status complete_flight(lms_query* q, lms_query::Flight& f) {
     const double t0 = now_host();
     // device rows -> (DMA) -> pinned host FIFO
     const uint8_t* src = static_cast<const uint8_t*>(f.d_rows);
-    // on the copy stream: the batch is complete (ev_end), and a pipelined successor may be
+    // on the copy stream: the batch is complete (ev_close), and a pipelined successor may be
     // running on the compute stream — the copy must not queue behind it
     if (is_lr1(q->kind)) {
       CUDA_TRY(q->lr1_rows.reserve(nrows));
@@ -1172,7 +1178,7 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
     const int nslots = q->pipeline ? lms_query::kPipeDepth : 1;
     for (int sl = 0; sl < nslots; sl++) {
       lms_query::Flight& f = q->fl[sl];
-      for (cudaEvent_t* e : {&f.ev_admit, &f.ev_start, &f.ev_agg, &f.ev_close, &f.ev_end}) QC_TRY(cudaEventCreate(e));
+      for (cudaEvent_t* e : {&f.ev_admit, &f.ev_start, &f.ev_agg, &f.ev_close}) QC_TRY(cudaEventCreate(e));
       QC_TRY(cudaHostAlloc((void**)&f.h_report, sizeof(BatchReport), cudaHostAllocMapped));
       std::memset(f.h_report, 0, sizeof(BatchReport));
       QC_TRY(cudaHostGetDevicePointer((void**)&f.d_report, f.h_report, 0));   // zero-copy report
@@ -1416,7 +1422,7 @@ lms_status lms_poll(lms_query* q, double now, int32_t* admitted, uint64_t* bidx)
     if (q->poisoned) return fail(LMS_ESTATE, "handle poisoned by a failed fused exchange");
     cs = take_deferred(q, cs);
     if (q->in_flight) {
-      cudaError_t e = cudaEventQuery(q->F().ev_end);
+      cudaError_t e = cudaEventQuery(q->F().ev_close);
       if (e == cudaErrorNotReady) return cs;        // one micro-batch in flight at a time
       if (e != cudaSuccess) return fail(LMS_ECUDA, cudaGetErrorString(e));
       lms_status c2 = complete(q);

@@ -3,7 +3,7 @@
 # stream-latency configs and the f3 timelines.
 # Usage (under gpurun): bash tools/gpu_round.sh <tag>
 set -u
-TAG=${1:-r02i}
+TAG=${1:-r02j}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.sw_power_cap --format=csv > $OUT/nvsmi.txt 2>&1
@@ -15,6 +15,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cm_agg -s 2 -c 1 -o $OUT/cm2_agg python tools/prof_batch.py --workload cm2 --batches 3 > $OUT/ncu_cm2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lr_agg -s 2 -c 1 -o $OUT/lr2_agg python tools/prof_batch.py --workload lr2 --batches 3 > $OUT/ncu_lr2.log 2>&1
 timeout 600 ncu --set full --clock-control none -k regex:k_close -s 2 -c 1 -o $OUT/lr2_close python tools/prof_batch.py --workload lr2 --batches 3 > $OUT/ncu_lr2c.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_close_agg -s 65 -c 1 -o $OUT/cm2_close python tools/prof_batch.py --workload cm2 --batches 67 --records 2000000 > $OUT/ncu_cm2c.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_lr1_agg -s 3 -c 1 -o $OUT/lr1_agg python tools/prof_batch.py --workload lr1 --batches 5 --records 10000000 --flags 4 > $OUT/ncu_lr1.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_lr1_agg -s 3 -c 1 -o $OUT/lr1_agg_dict python tools/prof_batch.py --workload lr1 --batches 5 --records 10000000 --flags 0 > $OUT/ncu_lr1d.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_close_lr1 -s 5 -c 1 -o $OUT/lr1_close python tools/prof_batch.py --workload lr1 --batches 7 --records 10000000 --flags 4 > $OUT/ncu_lr1c.log 2>&1
