@@ -287,6 +287,43 @@ def test_pipelined_batches_equal_serial(qname, traffic):
     assert [tuple(r[k] for k in keys) for r in recs_p] == [tuple(o[1][k] for k in keys) for o in serial]
 
 
+def test_pipelined_three_deep_staging_and_deferred_status():
+    """LMS_FLAG_PIPELINE with host pushes only (two staging buffers, up to three batches in
+    flight): the pushes of batch i+2 refill the staging buffer batch i read, so they complete
+    batch i first; a batch with malformed lines completed that way reports LMS_EFORMAT from a
+    later call (deferred, never dropped).  Rows and batch records equal the serial run's."""
+    import ctypes as C
+
+    import numpy as np
+    import paper_2111_04289_b200 as P
+    from paper_2111_04289_b200 import _lib as L
+    secs = stream("CM", "B(1.3)", 40, params=g.CMParams(num_jobs=200))
+    batches = split(secs, [3, 2, 4, 1, 3, 5, 2, 3, 4])
+    bad = b"abc,,1234567890,1,x,1,u,2,0,0.100000,0.1,0.1,0\n7,,bad\n"   # non-digit ts; 3 fields
+    batches[1] = [batches[1][0] + bad] + batches[1][1:]
+    serial = product_run("CM2S", batches)
+    statuses = []
+    with P.Query("CM2S", mode="manual", flags=L.LMS_FLAG_PIPELINE) as q:
+        t = 0.0
+        for b in batches:
+            for d in b:
+                arr = np.frombuffer(d, dtype=np.uint8)
+                statuses.append(L.lms_push(q.h, C.c_void_p(arr.ctypes.data), len(d), t, None))
+                t += 1.0
+            statuses.append(L.lms_force_batch(q.h, t, None))
+        statuses.append(L.lms_flush(q.h, t))
+        rows_p = q.read_agg()
+        recs_p = q.records()
+    assert set(statuses) <= {L.LMS_OK, L.LMS_EFORMAT}
+    assert statuses.count(L.LMS_EFORMAT) >= 1, "the malformed batch's status was dropped"
+    assert sum(r["bad_records"] for r in recs_p) == 2
+    rows_s = np.concatenate([o[0] for o in serial])
+    assert sorted(map(bytes, rows_p)) == sorted(map(bytes, rows_s))
+    keys = ("num_records", "num_datasets", "batch_bytes", "windows_closed", "rows_emitted", "late_records",
+            "bad_records", "watermark")
+    assert [tuple(r[k] for k in keys) for r in recs_p] == [tuple(o[1][k] for k in keys) for o in serial]
+
+
 # ---------------------------------------------------------------- capacity limits (degenerate cases)
 
 def _one_batch(qname, data, **cfg):
