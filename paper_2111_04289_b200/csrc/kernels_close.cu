@@ -171,7 +171,10 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
   const bool lr1 = (q.kind == kLR1S || q.kind == kLR1T);
   if (q.kind == kLR2S)
     for (uint32_t i = threadIdx.x; i < 2 * q.n_agg_ctas; i += blockDim.x) q.part_tag[i] = kEmpty64;
-  if (w.any && !lr1) evict_rebuild_cta(q, w.k_last);      // LR1: k_lr1_evict frees the slots
+  // LR1: k_lr1_evict frees the slots.  A batch that closes nothing has nothing to evict: its
+  // k_last is the previous close's, whose panes are gone, and a kept record's pane lies past it
+  // (ts >= the previous watermark) — unless a pane claim failed, which the rebuild retries.
+  if (w.any && !lr1 && (w.k_last >= w.nk || *(volatile uint32_t*)&st->pane_fail)) evict_rebuild_cta(q, w.k_last);
   {   // tombstones above a quarter of the table: rebuild it (LR1: in k_lr1_evict)
     __shared__ int s_rehash;
     if (threadIdx.x == 0) {
@@ -955,7 +958,9 @@ int close_ctas(const QueryDev& q) {
   // LR2: ~3 keys per CTA, so each (key, entry-lane) thread walks only ~7 of the 2C partial
   // entries (the merge is load-latency bound, not bandwidth bound)
   // LR1: the closing probe is load-latency bound (two 256-thread CTAs per SM at its register count)
-  return q.kind == kLR2S ? 4 * nsm : (q.kind == kLR1S || q.kind == kLR1T) ? 4 * nsm : nsm;
+  // (LR2 with direct accumulator adds — the default — has no partials to merge: one CTA per SM,
+  // a quarter of the ticket arrivals of a batch that closes nothing)
+  return q.kind == kLR2S ? (q.lr2_direct ? nsm : 4 * nsm) : (q.kind == kLR1S || q.kind == kLR1T) ? 4 * nsm : nsm;
 }
 
 cudaError_t launch_dict_rehash(const QueryDev& q, cudaStream_t st) {
