@@ -6,12 +6,15 @@
 // as the last instance containing it has been emitted (pane state carried between batches).
 //
 // One launch per micro-batch.  Every CTA owns a slice of the key space and, for that slice,
-//   1. merges the aggregate kernel's per-CTA partial tables into the pane accumulators (LR2):
-//      (partial, key) items spread over all threads, native u32 smem atomics,
+//   1. (LR2 with LMS_LR2_PARTIALS=1 only, an A/B path) merges the aggregate kernel's per-CTA
+//      partial tables into the pane accumulators; by default the aggregate CTAs add directly,
 //   2. emits every instance k in [next_k, k_last] (k_last = floor((W-R)/S), flush:
 //      floor(W/S)): SUM/COUNT over its panes, AVG = SUM/COUNT in fp64, HAVING avg < 40.0
-//      (LR2), ORDER BY SUM(cpu) rank (CM1), one row per non-empty group,
+//      (LR2), ORDER BY SUM(cpu) rank (CM1), one row per non-empty group — CM2's 16 striped
+//      copies per pane are summed by 32 warps over (pane, stripe) pairs (close_striped),
 //   3. zeroes its slice of every pane <= k_last.
+// A batch that closes nothing goes straight to the ticket: one round trip for the window
+// range, the last CTA advances the state and writes the report.
 // The slices are disjoint, so no grid barrier is needed; the last CTA (atomic ticket) frees
 // the evicted pane slots, rebuilds the pane table, advances next_k / the watermark snapshot
 // and writes the batch report.  LR1 instead probes the retained rows of each closing
