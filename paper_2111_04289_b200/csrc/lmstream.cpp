@@ -1257,10 +1257,11 @@ lms_status lms_query_create(const lms_config* cfg, lms_query** out) {
       Q_TRY(q->dalloc(&d.part_tag, (size_t)d.n_agg_ctas * 2, 0xFF));
     }
     if (q->kind == kCM2S || is_lr1(q->kind)) {
-      // open addressing at load factor <= 1/2 (<= 1/4 for LR1, whose default 2^20 vehicle slots
-      // hold ~10^6 live vehicles: one probe per record, and at load 1/2 a quarter of them walk
-      // past the home entry — a 10M-record LR1 batch 0.37 -> 0.30 ms with the 64 MB table)
-      const uint64_t cap = next_pow2((is_lr1(q->kind) ? 4 : 2) * cfg->max_keys);
+      // open addressing at load factor <= 1/4: with the keys near max_keys (LR1's default 2^20
+      // vehicle slots hold ~10^6 live vehicles; CM2 with 10^6 jobIds) a quarter of the probes
+      // walk past the home entry at load 1/2 — a 10M-record LR1 batch 0.37 -> 0.30 ms with the
+      // 64 MB table
+      const uint64_t cap = next_pow2(4 * cfg->max_keys);
       d.dict.cap_mask = cap - 1;
       d.dict.max_keys = (uint32_t)cfg->max_keys;
       Q_TRY(q->dalloc(&d.dict.keys, 2 * cap, 0xFF));   // {key, index} entries of 16 B
