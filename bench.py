@@ -12,7 +12,8 @@ A step = one micro-batch through the whole hot path via the C ABI: push (device-
 input, borrowed), admission, Alg. 2 labels, framing/decode/filter/aggregate kernel, window
 close kernel, batch report + result rows to the host.  `value` = records of all ranks / max
 over ranks of the device-clock time of the K timed steps (CUDA events, synchronize + barrier
-on both sides).  Inputs (1.375 GB / 0.70 GB per step) exceed L2, so no L2 flush is needed.
+on both sides).  Before the warm-up an untimed fill of the window's R seconds (small batches)
+puts the query in steady state: every pane of the window live, closes summing R/S panes.  Inputs (1.375 GB / 0.70 GB per step) exceed L2, so no L2 flush is needed.
 `e2e` = same metric with the inputs in pinned HOST memory: lms_push_pinned (asynchronous H2D,
 the next step's copy overlapping this step's kernels) + batch + rows to host per step.
 Batch latency p50/p99 (nearest rank, lms_percentile) come from a separate loop of >= 200
