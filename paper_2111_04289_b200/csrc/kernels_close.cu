@@ -237,15 +237,18 @@ __device__ void finish(const QueryDev& q, const WinRange& w, bool swap_fifo = tr
     st->vid_range = 0;
     st->ts_min = kEmpty32;
     st->close_ticket = 0;
-    __threadfence();
+    // (no trailing fence: the next kernel on the stream sees these writes, and the host reads
+    // the mapped report after the batch's end event)
   }
 }
 
-__device__ __forceinline__ bool ticket(DevState* st) {
+// The last CTA to arrive returns true.  publish: this CTA wrote global data the last one will
+// read (the fence orders it before the arrival); a CTA that wrote nothing skips the fence.
+__device__ __forceinline__ bool ticket(DevState* st, bool publish = true) {
   __shared__ bool last;
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
+    if (publish) __threadfence();
     last = atomicAdd(&st->close_ticket, 1u) == gridDim.x - 1;
   }
   __syncthreads();
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(kCloseThreadsCm2) k_close_agg(const CloseArgs 
   // next_k_valid / ts_min, and a CTA that had not read them yet could otherwise see a torn
   // snapshot (next_k_valid = 1 with a stale next_k) and close instances that do not exist.
   if ((q.kind != kLR2S || q.lr2_direct) && !(w.any && w.k_last >= w.nk)) {
-    if (ticket(st)) finish(q, w);
+    if (ticket(st, false)) finish(q, w);
     return;
   }
 
