@@ -96,7 +96,10 @@ typedef struct {
   double   inf_pt_bytes;     /* InfPT_0 = 150e3                           */
   double   base_trans_cost;  /* baseTransCost = 0.1                       */
   uint64_t max_batch_bytes;  /* capacity of one micro-batch of host-pushed bytes  */
-  uint64_t max_keys;         /* distinct-key capacity (CM2 jobIds, LR1 vehicles)  */
+  uint64_t max_keys;         /* distinct-key capacity (CM2 jobIds, LR1 vehicles) live in
+                                the window (evicted keys' indices are reused); defaults
+                                2^16 (CM2) / 2^20 (LR1); the key dictionary holds
+                                next_pow2(4 * max_keys) 16 B entries (load <= 1/4)       */
   uint64_t max_result_rows;  /* result rows one batch may emit                    */
   uint32_t pane_slots;       /* distinct live panes (accumulator slots); 0 -> 2*R/S + 64 */
   uint32_t flags;            /* LMS_FLAG_*                                        */
