@@ -53,11 +53,7 @@ e1.record()
 torch.cuda.synchronize()
 el = e0.elapsed_time(e1) / a.steps
 print(f"fill={not a.no_fill} ms/step {el:.4f}", flush=True)
-try:
-    rows = list(enumerate(host))
-except BrokenPipeError:
-    rows = []
-for i, (h, b, ag, c, hp, hf, hd, nr) in rows:
+for i, (h, b, ag, c, hp, hf, hd, nr) in enumerate(host):
     try:
         print(f"step {i}: host {h * 1e3:.3f} ms (push {hp * 1e3:.3f} force {hf * 1e3:.3f} drain {hd * 1e3:.3f}, "
               f"{nr} rows)  batch {b * 1e3:.3f} agg {ag * 1e3:.3f} close {c * 1e3:.3f}")
