@@ -638,7 +638,7 @@ def main():
     sec = None
     if args.secondary and args.secondary != args.workload:
         w2 = WORKLOADS[args.secondary]
-        r2 = device_run(w2, max(5, args.steps // 2), args.warmup, seed, rank, world, torch, dist, exchange_mode(w2),
+        r2 = device_run(w2, args.steps, args.warmup, seed, rank, world, torch, dist, exchange_mode(w2),
                         scaling)
         if world > 1:
             r2["elapsed_s"] = max_over_ranks(r2["elapsed_s"], torch, dist)
