@@ -47,30 +47,40 @@ __host__ __device__ constexpr uint32_t lr_word(int j, bool bias) {
   return v;
 }
 
+// Field decode, SWAR on digit bytes at compile-time offsets of the pair words.  Only records
+// that lr_validate_pair accepted are used, so every field byte is an ASCII digit here.
+// bytes4<B>: bytes [B, B+4) of the pair, first byte in the low byte.
 template <int B>
-__device__ __forceinline__ uint32_t byte_at(const uint32_t (&w)[kPairWords]) {
-  return (w[B >> 2] >> ((B & 3) * 8)) & 0xFFu;
+__device__ __forceinline__ uint32_t bytes4(const uint32_t (&w)[kPairWords]) {
+  if constexpr ((B & 3) == 0) return w[B >> 2];
+  else return __funnelshift_r(w[B >> 2], w[(B >> 2) + 1], (B & 3) * 8);
 }
+// value of 4 digit values (first = most significant): pairs 10*d0+d1, 10*d2+d3 land in bytes 1
+// and 3 of d * 0xA01 (each <= 99: no carries), PRMT moves them to bytes 0 and 2, and
+// (p * (100 << 16 | 1)) >> 16 = 100 * pair0 + pair1 (the same identity as kernels_cm.cu swar4d,
+// checked in tests/test_kernel_math.py)
+__device__ __forceinline__ uint32_t lr_swar4d(uint32_t d) {
+  const uint32_t p = __byte_perm(d * 0xA01u, 0u, 0x4341u);
+  return (p * 0x640001u) >> 16;
+}
+// N <= 4 digits at byte B: the digit values of the field's bytes shifted to the top of the word
+// (zero digits come in below).  Subtracting '0' cannot disturb the field's bytes: a borrow only
+// runs from a non-digit byte toward later (higher) bytes, and the field's bytes come first.
 template <int B, int N>
 __device__ __forceinline__ uint32_t dec_u32(const uint32_t (&w)[kPairWords]) {
-  uint32_t v = 0;
-#pragma unroll
-  for (int i = 0; i < N; i++) {
-    // byte_at with a compile-time index after unrolling
-    const int b = B + i;
-    v = v * 10u + (((w[b >> 2] >> ((b & 3) * 8)) & 0xFFu) - 48u);
-  }
-  return v;
+  static_assert(N >= 1 && N <= 4, "1..4 digits");
+  const uint32_t d = bytes4<B>(w) - 0x30303030u;
+  if constexpr (N == 1) return d & 0xFFu;
+  else return lr_swar4d(d << (8 * (4 - N)));
 }
-template <int B, int N>
-__device__ __forceinline__ unsigned long long dec_u64(const uint32_t (&w)[kPairWords]) {
-  unsigned long long v = 0;
-#pragma unroll
-  for (int i = 0; i < N; i++) {
-    const int b = B + i;
-    v = v * 10ull + (((w[b >> 2] >> ((b & 3) * 8)) & 0xFFu) - 48u);
-  }
-  return v;
+template <int B>
+__device__ __forceinline__ uint32_t dec_u32_6(const uint32_t (&w)[kPairWords]) {   // 6 digits
+  return dec_u32<B, 4>(w) * 100u + dec_u32<B + 4, 2>(w);
+}
+template <int B>
+__device__ __forceinline__ unsigned long long dec_u64_10(const uint32_t (&w)[kPairWords]) {   // 10 digits
+  const uint32_t hi8 = dec_u32<B, 4>(w) * 10000u + dec_u32<B + 4, 4>(w);
+  return (unsigned long long)hi8 * 100ull + dec_u32<B + 8, 2>(w);
 }
 
 struct LrRec {
@@ -81,13 +91,13 @@ struct LrRec {
 template <int BASE, bool NEED_VID>
 __device__ __forceinline__ LrRec lr_decode(const uint32_t (&w)[kPairWords]) {
   LrRec r;
-  r.ts = dec_u32<BASE + 2, 6>(w);
+  r.ts = dec_u32_6<BASE + 2>(w);
   r.speed = dec_u32<BASE + 20, 3>(w);
   r.xway = dec_u32<BASE + 24, 3>(w);
   r.lane = dec_u32<BASE + 28, 1>(w);
   r.dir = dec_u32<BASE + 30, 1>(w);
   r.seg = dec_u32<BASE + 32, 3>(w);
-  r.vid = NEED_VID ? dec_u64<BASE + 9, 10>(w) : 0ull;
+  r.vid = NEED_VID ? dec_u64_10<BASE + 9>(w) : 0ull;
   return r;
 }
 

@@ -92,3 +92,46 @@ def test_floor_div_S_is_floor_division():
         cases += [rng.randrange(-(2 ** 32) + 1, 2 ** 32) for _ in range(300)]
         for a in cases:
             assert floor_div_S(a, S) == a // S, (S, a)
+
+
+def test_lr_pair_field_decode():
+    # kernels_lr.cu lr_decode: a record pair as 35 little-endian words; a field of N <= 4 digits
+    # at byte B = funnel shift of words B // 4, B // 4 + 1 by 8 * (B % 4), minus '0' in every
+    # byte, shifted left by 8 * (4 - N), swar4d; 6 / 10 digits from 4 + 2 / 4 + 4 + 2.  The
+    # bytes after a field are arbitrary (commas, other fields, the next record): random here.
+    import lmsgen as g
+    rng = random.Random(5)
+    data = g.second_bytes("LR", 7, 400, 11)
+    for k in range(0, len(data) - 139, 140):
+        pair = bytearray(data[k:k + 140])
+        w = [int.from_bytes(pair[4 * j:4 * j + 4], "little") for j in range(35)]
+
+        def bytes4(b):
+            lo, hi = w[b // 4], w[b // 4 + 1] if b // 4 + 1 < 35 else 0
+            return ((lo | (hi << 32)) >> (8 * (b % 4))) & 0xFFFFFFFF
+
+        def dec(b, n):
+            d = (bytes4(b) - 0x30303030) & 0xFFFFFFFF
+            return d & 0xFF if n == 1 else swar4d((d << (8 * (4 - n))) & 0xFFFFFFFF)
+
+        for base in (0, 70):
+            rec = pair[base:base + 70].decode()
+            f = rec.rstrip("\n").split(",")
+            assert dec(base + 2, 4) * 100 + dec(base + 6, 2) == int(f[1])                   # Time
+            assert (dec(base + 9, 4) * 10000 + dec(base + 13, 4)) * 100 + dec(base + 17, 2) == int(f[2])   # VID
+            assert dec(base + 20, 3) == int(f[3]) and dec(base + 24, 3) == int(f[4])       # Spd, XWay
+            assert dec(base + 28, 1) == int(f[5]) and dec(base + 30, 1) == int(f[6])       # Lane, Dir
+            assert dec(base + 32, 3) == int(f[7])                                          # Seg
+    # random digit strings at every alignment, arbitrary bytes after them
+    for _ in range(2000):
+        n = rng.randint(1, 4)
+        b = rng.randint(0, 100)
+        digits = "".join(rng.choice("0123456789") for _ in range(n))
+        pair = bytearray(rng.randrange(256) for _ in range(140))
+        pair[b:b + n] = digits.encode()
+        w = [int.from_bytes(pair[4 * j:4 * j + 4], "little") for j in range(35)]
+        lo, hi = w[b // 4], w[b // 4 + 1]
+        x = ((lo | (hi << 32)) >> (8 * (b % 4))) & 0xFFFFFFFF
+        d = (x - 0x30303030) & 0xFFFFFFFF
+        got = d & 0xFF if n == 1 else swar4d((d << (8 * (4 - n))) & 0xFFFFFFFF)
+        assert got == int(digits), (b, n, digits)
